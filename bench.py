@@ -1,0 +1,372 @@
+"""REABK benchmark (BASELINE.json metric) on BASELINE config 2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c1]
+
+A step is one full solve of the workload to ||x - x*|| <= 1e-6 ||x*|| (the
+reference's run(), solvers.py:425-474).  `value` = iterations/s with A, b,
+x* resident in HBM (rebk_run_device); `e2e` = the same metric through the
+public API `paper_2001_04179_b200.run(problem, config)` from pinned host
+buffers, re-uploading A every step.  Multi-GPU: C2 does not shard
+(SURVEY §8e), so N ranks run independent replicas (weak scaling); timing is
+the max over ranks.  `--impl reference` times the reference's CPU algorithm
+(the oracle port, oracle/rebk_oracle.py) on the host cores on a bounded
+sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "REABK iterations/s"
+UNIT = "iters/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_workload(name):
+    from paper_2001_04179_b200 import workloads
+
+    t0 = time.time()
+    wl = workloads.build(name)
+    log(f"[bench] built {name}: A {wl.problem.a.shape}, beta_max={wl.beta_max:.6g}, alpha={wl.alpha:.6g} "
+        f"({time.time() - t0:.1f}s)")
+    return wl
+
+
+def workload_desc(name, wl):
+    m, n = wl.problem.a.shape
+    tr, tc = max(wl.row_partition.block_sizes()), max(wl.col_partition.block_sizes())
+    desc = {
+        "c1": "C1 dense fp64 2000x500 randn, inconsistent",
+        "c2": "C2 dense fp64 4000x10000 rank 2000 (U diag(s) V^T, s~U[1,10]), inconsistent",
+    }[name]
+    return {
+        "workload": f"{desc}; row/col blocks {tr}/{tc}; alpha=1/beta_max; stop ||x-x*||/||x*||<1e-6; seed 17",
+        "m": m, "n": n, "row_block": tr, "col_block": tc,
+        "alpha": wl.alpha, "beta_max": wl.beta_max,
+        "l2_policy": f"inputs larger than L2: A = {m * n * 8 / 1e6:.0f} MB > 126 MB L2, no flush",
+    }
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception as exc:  # pragma: no cover
+            log(f"[bench] nvidia-smi unavailable: {exc}")
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names[1:], parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {
+            "sm_mhz": float(np.median(sm)) if sm else None,
+            "sm_max_mhz": float(max(smax)) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic(workload):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU arms
+def cpu_reference_run(wl, max_iters, time_cap_s=None):
+    """The reference algorithm on the host cores (oracle port with numpy's C
+    Philox), bounded to max_iters iterations.  Returns (iters, seconds)."""
+    from oracle.rebk_oracle import NumpyRng, OracleSolver
+
+    a = wl.problem.a.to_dense()
+    orc = OracleSolver(a, wl.problem.b, wl.row_partition.pointers(), wl.col_partition.pointers(), wl.alpha,
+                       "rebk")
+    tol = wl.rel_tol * float(np.linalg.norm(wl.problem.x_star))
+    res = orc.run(wl.seed, max_iters, tol, wl.problem.x_star, rng=NumpyRng(wl.seed))
+    return res["iters"], res["wall_time"]
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [d.get("num_threads", 1) for d in threadpool_info() if d.get("user_api") == "blas"]
+        return int(max(n)) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    wl = build_workload(args.workload)
+    sample_iters = args.ref_iters
+    for _ in range(args.warmup):
+        cpu_reference_run(wl, min(sample_iters, 50))
+    iters_tot, secs = 0, 0.0
+    for _ in range(args.steps):
+        it, s = cpu_reference_run(wl, sample_iters)
+        iters_tot += it
+        secs += s
+    v = iters_tot / secs
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_desc(args.workload, wl),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{sample_iters} REBK iterations of {args.workload} per step (oracle port: the "
+                                   f"reference's numpy operations and numpy Philox stream), OpenBLAS {cores} threads"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args):
+    import ctypes
+
+    import torch
+
+    import paper_2001_04179_b200 as P
+    from paper_2001_04179_b200 import _lib
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    wl = build_workload(args.workload)
+    prob = wl.problem
+    m, n = prob.a.shape
+    cfg = wl.config(max_iters=args.max_iters)
+    ctx = P.prepare(prob, cfg)
+    key = _lib.philox_key(cfg.seed)
+    tol = cfg.stop.tol
+    c = ctx.make_cfg(stop_mode="oracle_error", tol=tol, stride=1, max_iters=cfg.max_iters, key=key)
+    dm = prob.a.device(device=local)
+    dev = torch.device("cuda", local)
+    b_d = torch.from_numpy(prob.b).to(dev)
+    xs_d = torch.from_numpy(np.asarray(prob.x_star)).to(dev)
+    x_d = torch.zeros(n, dtype=torch.float64, device=dev)
+    z_d = torch.empty(m, dtype=torch.float64, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    lib = _lib.load()
+
+    def device_solve():
+        with torch.cuda.stream(stream):
+            x_d.zero_()
+            z_d.copy_(b_d)
+        tr = _lib.RebkTrace()
+        rc = lib.rebk_run_device(dm.handle, ctypes.byref(c), ctypes.c_void_p(b_d.data_ptr()),
+                                 ctypes.c_void_p(xs_d.data_ptr()), ctypes.c_void_p(x_d.data_ptr()),
+                                 ctypes.c_void_p(z_d.data_ptr()), ctypes.c_void_p(stream.cuda_stream),
+                                 ctypes.byref(tr))
+        _lib.check(rc, "rebk_run_device")
+        return tr
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        tr = device_solve()
+    log(f"[bench] warm-up solve: ITER={tr.iters} converged={bool(tr.converged)} "
+        f"loop={tr.loop_ms:.3f} ms grid={tr.grid_ctas}")
+
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    iters_total, loop_ms_total, launches = 0, 0.0, 0
+    for _ in range(args.steps):
+        tr = device_solve()
+        iters_total += int(tr.iters)
+        loop_ms_total += float(tr.loop_ms)
+        launches += 2  # sample_plan_kernel + rebk_dense_kernel (single chunk: max_iters < 2^20)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    iters_t = torch.tensor([float(iters_total)], dtype=torch.float64, device=dev)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(iters_t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = float(iters_t.item()) / (ms_max / 1e3)
+    per_solve_iters = iters_total / args.steps
+
+    # roofline of the dominant kernel (rebk_dense_kernel), from its own events
+    bytes_per_iter = wl.algorithmic_bytes_per_iter
+    kernel_ms = loop_ms_total / args.steps
+    achieved = bytes_per_iter * per_solve_iters / (kernel_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = profiled_traffic(args.workload)
+
+    # e2e through the public API from pinned host buffers, A re-uploaded each step
+    e2e = None
+    if not args.no_e2e:
+        a_pin = torch.from_numpy(prob.a.to_dense()).pin_memory()
+        b_pin = torch.from_numpy(prob.b).pin_memory()
+        xs_pin = torch.from_numpy(np.asarray(prob.x_star)).pin_memory()
+        mat = P.Matrix.from_dense(a_pin.numpy())
+        assert mat.to_dense().ctypes.data == a_pin.data_ptr()
+        prob2 = P.ProblemInstance(a=mat, b=b_pin.numpy(), x_star=xs_pin.numpy(), b_perp=None, meta=prob.meta)
+        cfg2 = wl.config(max_iters=args.max_iters)
+        cfg2.row_partition, cfg2.col_partition = wl.row_partition, wl.col_partition
+        P.run(prob2, cfg2)  # warm
+        mat.release_device()
+        barrier()
+        t0 = time.perf_counter()
+        e_iters = 0
+        for _ in range(args.steps):
+            tr2 = P.run(prob2, cfg2)
+            e_iters += tr2.iters
+            mat.release_device()
+        barrier()
+        e_s = time.perf_counter() - t0
+        e_t = torch.tensor([e_s], dtype=torch.float64, device=dev)
+        ei_t = torch.tensor([float(e_iters)], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+            dist.all_reduce(ei_t, op=dist.ReduceOp.SUM)
+        e2e = {
+            "value": float(ei_t.item()) / float(e_t.item()), "unit": UNIT,
+            "h2d_bytes_per_step": int(m * n * 8 + 2 * m * 8 + 2 * n * 8),
+            "d2h_bytes_per_step": int((m + n) * 8 + 64),
+            "time_to_tol_s": float(e_t.item()) / args.steps,
+            "path": "paper_2001_04179_b200.run(problem, config): A, b, x* uploaded from pinned host memory "
+                    "every step (fresh device ctx), x and z read back",
+        }
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        it, s = cpu_reference_run(wl, args.ref_iters)
+        cores = blas_threads()
+        cpu = {"value": it / s, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"first {it} REBK iterations of the same {args.workload} instance (oracle port: the "
+                         f"reference's numpy ops + numpy Philox), OpenBLAS {cores} threads, {s:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {**workload_desc(args.workload, wl), "parallelism": f"replicas x{ws}",
+                       "iters_per_solve": per_solve_iters, "grid_ctas": int(tr.grid_ctas)},
+            "time_to_tol_s": ms_max / args.steps / 1e3,
+            "achieved_gbps": achieved,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "rebk_dense_kernel", "peak_source": peak_src,
+                         "algorithmic_bytes_per_iter": bytes_per_iter,
+                         "iters_per_launch": per_solve_iters, "kernel_ms_per_launch": kernel_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--max-iters", type=int, default=50_000)
+    ap.add_argument("--ref-iters", type=int, default=2000, help="iterations per CPU reference sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,166 @@
+/*
+ * rebk.h — C ABI of librebk.so, the B200 (sm_100a) backend for the randomized
+ * extended (average) block Kaczmarz iteration of arXiv 2001.04179.
+ *
+ * The reference (`kaczmarz`, pure Python, /root/reference/pkg) has no FFI; its
+ * boundary for this path is Python-level:
+ *   run(problem, config) -> RunTrace              solvers.py:425-474
+ *   prepare(problem, config) -> SolverContext     solvers.py:271-273
+ *   SolverContext.initial_state / .step           solvers.py:231-249, :267-268
+ *   _STEPPERS[algo](state, ctx)                    solvers.py:384-392 (plugin point)
+ * Each entry point below replaces one piece of that boundary; the citation on
+ * each declaration names the reference code it stands in for.  Plain pointers
+ * and sizes only: no torch / numpy types cross this ABI.
+ *
+ * Conventions
+ *  - Every function returns 0 on success or a negative REBK_E* code; the
+ *    message is kept per thread and read with rebk_last_error().
+ *  - Dense A is row-major fp64 (m x n, leading dimension lda >= n), exactly
+ *    the reference Matrix layout (matrix.py:37-44).
+ *  - Row/column partitions are CONTIGUOUS blocks given by block pointers
+ *    ptr[0]=0 < ptr[1] < ... < ptr[nb]=axis_len (sampling.py:107-112).  The
+ *    host layer permutes A once for non-contiguous partitions.
+ *  - The per-block sampling arrays (cumulative weights, total, alpha/w scales)
+ *    are inputs, computed on the host exactly as the reference computes them
+ *    (sampling.py:122-132, solvers.py:151/:164), so the device reproduces the
+ *    reference block-index sequence bit for bit.
+ *  - A rebk_ctx is immutable after creation ("Matrices are
+ *    immutable"); concurrent rebk_run calls on one ctx are allowed.
+ */
+#ifndef REBK_H
+#define REBK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define REBK_ABI_VERSION 1
+
+/* error codes */
+#define REBK_OK 0
+#define REBK_EINVAL -1     /* bad argument / dimension (reference: ValueError) */
+#define REBK_ECUDA -2      /* CUDA runtime failure */
+#define REBK_ENOMEM -3     /* device allocation failed */
+#define REBK_ENODEV -4     /* no CUDA device */
+#define REBK_ENONFINITE -5 /* NaN/Inf met in the stopping reduction */
+
+/* algorithms served by the device kernel (solvers.py:39, :306-342) */
+#define REBK_ALGO_REBK 0 /* step_rebk  solvers.py:324-337 */
+#define REBK_ALGO_REK 1  /* step_rek   solvers.py:340-342 (singleton rebk) */
+#define REBK_ALGO_RABK 2 /* step_rabk  solvers.py:315-321 (row sweep only) */
+#define REBK_ALGO_RK 3   /* step_rk    solvers.py:306-312 (singleton rabk) */
+
+/* stopping modes (solvers.py:50-70, :398-422) */
+#define REBK_STOP_ORACLE_ERROR 0
+#define REBK_STOP_RESIDUAL_PROXY 1
+#define REBK_STOP_MAX_ITERS_ONLY 2
+
+typedef struct rebk_ctx rebk_ctx;
+
+/* One run's configuration: SolverConfig (solvers.py:73-85) with every
+ * host-resolved quantity the device needs. */
+typedef struct rebk_cfg {
+  int32_t algorithm;     /* REBK_ALGO_* */
+  int32_t stop_mode;     /* REBK_STOP_* */
+  double tol;            /* StoppingRule.tol (absolute, solvers.py:61) */
+  int64_t check_stride;  /* StoppingRule.check_stride */
+  int64_t max_iters;     /* SolverConfig.max_iters */
+  uint64_t philox_key[2];/* SeedSequence(seed).generate_state(2, u64) (sampling.py:36-37) */
+  uint64_t draw_offset;  /* index of the first uniform this run consumes (0 for run()) */
+  /* row partition (always present) */
+  int64_t n_row_blocks;
+  const int64_t* row_ptr;   /* [n_row_blocks+1] */
+  const double* row_cum;    /* [n_row_blocks]  np.cumsum(weights) */
+  double row_total;         /* cumulative[-1] */
+  const double* row_scale;  /* [n_row_blocks]  alpha / w */
+  /* column partition (REBK/REK only; 0/NULL for RABK/RK) */
+  int64_t n_col_blocks;
+  const int64_t* col_ptr;
+  const double* col_cum;
+  double col_total;
+  const double* col_scale;
+  /* optional explicit picks: [2*max_iters] int32 (col, row) per iteration,
+   * used instead of the Philox stream (ScriptedRng in the reference tests,
+   * test_solvers.py:23-31).  NULL = sample on device. */
+  const int32_t* picks;
+  int32_t record_errors;    /* SolverConfig.record_errors */
+  int32_t grid_ctas;        /* 0 = automatic */
+  double residual_scale;    /* sqrt(||A||_F^2) * ||b|| (solvers.py:411-413) */
+} rebk_cfg;
+
+/* RunTrace (solvers.py:96-112). errors is caller-allocated (capacity
+ * errors_cap); checkpoints follow from (n_checks, check_stride, iters). */
+typedef struct rebk_trace {
+  int64_t iters;
+  int32_t converged;
+  int32_t has_error;        /* 0 when stop_mode == MAX_ITERS_ONLY */
+  double final_error;
+  double loop_ms;           /* device time of the iteration loop (CUDA events) */
+  double* errors;
+  int64_t errors_cap;
+  int64_t n_checks;
+  int32_t grid_ctas;        /* CTAs the persistent kernel used */
+  int32_t reserved;
+} rebk_trace;
+
+/* ---- library / device ---------------------------------------------------- */
+int rebk_abi_version(void);
+const char* rebk_last_error(void);
+int rebk_device_count(int* count);
+
+/* ---- context: device copy of A (replaces Matrix dense storage,
+ *      matrix.py:26-44, and the cached block views of
+ *      SolverContext._materialize_blocks, solvers.py:115-120) --------------- */
+int rebk_ctx_create_dense(const double* a_host, int64_t m, int64_t n, int64_t lda,
+                          int device, rebk_ctx** out);
+/* borrow an existing device array (caller keeps it alive; e.g. a torch tensor) */
+int rebk_ctx_create_dense_device(const double* a_dev, int64_t m, int64_t n, int64_t lda,
+                                 int device, rebk_ctx** out);
+int rebk_ctx_destroy(rebk_ctx* ctx);
+int rebk_ctx_shape(const rebk_ctx* ctx, int64_t* m, int64_t* n);
+
+/* ---- the hot path ---------------------------------------------------------
+ * run(): solvers.py:425-474 with step_rebk / step_rek / step_rabk / step_rk.
+ * Host buffers; copies in and out are part of the call.
+ *   b [m] required; x0 [n] / z0 [m] optional (NULL -> x0 = 0, z0 = b,
+ *   solvers.py:231-249); x_star [n] required for ORACLE_ERROR;
+ *   x_out [n] required; z_out [m] optional. */
+int rebk_run(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b, const double* x0,
+             const double* z0, const double* x_star, double* x_out, double* z_out,
+             rebk_trace* trace);
+
+/* Same with DEVICE buffers on `stream` (cudaStream_t as void*); x_io / z_io
+ * hold the start point on entry (z_io ignored for RABK/RK) and the final
+ * iterates on return.  Synchronises the stream before returning. */
+int rebk_run_device(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev,
+                    const double* x_star_dev, double* x_io_dev, double* z_io_dev,
+                    void* stream, rebk_trace* trace);
+
+/* ---- sampler (sampling.py:23-45 Rng, :137-145 WeightedSampler.sample) -----
+ * Device sampling of the (col, row) block-index pairs of iterations
+ * [k0, k0+count) (k is 1-based), written to picks_out[2*count] (host). */
+int rebk_sample_sequence(const rebk_cfg* cfg, int64_t k0, int64_t count, int32_t* picks_out);
+
+/* Device block Frobenius norms (matrix.py:170-189): out[nb] for contiguous
+ * blocks ptr[nb+1] along axis 0 (rows) or 1 (columns). */
+int rebk_block_frobenius_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* ptr,
+                            double* out);
+
+/* ---- host-side helpers (no GPU needed) ---------------------------------- */
+/* numpy SeedSequence(entropy, spawn_key).generate_state(2, uint64): the
+ * Philox key of Rng(seed, spawn_key) (sampling.py:33-37). entropy / spawn
+ * words are the little-endian uint32 digits of each non-negative integer,
+ * n_spawn_words[i] giving how many words spawn key i contributes. */
+int rebk_philox_key(const uint32_t* entropy_words, int64_t n_entropy_words,
+                    const uint32_t* spawn_words, int64_t n_spawn_words, uint64_t key_out[2]);
+/* Uniform doubles draws [first, first+count) of Rng with this key
+ * (Generator.random: (u64 >> 11) * 2^-53). */
+int rebk_philox_uniforms_host(const uint64_t key[2], uint64_t first, int64_t count,
+                              double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REBK_H */

@@ -1,0 +1,599 @@
+// rebk_api.cu — the extern "C" boundary of librebk.so (declared in include/rebk.h).
+//
+// Host orchestration of one run (solvers.py:425-474): validate, upload the
+// per-run vectors, expand the block-index stream into per-iteration plans on
+// the device, launch the persistent kernel over chunks of iterations, read
+// back the iterates and the RunTrace fields.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/rebk.h"
+#include "philox.h"
+#include "rebk_internal.h"
+
+using namespace rebk;
+
+struct rebk_ctx {
+  int device;
+  int64_t m, n, lda;
+  const double* A;    // device
+  double* A_owned;    // non-null when the ctx allocated A
+  int sm_count;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(_e == cudaErrorMemoryAllocation ? REBK_ENOMEM : REBK_ECUDA, "%s: %s", #expr, \
+                  cudaGetErrorString(_e));                                                 \
+  } while (0)
+
+// RAII bundle of per-run device allocations, freed on the run's stream.
+struct DevArena {
+  cudaStream_t stream = nullptr;
+  std::vector<void*> ptrs;
+  ~DevArena() {
+    for (void* p : ptrs) cudaFreeAsync(p, stream);
+  }
+  template <typename T>
+  cudaError_t alloc(T** out, size_t count) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), stream);
+    if (e == cudaSuccess) ptrs.push_back(p);
+    *out = (T*)p;
+    return e;
+  }
+};
+
+int check_partition(const char* what, int64_t nb, const int64_t* ptr, const double* cum,
+                    const double* scale, int64_t axis_len) {
+  if (nb < 1 || !ptr || !cum || !scale)
+    return fail(REBK_EINVAL, "%s partition: need at least one block with ptr/cum/scale arrays", what);
+  if (ptr[0] != 0 || ptr[nb] != axis_len)
+    return fail(REBK_EINVAL, "%s partition covers [%lld, %lld), matrix axis has %lld", what,
+                (long long)ptr[0], (long long)ptr[nb], (long long)axis_len);
+  for (int64_t b = 0; b < nb; ++b)
+    if (ptr[b + 1] <= ptr[b]) return fail(REBK_EINVAL, "empty block in %s partition", what);
+  return REBK_OK;
+}
+
+int max_block(int64_t nb, const int64_t* ptr) {
+  int64_t mx = 0;
+  for (int64_t b = 0; b < nb; ++b) mx = std::max(mx, ptr[b + 1] - ptr[b]);
+  return (int)mx;
+}
+
+bool blocks_even(int64_t nb, const int64_t* ptr) {
+  for (int64_t b = 0; b < nb; ++b)
+    if (ptr[b] & 1) return false;
+  return true;
+}
+
+int grid_override() {
+  const char* s = getenv("REBK_GRID");
+  return s ? atoi(s) : 0;
+}
+
+// The persistent kernel's grid size depends only on the matrix shape, so two
+// runs on one matrix (e.g. rebk with z0 = 0 and rabk) do bit-identical row
+// sweeps (test_solvers.py:249-265).
+int choose_grid(const rebk_ctx* ctx, const rebk_cfg* cfg, int max_resident) {
+  int G = cfg->grid_ctas > 0 ? cfg->grid_ctas : grid_override();
+  if (G <= 0) {
+    const int64_t cells = ctx->m * ctx->n;
+    G = (int)std::min<int64_t>((cells + 65535) / 65536, (int64_t)ctx->sm_count);
+  }
+  G = std::max(1, std::min(G, max_resident));
+  return G;
+}
+
+struct Geometry {
+  int G;
+  int nR_max, nC_max, nJ_max, nI_max;
+  int ct_ld, rt_ld;
+  int stage_ct, stage_rt;
+  int ct_off, rt_off, vec_off;
+  size_t smem_bytes;
+};
+
+Geometry plan_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int G, bool extended) {
+  Geometry g{};
+  g.G = G;
+  for (int q = 0; q < G; ++q) {
+    g.nR_max = std::max(g.nR_max, split_rows(ctx->m, G, q + 1) - split_rows(ctx->m, G, q));
+    g.nC_max = std::max(g.nC_max, split_even(ctx->n, G, q + 1) - split_even(ctx->n, G, q));
+  }
+  g.nI_max = max_block(cfg->n_row_blocks, cfg->row_ptr);
+  g.nJ_max = extended ? max_block(cfg->n_col_blocks, cfg->col_ptr) : 0;
+  g.ct_ld = (g.nJ_max + 1) & ~1;
+  g.rt_ld = ((g.nC_max + 1) & ~1);
+  if (g.rt_ld % 4 == 0) g.rt_ld += 2;  // ≡ 2 (mod 4): conflict-free 2-lane row reads
+  const size_t vec = (size_t)(2 * g.nC_max + g.nR_max + g.nJ_max + g.nI_max + kThreads);
+  const size_t ct = (size_t)g.nR_max * g.ct_ld;
+  const size_t rt = (size_t)g.nI_max * g.rt_ld;
+  const size_t budget = (size_t)kSmemBudget / 8;
+  const bool aligned = (ctx->lda % 2 == 0) && ((uintptr_t)ctx->A % 16 == 0);
+  const bool ct_ok = aligned && extended && g.nJ_max >= 2 &&
+                     blocks_even(cfg->n_col_blocks, cfg->col_ptr);
+  const bool rt_ok = aligned && g.nC_max >= 2;
+  const char* no_stage = getenv("REBK_NO_STAGE");
+  const bool allow = !(no_stage && no_stage[0] == '1');
+  g.stage_ct = g.stage_rt = 0;
+  if (allow && ct_ok && rt_ok && vec + ct + rt <= budget) {
+    g.stage_ct = g.stage_rt = 1;
+  } else if (allow && rt_ok && vec + rt <= budget) {
+    g.stage_rt = 1;
+  } else if (allow && ct_ok && vec + ct <= budget) {
+    g.stage_ct = 1;
+  }
+  size_t off = 0;
+  g.ct_off = (int)off;
+  if (g.stage_ct) off += ct;
+  g.rt_off = (int)off;
+  if (g.stage_rt) off += rt;
+  g.vec_off = (int)off;
+  off += vec;
+  g.smem_bytes = off * 8;
+  return g;
+}
+
+int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev,
+                    double* x_dev, double* z_dev, cudaStream_t stream, rebk_trace* trace) {
+  const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
+  if (cfg->algorithm < 0 || cfg->algorithm > 3) return fail(REBK_EINVAL, "unknown algorithm %d", cfg->algorithm);
+  if (cfg->stop_mode < 0 || cfg->stop_mode > 2) return fail(REBK_EINVAL, "unknown stopping mode %d", cfg->stop_mode);
+  if (cfg->stop_mode != REBK_STOP_MAX_ITERS_ONLY && !(cfg->tol > 0.0)) return fail(REBK_EINVAL, "tol must be positive");
+  if (cfg->check_stride < 1) return fail(REBK_EINVAL, "check_stride must be at least 1");
+  if (cfg->max_iters < 0) return fail(REBK_EINVAL, "max_iters must be nonnegative");
+  if (cfg->stop_mode == REBK_STOP_ORACLE_ERROR && !xs_dev)
+    return fail(REBK_EINVAL, "oracle_error stopping needs a problem with x_star");
+  if (!b_dev || !x_dev || (extended && !z_dev)) return fail(REBK_EINVAL, "missing b / x / z buffer");
+  int rc = check_partition("row", cfg->n_row_blocks, cfg->row_ptr, cfg->row_cum, cfg->row_scale, ctx->m);
+  if (rc) return rc;
+  if (extended) {
+    rc = check_partition("col", cfg->n_col_blocks, cfg->col_ptr, cfg->col_cum, cfg->col_scale, ctx->n);
+    if (rc) return rc;
+  }
+  if (ctx->m > INT32_MAX || ctx->n > INT32_MAX) return fail(REBK_EINVAL, "matrix dimension exceeds 2^31");
+
+  CUDA_TRY(cudaSetDevice(ctx->device));
+
+  // geometry: find the largest grid that is co-resident with our smem need
+  int G0 = choose_grid(ctx, cfg, 1 << 20);
+  Geometry geo = plan_geometry(ctx, cfg, G0, extended);
+  int occ = 0;
+  CUDA_TRY(dense_kernel_occupancy(geo.smem_bytes, &occ));
+  if (occ < 1) return fail(REBK_EINVAL, "problem too large for one CTA's shared memory (%zu bytes)", geo.smem_bytes);
+  if (G0 > occ * ctx->sm_count) {
+    geo = plan_geometry(ctx, cfg, occ * ctx->sm_count, extended);
+  }
+  const int G = geo.G;
+
+  DevArena arena;
+  arena.stream = stream;
+  const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
+  int64_t *d_row_ptr, *d_col_ptr = nullptr;
+  double *d_row_cum, *d_row_scale, *d_col_cum = nullptr, *d_col_scale = nullptr;
+  CUDA_TRY(arena.alloc(&d_row_ptr, s + 1));
+  CUDA_TRY(arena.alloc(&d_row_cum, s));
+  CUDA_TRY(arena.alloc(&d_row_scale, s));
+  CUDA_TRY(cudaMemcpyAsync(d_row_ptr, cfg->row_ptr, (s + 1) * 8, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(d_row_cum, cfg->row_cum, s * 8, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(d_row_scale, cfg->row_scale, s * 8, cudaMemcpyHostToDevice, stream));
+  if (extended) {
+    CUDA_TRY(arena.alloc(&d_col_ptr, t + 1));
+    CUDA_TRY(arena.alloc(&d_col_cum, t));
+    CUDA_TRY(arena.alloc(&d_col_scale, t));
+    CUDA_TRY(cudaMemcpyAsync(d_col_ptr, cfg->col_ptr, (t + 1) * 8, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d_col_cum, cfg->col_cum, t * 8, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d_col_scale, cfg->col_scale, t * 8, cudaMemcpyHostToDevice, stream));
+  }
+  int32_t* d_picks = nullptr;
+  if (cfg->picks && cfg->max_iters > 0) {
+    CUDA_TRY(arena.alloc(&d_picks, 2 * cfg->max_iters));
+    CUDA_TRY(cudaMemcpyAsync(d_picks, cfg->picks, 2 * cfg->max_iters * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, stream));
+  }
+
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(cfg->max_iters, (int64_t)1 << 20));
+  Plan* d_plan;
+  double *d_upart, *d_rpart, *d_u, *d_r, *d_errpart, *d_res = nullptr, *d_errs = nullptr;
+  Control* d_ctl;
+  CUDA_TRY(arena.alloc(&d_plan, chunk));
+  CUDA_TRY(arena.alloc(&d_upart, (size_t)std::max(geo.nJ_max, 1) * G));
+  CUDA_TRY(arena.alloc(&d_rpart, (size_t)std::max(geo.nI_max, 1) * G));
+  CUDA_TRY(arena.alloc(&d_u, std::max(geo.nJ_max, 1)));
+  CUDA_TRY(arena.alloc(&d_r, std::max(geo.nI_max, 1)));
+  CUDA_TRY(arena.alloc(&d_errpart, G));
+  if (cfg->stop_mode == REBK_STOP_RESIDUAL_PROXY) CUDA_TRY(arena.alloc(&d_res, ctx->m));
+  const int64_t errs_cap = (cfg->record_errors && trace && trace->errors) ? trace->errors_cap : 0;
+  if (errs_cap > 0) CUDA_TRY(arena.alloc(&d_errs, errs_cap));
+  CUDA_TRY(arena.alloc(&d_ctl, 1));
+  CUDA_TRY(cudaMemsetAsync(d_ctl, 0, sizeof(Control), stream));
+
+  SampleParams sp{};
+  sp.key0 = cfg->philox_key[0];
+  sp.key1 = cfg->philox_key[1];
+  sp.draw_offset = cfg->draw_offset;
+  sp.extended = extended;
+  sp.n_row_blocks = (int32_t)s;
+  sp.n_col_blocks = (int32_t)t;
+  sp.row_ptr = d_row_ptr;
+  sp.row_cum = d_row_cum;
+  sp.row_total = cfg->row_total;
+  sp.row_scale = d_row_scale;
+  sp.col_ptr = d_col_ptr;
+  sp.col_cum = d_col_cum;
+  sp.col_total = cfg->col_total;
+  sp.col_scale = d_col_scale;
+  sp.picks = d_picks;
+
+  DenseParams p{};
+  p.A = ctx->A;
+  p.lda = ctx->lda;
+  p.m = (int32_t)ctx->m;
+  p.n = (int32_t)ctx->n;
+  p.b = b_dev;
+  p.xs = xs_dev;
+  p.x = x_dev;
+  p.z = z_dev;
+  p.upart = d_upart;
+  p.rpart = d_rpart;
+  p.u = d_u;
+  p.r = d_r;
+  p.errpart = d_errpart;
+  p.res = d_res;
+  p.errs = d_errs;
+  p.errs_cap = errs_cap;
+  p.plan = d_plan;
+  p.ctl = d_ctl;
+  p.extended = extended;
+  p.stop_mode = cfg->stop_mode;
+  p.tol = cfg->tol;
+  p.stride = cfg->check_stride;
+  p.max_iters = cfg->max_iters;
+  p.res_scale = cfg->residual_scale > 0.0 ? cfg->residual_scale : 1.0;
+  p.record = errs_cap > 0;
+  p.nJ_max = geo.nJ_max;
+  p.nI_max = geo.nI_max;
+  p.nR_max = geo.nR_max;
+  p.nC_max = geo.nC_max;
+  p.ct_ld = geo.ct_ld;
+  p.rt_ld = geo.rt_ld;
+  p.stage_ct = geo.stage_ct;
+  p.stage_rt = geo.stage_rt;
+  p.ct_off = geo.ct_off;
+  p.rt_off = geo.rt_off;
+  p.vec_off = geo.vec_off;
+
+  cudaEvent_t ev0, ev1;
+  CUDA_TRY(cudaEventCreate(&ev0));
+  CUDA_TRY(cudaEventCreate(&ev1));
+  cudaError_t err = cudaEventRecord(ev0, stream);
+  int64_t k = 1;
+  do {
+    const int64_t count = std::min(chunk, cfg->max_iters - k + 1);
+    if (err == cudaSuccess) err = launch_sample_plan(sp, k, count, d_plan, nullptr, stream);
+    if (err == cudaSuccess) err = cudaMemsetAsync(&d_ctl->bar, 0, sizeof(unsigned long long), stream);
+    p.k_begin = k;
+    p.k_end = k + count - 1;
+    if (err == cudaSuccess) err = launch_dense(p, G, geo.smem_bytes, stream);
+    k += std::max<int64_t>(count, 1);
+    if (err == cudaSuccess && k <= cfg->max_iters) {
+      int32_t done = 0;
+      err = cudaMemcpyAsync(&done, &d_ctl->done, sizeof done, cudaMemcpyDeviceToHost, stream);
+      if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
+      if (done) break;
+    }
+  } while (err == cudaSuccess && k <= cfg->max_iters);
+  if (err == cudaSuccess) err = cudaEventRecord(ev1, stream);
+  Control ctl{};
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&ctl, d_ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream);
+  if (err == cudaSuccess && errs_cap > 0) {
+    const int64_t nrec = errs_cap;
+    err = cudaMemcpyAsync(trace->errors, d_errs, nrec * sizeof(double), cudaMemcpyDeviceToHost, stream);
+  }
+  if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
+  float ms = 0.f;
+  if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, ev0, ev1);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  if (err != cudaSuccess) return fail(REBK_ECUDA, "REBK run failed: %s", cudaGetErrorString(err));
+  if (trace) {
+    trace->iters = ctl.iters;
+    trace->converged = ctl.converged;
+    trace->has_error = ctl.has_error;
+    trace->final_error = ctl.final_error;
+    trace->loop_ms = ms;
+    trace->n_checks = ctl.n_checks;
+    trace->grid_ctas = G;
+  }
+  return REBK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rebk_abi_version(void) { return REBK_ABI_VERSION; }
+
+const char* rebk_last_error(void) { return g_last_error.c_str(); }
+
+int rebk_device_count(int* count) {
+  if (!count) return fail(REBK_EINVAL, "null count");
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(REBK_ENODEV, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *count = c;
+  return REBK_OK;
+}
+
+static int ctx_common(rebk_ctx* c, int device) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) return fail(REBK_ENODEV, "no CUDA device available");
+  if (device < 0 || device >= ndev) return fail(REBK_EINVAL, "device %d out of range", device);
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+  c->device = device;
+  return REBK_OK;
+}
+
+int rebk_ctx_create_dense(const double* a_host, int64_t m, int64_t n, int64_t lda, int device,
+                          rebk_ctx** out) {
+  if (!out || !a_host) return fail(REBK_EINVAL, "null argument");
+  if (m < 1 || n < 1) return fail(REBK_EINVAL, "matrix must be 2-D and nonempty");
+  if (lda < n) return fail(REBK_EINVAL, "lda < n");
+  rebk_ctx* c = new rebk_ctx{};
+  int rc = ctx_common(c, device);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  // store with an even leading dimension so every row is 16-byte aligned
+  const int64_t ld = (n + 1) & ~(int64_t)1;
+  double* dA = nullptr;
+  cudaError_t e = cudaMalloc(&dA, (size_t)m * ld * sizeof(double));
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(REBK_ENOMEM, "cudaMalloc(A, %lld bytes): %s", (long long)(m * ld * 8), cudaGetErrorString(e));
+  }
+  if (ld != n) cudaMemset(dA, 0, (size_t)m * ld * sizeof(double));
+  e = cudaMemcpy2D(dA, ld * sizeof(double), a_host, lda * sizeof(double), n * sizeof(double), m,
+                   cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(dA);
+    delete c;
+    return fail(REBK_ECUDA, "upload of A failed: %s", cudaGetErrorString(e));
+  }
+  c->m = m;
+  c->n = n;
+  c->lda = ld;
+  c->A = dA;
+  c->A_owned = dA;
+  *out = c;
+  return REBK_OK;
+}
+
+int rebk_ctx_create_dense_device(const double* a_dev, int64_t m, int64_t n, int64_t lda, int device,
+                                 rebk_ctx** out) {
+  if (!out || !a_dev) return fail(REBK_EINVAL, "null argument");
+  if (m < 1 || n < 1) return fail(REBK_EINVAL, "matrix must be 2-D and nonempty");
+  if (lda < n) return fail(REBK_EINVAL, "lda < n");
+  rebk_ctx* c = new rebk_ctx{};
+  int rc = ctx_common(c, device);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  c->m = m;
+  c->n = n;
+  c->lda = lda;
+  c->A = a_dev;
+  c->A_owned = nullptr;
+  *out = c;
+  return REBK_OK;
+}
+
+int rebk_ctx_destroy(rebk_ctx* ctx) {
+  if (!ctx) return REBK_OK;
+  if (ctx->A_owned) {
+    cudaSetDevice(ctx->device);
+    cudaFree(ctx->A_owned);
+  }
+  delete ctx;
+  return REBK_OK;
+}
+
+int rebk_ctx_shape(const rebk_ctx* ctx, int64_t* m, int64_t* n) {
+  if (!ctx) return fail(REBK_EINVAL, "null ctx");
+  if (m) *m = ctx->m;
+  if (n) *n = ctx->n;
+  return REBK_OK;
+}
+
+int rebk_run_device(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* x_star_dev,
+                    double* x_io_dev, double* z_io_dev, void* stream, rebk_trace* trace) {
+  if (!ctx || !cfg) return fail(REBK_EINVAL, "null ctx/cfg");
+  return run_device_impl(ctx, cfg, b_dev, x_star_dev, x_io_dev, z_io_dev, (cudaStream_t)stream, trace);
+}
+
+int rebk_run(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b, const double* x0, const double* z0,
+             const double* x_star, double* x_out, double* z_out, rebk_trace* trace) {
+  if (!ctx || !cfg || !b || !x_out) return fail(REBK_EINVAL, "null argument");
+  if (cfg->stop_mode == REBK_STOP_ORACLE_ERROR && !x_star)
+    return fail(REBK_EINVAL, "oracle_error stopping needs a problem with x_star");
+  const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t stream;
+  CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  const int64_t m = ctx->m, n = ctx->n;
+  int rc = REBK_OK;
+  {
+    DevArena arena;
+    arena.stream = stream;
+    double *d_b, *d_x, *d_z = nullptr, *d_xs = nullptr;
+    cudaError_t e = arena.alloc(&d_b, m);
+    if (e == cudaSuccess) e = arena.alloc(&d_x, n);
+    if (e == cudaSuccess && extended) e = arena.alloc(&d_z, m);
+    if (e == cudaSuccess && x_star) e = arena.alloc(&d_xs, n);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_b, b, m * 8, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess)
+      e = x0 ? cudaMemcpyAsync(d_x, x0, n * 8, cudaMemcpyHostToDevice, stream)
+             : cudaMemsetAsync(d_x, 0, n * 8, stream);
+    if (e == cudaSuccess && extended)
+      e = cudaMemcpyAsync(d_z, z0 ? z0 : b, m * 8, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess && x_star) e = cudaMemcpyAsync(d_xs, x_star, n * 8, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) {
+      rc = fail(REBK_ECUDA, "input upload failed: %s", cudaGetErrorString(e));
+    } else {
+      rc = run_device_impl(ctx, cfg, d_b, d_xs, d_x, d_z, stream, trace);
+    }
+    if (rc == REBK_OK) {
+      e = cudaMemcpyAsync(x_out, d_x, n * 8, cudaMemcpyDeviceToHost, stream);
+      if (e == cudaSuccess && z_out && extended)
+        e = cudaMemcpyAsync(z_out, d_z, m * 8, cudaMemcpyDeviceToHost, stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+      if (e != cudaSuccess) rc = fail(REBK_ECUDA, "output download failed: %s", cudaGetErrorString(e));
+    }
+  }
+  cudaStreamSynchronize(stream);
+  cudaStreamDestroy(stream);
+  return rc;
+}
+
+int rebk_sample_sequence(const rebk_cfg* cfg, int64_t k0, int64_t count, int32_t* picks_out) {
+  if (!cfg || !picks_out || k0 < 1 || count < 0) return fail(REBK_EINVAL, "bad argument");
+  const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
+  if (count == 0) return REBK_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(REBK_ENODEV, "no CUDA device available");
+  cudaStream_t stream;
+  CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  int rc = REBK_OK;
+  {
+    DevArena arena;
+    arena.stream = stream;
+    const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
+    int64_t *d_row_ptr, *d_col_ptr = nullptr;
+    double *d_row_cum, *d_row_scale, *d_col_cum = nullptr, *d_col_scale = nullptr;
+    int32_t* d_out;
+    cudaError_t e = arena.alloc(&d_row_ptr, s + 1);
+    if (!e) e = arena.alloc(&d_row_cum, s);
+    if (!e) e = arena.alloc(&d_row_scale, s);
+    if (!e) e = cudaMemcpyAsync(d_row_ptr, cfg->row_ptr, (s + 1) * 8, cudaMemcpyHostToDevice, stream);
+    if (!e) e = cudaMemcpyAsync(d_row_cum, cfg->row_cum, s * 8, cudaMemcpyHostToDevice, stream);
+    if (!e) e = cudaMemcpyAsync(d_row_scale, cfg->row_scale, s * 8, cudaMemcpyHostToDevice, stream);
+    if (!e && extended) {
+      e = arena.alloc(&d_col_ptr, t + 1);
+      if (!e) e = arena.alloc(&d_col_cum, t);
+      if (!e) e = arena.alloc(&d_col_scale, t);
+      if (!e) e = cudaMemcpyAsync(d_col_ptr, cfg->col_ptr, (t + 1) * 8, cudaMemcpyHostToDevice, stream);
+      if (!e) e = cudaMemcpyAsync(d_col_cum, cfg->col_cum, t * 8, cudaMemcpyHostToDevice, stream);
+      if (!e) e = cudaMemcpyAsync(d_col_scale, cfg->col_scale, t * 8, cudaMemcpyHostToDevice, stream);
+    }
+    if (!e) e = arena.alloc(&d_out, 2 * count);
+    SampleParams sp{};
+    sp.key0 = cfg->philox_key[0];
+    sp.key1 = cfg->philox_key[1];
+    sp.draw_offset = cfg->draw_offset;
+    sp.extended = extended;
+    sp.n_row_blocks = (int32_t)s;
+    sp.n_col_blocks = (int32_t)t;
+    sp.row_ptr = d_row_ptr;
+    sp.row_cum = d_row_cum;
+    sp.row_total = cfg->row_total;
+    sp.row_scale = d_row_scale;
+    sp.col_ptr = d_col_ptr;
+    sp.col_cum = d_col_cum;
+    sp.col_total = cfg->col_total;
+    sp.col_scale = d_col_scale;
+    if (!e) e = launch_sample_plan(sp, k0, count, nullptr, d_out, stream);
+    if (!e) e = cudaMemcpyAsync(picks_out, d_out, 2 * count * sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
+    if (!e) e = cudaStreamSynchronize(stream);
+    if (e) rc = fail(REBK_ECUDA, "sampling failed: %s", cudaGetErrorString(e));
+  }
+  cudaStreamSynchronize(stream);
+  cudaStreamDestroy(stream);
+  return rc;
+}
+
+int rebk_block_frobenius_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* ptr, double* out) {
+  if (!ctx || !ptr || !out || nb < 1 || (axis != 0 && axis != 1)) return fail(REBK_EINVAL, "bad argument");
+  const int64_t len = axis == 0 ? ctx->m : ctx->n;
+  if (ptr[0] != 0 || ptr[nb] != len) return fail(REBK_EINVAL, "partition does not cover the axis");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t stream;
+  CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  int rc = REBK_OK;
+  {
+    DevArena arena;
+    arena.stream = stream;
+    int64_t* d_ptr;
+    double* d_out;
+    cudaError_t e = arena.alloc(&d_ptr, nb + 1);
+    if (!e) e = arena.alloc(&d_out, nb);
+    if (!e) e = cudaMemcpyAsync(d_ptr, ptr, (nb + 1) * 8, cudaMemcpyHostToDevice, stream);
+    if (!e) e = launch_block_norms(ctx->A, ctx->lda, ctx->m, ctx->n, axis, nb, d_ptr, d_out, stream);
+    if (!e) e = cudaMemcpyAsync(out, d_out, nb * 8, cudaMemcpyDeviceToHost, stream);
+    if (!e) e = cudaStreamSynchronize(stream);
+    if (e) rc = fail(REBK_ECUDA, "block norms failed: %s", cudaGetErrorString(e));
+  }
+  cudaStreamSynchronize(stream);
+  cudaStreamDestroy(stream);
+  return rc;
+}
+
+int rebk_philox_key(const uint32_t* entropy_words, int64_t n_entropy_words, const uint32_t* spawn_words,
+                    int64_t n_spawn_words, uint64_t key_out[2]) {
+  if (!key_out || n_entropy_words < 0 || n_spawn_words < 0) return fail(REBK_EINVAL, "bad argument");
+  std::vector<uint32_t> ent;
+  if (n_entropy_words == 0)
+    ent.push_back(0u);
+  else
+    ent.assign(entropy_words, entropy_words + n_entropy_words);
+  if (n_spawn_words > 0) {
+    while (ent.size() < 4) ent.push_back(0u);
+    ent.insert(ent.end(), spawn_words, spawn_words + n_spawn_words);
+  }
+  seedseq_generate_u64x2(ent.data(), (int64_t)ent.size(), key_out);
+  return REBK_OK;
+}
+
+int rebk_philox_uniforms_host(const uint64_t key[2], uint64_t first, int64_t count, double* out) {
+  if (!key || !out || count < 0) return fail(REBK_EINVAL, "bad argument");
+  for (int64_t q = 0; q < count; ++q) {
+    const uint64_t d = first + (uint64_t)q;
+    const u64x4 blk = philox_block(d >> 2, key[0], key[1]);
+    out[q] = u64_to_unit_double(blk.v[d & 3]);
+  }
+  return REBK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// rebk_internal.h — types shared by the sm_100a kernels and the C-ABI layer.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rebk {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+// dynamic shared memory we are willing to ask for (227 KB max per CTA on B200)
+constexpr int kSmemBudget = 220 * 1024;
+
+// One iteration's resolved picks (32 bytes): the column block [c_lo, c_hi)
+// with its scale alpha/||A_{:,J}||_F^2 and the row block [r_lo, r_hi) with
+// alpha/||A_{I,:}||_F^2 (solvers.py:151, :164).
+struct Plan {
+  int32_t c_lo, c_hi, r_lo, r_hi;
+  double c_scale, r_scale;
+};
+
+// Device-resident run control (one per rebk_run).
+struct Control {
+  unsigned long long bar;  // grid-barrier arrival counter (reset per launch)
+  int32_t done;            // run finished (converged, or budget spent)
+  int32_t converged;
+  int64_t iters;
+  double final_error;
+  int64_t n_checks;
+  int32_t has_error;
+  int32_t pad;
+};
+
+struct DenseParams {
+  const double* A;
+  int64_t lda;
+  int32_t m, n;
+  const double* b;
+  const double* xs;  // x_star (oracle_error)
+  double* x;
+  double* z;
+  // workspace (partials are stored transposed: part[e * G + g])
+  double* upart;
+  double* rpart;
+  double* u;
+  double* r;
+  double* errpart;  // [G]
+  double* res;      // [m] residual-proxy scratch
+  double* errs;     // recorded errors
+  int64_t errs_cap;
+  const Plan* plan;  // plan[k - k_begin]
+  int64_t k_begin, k_end;  // 1-based iterations handled by this launch
+  Control* ctl;
+  int32_t extended;   // REBK/REK: column sweep on z
+  int32_t stop_mode;  // REBK_STOP_*
+  double tol;
+  int64_t stride;
+  int64_t max_iters;
+  double res_scale;
+  int32_t record;
+  // tile geometry (host-computed)
+  int32_t nJ_max, nI_max;  // largest column / row block
+  int32_t nR_max, nC_max;  // largest owned z-row / x-column slice
+  int32_t ct_ld, rt_ld;    // leading dims of the staged tiles (doubles)
+  int32_t stage_ct, stage_rt;  // 1 = tile staged in shared memory by TMA bulk copies
+  int32_t ct_off, rt_off, vec_off;  // shared-memory carve-up (in doubles)
+};
+
+struct SampleParams {
+  uint64_t key0, key1;
+  uint64_t draw_offset;
+  int32_t extended;
+  int32_t n_row_blocks, n_col_blocks;
+  const int64_t* row_ptr;
+  const double* row_cum;
+  double row_total;
+  const double* row_scale;
+  const int64_t* col_ptr;
+  const double* col_cum;
+  double col_total;
+  const double* col_scale;
+  const int32_t* picks;  // optional scripted picks, indexed by (k-1)
+};
+
+// balanced split of [0, len) over G parts; boundaries rounded down to even
+// so that staged row segments start 16-byte aligned
+__host__ __device__ inline int32_t split_even(int64_t len, int32_t G, int32_t g) {
+  if (g >= G) return (int32_t)len;
+  int64_t p = (len * (int64_t)g) / G;
+  return (int32_t)(p & ~(int64_t)1);
+}
+__host__ __device__ inline int32_t split_rows(int64_t len, int32_t G, int32_t g) {
+  if (g >= G) return (int32_t)len;
+  return (int32_t)((len * (int64_t)g) / G);
+}
+
+// launchers (rebk_dense.cu)
+cudaError_t launch_sample_plan(const SampleParams& sp, int64_t k0, int64_t count, Plan* plan,
+                               int32_t* picks_out, cudaStream_t stream);
+cudaError_t launch_dense(const DenseParams& p, int G, size_t smem_bytes, cudaStream_t stream);
+cudaError_t dense_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
+cudaError_t launch_block_norms(const double* A, int64_t lda, int64_t m, int64_t n, int axis,
+                               int64_t nb, const int64_t* ptr_dev, double* out_dev,
+                               cudaStream_t stream);
+
+}  // namespace rebk

@@ -1,0 +1,124 @@
+"""Synthetic instances standing in for BASELINE.json's five configurations.
+
+No public dataset is involved: every config is a seeded synthetic recipe with
+the shapes and value distributions BASELINE.json names.
+All randomness comes from the reference's own stream family (numpy Philox via
+:class:`Rng`), so A is bit-identical on every machine; anything that goes
+through LAPACK (QR, Cholesky) may differ in the last bits between hosts,
+which is why parity tests compare the device with the oracle on the *same*
+in-process instance and use the committed golden vectors with a tolerance.
+
+Stepsize: the "reference stepsize rule" alpha = 1/beta_max (cli.py default
+``--alpha 1x``, PAPER.md Remark 2.8); beta_max via block Gram eigenvalues.
+Stop: ||x - x*|| / ||x*|| < 1e-6 as the reference's absolute oracle_error
+with tol = 1e-6 ||x*|| (1e-4 for C5).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .matrix import Matrix
+from .problems import ProblemInstance, ProblemMeta
+from .sampling import Partition, Rng, contiguous_partition
+from .solvers import SolverConfig, StoppingRule, compute_beta_max
+
+
+@dataclass
+class Workload:
+    name: str
+    problem: ProblemInstance
+    row_partition: Partition
+    col_partition: Partition
+    alpha: float
+    beta_max: float
+    rel_tol: float
+    seed: int = 17
+
+    def config(self, max_iters: int = 50_000, **kw) -> SolverConfig:
+        xs = np.asarray(self.problem.x_star)
+        tol = self.rel_tol * float(np.linalg.norm(xs))
+        stop = kw.pop("stop", StoppingRule(mode="oracle_error", tol=tol, check_stride=1))
+        return SolverConfig(
+            algorithm=kw.pop("algorithm", "rebk"), alpha=self.alpha,
+            row_partition=self.row_partition, col_partition=self.col_partition,
+            seed=kw.pop("seed", self.seed), max_iters=max_iters, stop=stop,
+            beta_max=self.beta_max, **kw,
+        )
+
+    @property
+    def algorithmic_bytes_per_iter(self) -> float:
+        """8 (m |J| + |I| n): the two selected blocks read once."""
+        m, n = self.problem.a.shape
+        tj = max(self.col_partition.block_sizes())
+        ti = max(self.row_partition.block_sizes())
+        return 8.0 * (m * tj + ti * n)
+
+
+def _instance(a: np.ndarray, b: np.ndarray, x_star: np.ndarray, seed: int, rank: int) -> ProblemInstance:
+    mat = Matrix.from_dense(a)
+    return ProblemInstance(
+        a=mat, b=b, x_star=x_star, b_perp=None,
+        meta=ProblemMeta(declared_rank=rank, kappa_bound=None, consistent=False, seed=seed,
+                         residual_norm=0.0),
+    )
+
+
+def c1_arrays(seed: int = 0):
+    """C1: A = randn(2000, 500); b = A x + r, r ⊥ range(A), ||r|| = 0.1 ||A x||."""
+    rng = Rng(seed)
+    a = rng.standard_normal((2000, 500))
+    xs = rng.standard_normal(500)
+    w = rng.standard_normal(2000)
+    q, _ = np.linalg.qr(a)
+    r = w - q @ (q.T @ w)
+    ax = a @ xs
+    r *= 0.1 * np.linalg.norm(ax) / np.linalg.norm(r)
+    b = ax + r
+    x_star = np.linalg.lstsq(a, b, rcond=None)[0]
+    return a, b, x_star
+
+
+def c1_matrix(seed: int = 0) -> np.ndarray:
+    """Just C1's A (pure Philox stream: identical bits on every host)."""
+    return Rng(seed).standard_normal((2000, 500))
+
+
+def c2_arrays(seed: int = 0):
+    """C2: A = U diag(sigma) V^T, 4000 x 10000, rank 2000, sigma ~ U[1, 10]."""
+    rng = Rng(seed)
+    u = np.linalg.qr(rng.standard_normal((4000, 2000)))[0]
+    v = np.linalg.qr(rng.standard_normal((10000, 2000)))[0]
+    sig = 1.0 + 9.0 * rng.uniforms(2000)
+    a = (u * sig) @ v.T
+    xs = rng.standard_normal(10000)
+    w = rng.standard_normal(4000)
+    r = w - u @ (u.T @ w)
+    ax = a @ xs
+    r *= 0.1 * np.linalg.norm(ax) / np.linalg.norm(r)
+    b = ax + r
+    x_star = v @ ((u.T @ b) / sig)
+    return a, b, x_star
+
+
+def make_workload(name: str, a: np.ndarray, b: np.ndarray, x_star: np.ndarray, tau_row: int,
+                  tau_col: int, rel_tol: float = 1e-6, beta_max: float | None = None,
+                  alpha_factor: float = 1.0, seed: int = 17) -> Workload:
+    prob = _instance(a, b, x_star, 0, min(a.shape))
+    rp = contiguous_partition(a.shape[0], tau_row, "row")
+    cp = contiguous_partition(a.shape[1], tau_col, "col")
+    if beta_max is None:
+        beta_max = compute_beta_max(prob.a, rp, cp)[2]
+    return Workload(name, prob, rp, cp, alpha_factor / beta_max, beta_max, rel_tol, seed)
+
+
+def build(name: str, **kw) -> Workload:
+    if name == "c1":
+        a, b, xs = c1_arrays()
+        return make_workload("c1", a, b, xs, 100, 100, **kw)
+    if name == "c2":
+        a, b, xs = c2_arrays()
+        return make_workload("c2", a, b, xs, 200, 200, **kw)
+    raise KeyError(f"unknown workload {name!r}")

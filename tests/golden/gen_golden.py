@@ -1,0 +1,249 @@
+"""Generate the golden vectors by running the REFERENCE package itself.
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/gen_golden.py [--skip-c2]
+
+Runs only in the build container (the reference is not present on the GPU
+box); the .npz files it writes are committed and read by the tests.
+Everything recorded comes from the reference's public API (kaczmarz.run,
+prepare/initial_state/step, Rng, samplers), never from this repo's code,
+except that the C1/C2 instance arrays are built by the recipes in
+paper_2001_04179_b200.workloads (plain numpy + the reference's own Rng
+stream) — the same recipes the GPU tests rebuild.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+if "/root/reference/pkg/src" not in sys.path:
+    sys.path.insert(0, "/root/reference/pkg/src")
+
+import kaczmarz as K  # noqa: E402  (the reference)
+from kaczmarz.rates import compute_beta_max  # noqa: E402
+
+from paper_2001_04179_b200 import workloads  # noqa: E402
+
+
+def ref_picks(ctx, seed, count):
+    rng = K.Rng(seed)
+    out = np.empty((count, 2), dtype=np.int32)
+    for k in range(count):
+        if ctx.col_sampler is not None and ctx.algorithm in ("rebk", "rek"):
+            out[k, 0] = ctx.col_sampler.sample(rng)
+        else:
+            rng.uniform()
+            out[k, 0] = -1
+        out[k, 1] = ctx.row_sampler.sample(rng)
+    return out
+
+
+def snapshots(problem, cfg, ks):
+    ctx = K.prepare(problem, cfg)
+    st = ctx.initial_state()
+    xs, zs = {}, {}
+    kmax = max(ks)
+    for k in range(1, kmax + 1):
+        ctx.step(st)
+        if k in ks:
+            xs[k] = st.x.copy()
+            zs[k] = None if st.z is None else st.z.copy()
+    return ctx, xs, zs
+
+
+def ptrs(p):
+    return np.concatenate([[0], np.cumsum(p.block_sizes())]).astype(np.int64)
+
+
+def philox_fixture():
+    seeds = [0, 1, 7, 17, 2024, 99, 2**64 + 3]
+    keys, draws = [], []
+    for s in seeds:
+        r = K.Rng(s)
+        keys.append(r._gen.bit_generator.state["state"]["key"].copy())
+        draws.append([r.uniform() for _ in range(64)])
+    spawn_cases = [(4, (0,)), (4, (1,)), (2**40 + 1, (3, 5))]
+    skeys, sdraws = [], []
+    for s, sk in spawn_cases:
+        r = K.Rng(s, sk)
+        skeys.append(r._gen.bit_generator.state["state"]["key"].copy())
+        sdraws.append([r.uniform() for _ in range(16)])
+    np.savez_compressed(
+        os.path.join(HERE, "philox.npz"),
+        seeds=np.asarray([str(s) for s in seeds]), keys=np.asarray(keys, dtype=np.uint64),
+        draws=np.asarray(draws),
+        spawn_seeds=np.asarray([str(s) for s, _ in spawn_cases]),
+        spawn_keys_flat=np.asarray([str(sk) for _, sk in spawn_cases]),
+        spawn_philox_keys=np.asarray(skeys, dtype=np.uint64), spawn_draws=np.asarray(sdraws),
+    )
+
+
+def small_case(name, a, b, algo, alpha, seed, row_p=None, col_p=None, max_iters=300, tol=1e-14,
+               stride=1, mode="oracle_error", ks=(1, 10, 100), z0=None, record=True, problem=None):
+    if problem is None:
+        mat = K.Matrix.from_dense(a) if not hasattr(a, "shape") or not hasattr(a, "tocsr") else K.Matrix.from_sparse(a)
+        problem = K.ProblemInstance(a=mat, b=np.asarray(b, float), x_star=None, b_perp=None,
+                                    meta=K.ProblemMeta(0, None, False, 0, 0.0))
+        problem.ensure_oracle()
+    cfg = K.SolverConfig(algorithm=algo, alpha=alpha, seed=seed, row_partition=row_p, col_partition=col_p,
+                         max_iters=max_iters, stop=K.StoppingRule(mode=mode, tol=tol, check_stride=stride),
+                         record_errors=record, z0=z0)
+    tr = K.run(problem, cfg)
+    ks = tuple(k for k in ks if k <= max(max_iters, 1))
+    ctx, xs, zs = snapshots(problem, K.SolverConfig(algorithm=algo, alpha=alpha, seed=seed, row_partition=row_p,
+                                                    col_partition=col_p, max_iters=max(ks), z0=z0,
+                                                    stop=K.StoppingRule(mode="max_iters_only")), ks)
+    npk = max(tr.iters, max(ks))
+    out = dict(
+        a=problem.a.to_dense(), b=problem.b, x_star=np.asarray(problem.x_star), algorithm=algo, alpha=alpha,
+        seed=seed, max_iters=max_iters, tol=tol, stride=stride, mode=mode,
+        row_blocks=np.asarray([np.asarray(bk, dtype=np.int64) for bk in ctx.row_partition.blocks], dtype=object),
+        iters=tr.iters, converged=tr.converged, final_error=np.nan if tr.final_error is None else tr.final_error,
+        errors=tr.errors if tr.errors is not None else np.zeros(0),
+        checkpoints=tr.checkpoints if tr.checkpoints is not None else np.zeros(0, dtype=np.int64),
+        warnings=np.asarray(tr.warnings), picks=ref_picks(ctx, seed, npk), ks=np.asarray(ks),
+        row_cum=ctx.row_sampler.cumulative, row_scales=np.asarray(ctx.row_scales),
+    )
+    if ctx.col_partition is not None:
+        out["col_blocks"] = np.asarray([np.asarray(bk, dtype=np.int64) for bk in ctx.col_partition.blocks],
+                                       dtype=object)
+        out["col_cum"] = ctx.col_sampler.cumulative
+        out["col_scales"] = np.asarray(ctx.col_scales)
+    if z0 is not None:
+        out["z0"] = z0
+    for k in ks:
+        out[f"x_{k}"] = xs[k]
+        if zs[k] is not None:
+            out[f"z_{k}"] = zs[k]
+    np.savez_compressed(os.path.join(HERE, f"case_{name}.npz"), **out)
+    print(f"{name}: iters={tr.iters} conv={tr.converged} err={tr.final_error}")
+
+
+def small_cases():
+    # hand values (test_solvers.py:307-316)
+    small_case("identity2", np.eye(2), [1.0, 2.0], "rebk", 1.0, 0, K.contiguous_partition(2, 2, "row"),
+               K.contiguous_partition(2, 2, "col"), max_iters=1, ks=(1,), tol=1e-30)
+    # run semantics problem (test_solvers.py:380-382, :423-431, :452-459)
+    a = K.gen_type2(15, 8, seed=24)
+    p = K.make_rhs(a, seed=25, inconsistent=True)
+    small_case("t2_15x8_rebk", None, None, "rebk", 1.2, 7, K.contiguous_partition(15, 3, "row"),
+               K.contiguous_partition(8, 2, "col"), max_iters=300, tol=1e-14, stride=10, problem=p)
+    small_case("t2_15x8_rek_residual", None, None, "rek", 1.0, 2, None, None, max_iters=500_000,
+               tol=1e-8, mode="residual_proxy", problem=p, ks=(1, 10))
+    small_case("t2_15x8_rek_stride7", None, None, "rek", 1.0, 1, None, None, max_iters=100, tol=1e-14,
+               stride=7, problem=p, ks=(1, 10))
+    # residual-proxy stop with a nonzero start residual (rabk has no z)
+    a = K.gen_type2(15, 8, seed=24)
+    p = K.make_rhs(a, seed=26, inconsistent=False)
+    small_case("t2_15x8_rabk_residual", None, None, "rabk", 1.0, 4, K.contiguous_partition(15, 3, "row"), None,
+               max_iters=100_000, tol=1e-8, stride=5, mode="residual_proxy", problem=p, ks=(1, 10))
+    # row-space / contraction problem (test_solvers.py:331-352)
+    a = K.gen_type1(40, 20, 15, 2.0, seed=20)
+    p = K.make_rhs(a, seed=21, inconsistent=True)
+    rp, cp = K.contiguous_partition(40, 5, "row"), K.contiguous_partition(20, 5, "col")
+    beta = compute_beta_max(p.a, rp, cp)[2]
+    small_case("t1_40x20_rebk", None, None, "rebk", 1.0 / beta, 9, rp, cp, max_iters=5000, tol=1e-10,
+               problem=p)
+    # REK == singleton REBK (test_solvers.py:136-151)
+    a = K.gen_type2(12, 7, seed=2)
+    p = K.make_rhs(a, seed=3, inconsistent=True)
+    small_case("t2_12x7_rek", None, None, "rek", 1.0, 17, None, None, max_iters=1000, tol=1e-12,
+               problem=p, ks=(1, 10, 100, 1000))
+    # RABK / REBK(z0=0) (test_solvers.py:249-265)
+    a = K.gen_type2(14, 9, seed=12)
+    p = K.make_rhs(a, seed=13, inconsistent=True)
+    small_case("t2_14x9_rabk", None, None, "rabk", 1.4, 33, K.contiguous_partition(14, 3, "row"), None,
+               max_iters=1000, mode="max_iters_only", problem=p, ks=(1, 10, 100, 1000))
+    # RK (test_solvers.py:236-246)
+    a = K.gen_type2(9, 5, seed=10)
+    p = K.make_rhs(a, seed=11)
+    small_case("t2_9x5_rk", None, None, "rk", 1.0, 21, None, None, max_iters=500, mode="max_iters_only",
+               problem=p, ks=(1, 10, 100, 500))
+    # ragged last blocks + odd sizes (unstaged path)
+    a = K.gen_type2(37, 23, seed=30)
+    p = K.make_rhs(a, seed=31, inconsistent=True)
+    rp, cp = K.contiguous_partition(37, 5, "row"), K.contiguous_partition(23, 4, "col")
+    beta = compute_beta_max(p.a, rp, cp)[2]
+    small_case("t2_37x23_ragged", None, None, "rebk", 1.5 / beta, 3, rp, cp, max_iters=4000, tol=1e-9,
+               problem=p, stride=3)
+    # non-contiguous index partitions
+    a = K.gen_type2(20, 12, seed=40)
+    p = K.make_rhs(a, seed=41, inconsistent=True)
+    rng = np.random.default_rng(5)
+    rperm, cperm = rng.permutation(20), rng.permutation(12)
+    rp = K.Partition("row", 20, tuple(np.sort(rperm[i:i + 4]) for i in range(0, 20, 4)))
+    cp = K.Partition("col", 12, tuple(np.sort(cperm[i:i + 3]) for i in range(0, 12, 3)))
+    small_case("t2_20x12_noncontig", None, None, "rebk", 1.0, 11, rp, cp, max_iters=3000, tol=1e-10, problem=p)
+    # underdetermined rank-deficient (type 1)
+    a = K.gen_type1(30, 50, 12, 3.0, seed=50)
+    p = K.make_rhs(a, seed=51, inconsistent=True)
+    rp, cp = K.contiguous_partition(30, 6, "row"), K.contiguous_partition(50, 10, "col")
+    beta = compute_beta_max(p.a, rp, cp)[2]
+    small_case("t1_30x50_rebk", None, None, "rebk", 1.75 / beta, 13, rp, cp, max_iters=20000, tol=1e-9,
+               problem=p, stride=5)
+
+
+def big_case(name, a, b, x_star, tau_r, tau_c, beta, seed=17, rel=1e-6, max_iters=50_000,
+             ks=(1, 10, 100), store_b=False):
+    mat = K.Matrix.from_dense(a)
+    prob = K.ProblemInstance(a=mat, b=b, x_star=x_star, b_perp=None, meta=K.ProblemMeta(0, None, False, 0, 0.0))
+    rp = K.contiguous_partition(a.shape[0], tau_r, "row")
+    cp = K.contiguous_partition(a.shape[1], tau_c, "col")
+    alpha = 1.0 / beta
+    tol = rel * float(np.linalg.norm(x_star))
+    cfg = K.SolverConfig(algorithm="rebk", alpha=alpha, seed=seed, row_partition=rp, col_partition=cp,
+                         max_iters=max_iters, stop=K.StoppingRule(tol=tol), beta_max=beta)
+    t0 = time.time()
+    tr = K.run(prob, cfg)
+    print(f"{name}: ITER={tr.iters} conv={tr.converged} err={tr.final_error} wall={tr.wall_time:.2f}s "
+          f"({time.time() - t0:.1f}s)")
+    ks = tuple(ks) + (tr.iters,)
+    ctx, xs, zs = snapshots(prob, K.SolverConfig(algorithm="rebk", alpha=alpha, seed=seed, row_partition=rp,
+                                                 col_partition=cp, max_iters=tr.iters, beta_max=beta,
+                                                 stop=K.StoppingRule(mode="max_iters_only")), ks)
+    out = dict(alpha=alpha, beta=beta, seed=seed, tol=tol, iters=tr.iters, final_error=tr.final_error,
+               ref_wall=tr.wall_time, picks=ref_picks(ctx, seed, tr.iters).astype(np.int16),
+               ks=np.asarray(ks), x_star=x_star, row_cum=ctx.row_sampler.cumulative,
+               col_cum=ctx.col_sampler.cumulative, tau=np.asarray([tau_r, tau_c]))
+    if store_b:
+        out["b"] = b
+    for k in ks:
+        out[f"x_{k}"] = xs[k]
+        out[f"z_{k}"] = zs[k]
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+
+
+def c1():
+    a, b, xs = workloads.c1_arrays()
+    assert np.array_equal(a, workloads.c1_matrix())
+    rp, cp = K.contiguous_partition(2000, 100, "row"), K.contiguous_partition(500, 100, "col")
+    t0 = time.time()
+    beta = compute_beta_max(K.Matrix.from_dense(a), rp, cp)[2]  # the reference's Jacobi-SVD rule
+    print(f"c1 beta_max={beta} ({time.time() - t0:.1f}s)")
+    big_case("c1_golden", a, b, xs, 100, 100, beta, store_b=True)
+
+
+def c2():
+    a, b, xs = workloads.c2_arrays()
+    rp, cp = K.contiguous_partition(4000, 200, "row"), K.contiguous_partition(10000, 200, "col")
+    from paper_2001_04179_b200.solvers import compute_beta_max as gram_beta
+    from paper_2001_04179_b200 import Matrix as M2, contiguous_partition as cpart
+    beta = gram_beta(M2.from_dense(a), cpart(4000, 200, "row"), cpart(10000, 200, "col"))[2]
+    print(f"c2 beta_max={beta}")
+    big_case("c2_golden", a, b, xs, 200, 200, beta, ks=(1, 10, 100, 1000))
+
+
+if __name__ == "__main__":
+    philox_fixture()
+    small_cases()
+    if "--small-only" in sys.argv:
+        sys.exit(0)
+    c1()
+    if "--skip-c2" not in sys.argv:
+        c2()

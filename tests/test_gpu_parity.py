@@ -1,0 +1,316 @@
+"""Parity of the B200 path (librebk.so) with the reference, through the
+public API and the C ABI.
+
+Gates (BASELINE.json north_star): block-index sequence bit-exact; x, z
+within 1e-10 relative (fp64); ITER equal; bitwise run-to-run replay.
+Golden vectors come from the reference itself (tests/golden/gen_golden.py);
+the oracle restatement checks the same instance in-process.
+"""
+
+import ctypes
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import paper_2001_04179_b200 as P
+from paper_2001_04179_b200 import _lib
+from oracle.rebk_oracle import OracleRng, OracleSolver
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+RTOL = 1e-10  # fp64 iterate tolerance stated by the north star
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    assert _lib.device_count() > 0, "gpu tests need a CUDA device (no CPU fallback exists)"
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name), allow_pickle=True)
+
+
+def case_problem(g):
+    a = g["a"]
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=g["b"], x_star=g["x_star"], b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    algo = str(g["algorithm"])
+    rb = [np.asarray(b, dtype=np.int64) for b in g["row_blocks"]]
+    rp = P.Partition("row", a.shape[0], tuple(rb)) if algo not in ("rk", "rek") else None
+    cp = None
+    if "col_blocks" in g.files and algo not in ("rk", "rek"):
+        cp = P.Partition("col", a.shape[1], tuple(np.asarray(b, dtype=np.int64) for b in g["col_blocks"]))
+    z0 = g["z0"] if "z0" in g.files else None
+    cfg = P.SolverConfig(algorithm=algo, alpha=float(g["alpha"]), row_partition=rp, col_partition=cp,
+                         seed=int(g["seed"]), max_iters=int(g["max_iters"]),
+                         stop=P.StoppingRule(mode=str(g["mode"]), tol=float(g["tol"]),
+                                             check_stride=int(g["stride"])),
+                         record_errors=True, z0=z0, beta_max=1e-300)
+    return prob, cfg
+
+
+CASES = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLD, "case_*.npz")))
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_run_matches_reference_case(case):
+    g = load(case)
+    prob, cfg = case_problem(g)
+    tr = P.run(prob, cfg)
+    assert tr.iters == int(g["iters"])
+    assert tr.converged == bool(g["converged"])
+    if str(g["mode"]) == "max_iters_only":
+        assert tr.final_error is None and tr.errors is None
+    else:
+        assert tr.final_error == pytest.approx(float(g["final_error"]), rel=1e-9, abs=1e-13)
+        assert np.array_equal(tr.checkpoints, g["checkpoints"])
+        np.testing.assert_allclose(tr.errors, g["errors"], rtol=1e-9, atol=1e-13)
+    k = int(g["iters"])
+    if f"x_{k}" in g.files:
+        assert rel(tr.x, g[f"x_{k}"]) <= RTOL
+        if tr.z is not None:
+            assert rel(tr.z, g[f"z_{k}"]) <= RTOL
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_step_snapshots_match_reference_case(case):
+    g = load(case)
+    prob, cfg = case_problem(g)
+    ctx = P.prepare(prob, cfg)
+    st = ctx.initial_state()
+    ks = set(int(k) for k in g["ks"])
+    for k in range(1, max(ks) + 1):
+        ctx.step(st)
+        if k in ks:
+            assert rel(st.x, g[f"x_{k}"]) <= RTOL, k
+            if st.z is not None:
+                assert rel(st.z, g[f"z_{k}"]) <= RTOL, k
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_device_sampler_sequence_bit_exact(case):
+    g = load(case)
+    prob, cfg = case_problem(g)
+    ctx = P.prepare(prob, cfg)
+    want = g["picks"].astype(np.int32)
+    c = ctx.make_cfg(stop_mode="max_iters_only", tol=1.0, stride=1, max_iters=len(want),
+                     key=_lib.philox_key(int(g["seed"])))
+    out = np.empty((len(want), 2), dtype=np.int32)
+    rc = _lib.load().rebk_sample_sequence(ctypes.byref(c), 1, len(want),
+                                          out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    _lib.check(rc, "rebk_sample_sequence")
+    assert np.array_equal(out, want)
+
+
+def test_hand_values_identity():
+    # test_solvers.py:307-316
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(np.eye(2)), b=np.array([1.0, 2.0]), x_star=None,
+                             b_perp=None, meta=P.ProblemMeta(0, None, True, 0, 0.0))
+    cfg = P.SolverConfig(algorithm="rebk", alpha=1.0, seed=0, row_partition=P.contiguous_partition(2, 2, "row"),
+                         col_partition=P.contiguous_partition(2, 2, "col"), beta_max=1.0)
+    ctx = P.prepare(prob, cfg)
+    st = ctx.initial_state()
+    ctx.step(st)
+    assert np.allclose(st.z, [0.5, 1.0], atol=1e-15)
+    assert np.allclose(st.x, [0.25, 0.5], atol=1e-15)
+
+
+class ScriptedRng:
+    def __init__(self, values):
+        self.values = list(values)
+
+    def uniform(self):
+        return self.values.pop(0)
+
+
+def test_scripted_rek_hand_formula():
+    # test_solvers.py:92-109
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((5, 3))
+    b = rng.standard_normal(5)
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=b, x_star=None, b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    ctx = P.prepare(prob, P.SolverConfig(algorithm="rek", seed=0, beta_max=1.0))
+    st = ctx.initial_state()
+    st.x = rng.standard_normal(3)
+    x_before, z_before = st.x.copy(), st.z.copy()
+    st.rng = ScriptedRng([0.0, 0.0])
+    ctx.step(st)
+    col = a[:, 0]
+    z_want = z_before - (col @ z_before) / (col @ col) * col
+    row = a[0]
+    x_want = x_before - (row @ x_before - b[0] + z_want[0]) / (row @ row) * row
+    assert np.allclose(st.z, z_want, rtol=1e-13)
+    assert np.allclose(st.x, x_want, rtol=1e-13)
+
+
+def test_scripted_rk_hand_formula():
+    # test_solvers.py:75-89
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((6, 4))
+    b = rng.standard_normal(6)
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=b, x_star=None, b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    ctx = P.prepare(prob, P.SolverConfig(algorithm="rk", alpha=0.8, seed=0, beta_max=1.0))
+    st = ctx.initial_state()
+    st.x = rng.standard_normal(4)
+    xb = st.x.copy()
+    st.rng = ScriptedRng([0.5, 0.0])
+    ctx.step(st)
+    row = a[0]
+    want = xb - 0.8 * (row @ xb - b[0]) / (row @ row) * row
+    assert np.allclose(st.x, want, rtol=1e-13)
+
+
+def small_problem(m, n, seed):
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((m, n))
+    b = rng.standard_normal(m)
+    xs = np.linalg.lstsq(a, b, rcond=None)[0]
+    return P.ProblemInstance(a=P.Matrix.from_dense(a), b=b, x_star=xs, b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, seed, 0.0))
+
+
+def test_rek_equals_singleton_rebk_bitwise():
+    # test_solvers.py:136-151 (bitwise over 1000 steps, via whole runs)
+    p = small_problem(12, 7, 2)
+    cfg_rek = P.SolverConfig(algorithm="rek", alpha=1.0, seed=17, max_iters=1000,
+                             stop=P.StoppingRule(mode="max_iters_only"), beta_max=1.0)
+    cfg_rebk = P.SolverConfig(algorithm="rebk", alpha=1.0, seed=17, max_iters=1000,
+                              row_partition=P.singleton_partition(12, "row"),
+                              col_partition=P.singleton_partition(7, "col"),
+                              stop=P.StoppingRule(mode="max_iters_only"), beta_max=1.0)
+    t1, t2 = P.run(p, cfg_rek), P.run(p, cfg_rebk)
+    assert np.array_equal(t1.x, t2.x) and np.array_equal(t1.z, t2.z)
+
+
+def test_rebk_zero_z_equals_rabk_bitwise():
+    # test_solvers.py:249-265 and :318-329
+    p = small_problem(14, 9, 12)
+    rp, cp = P.contiguous_partition(14, 3, "row"), P.contiguous_partition(9, 3, "col")
+    mk = dict(alpha=1.4, seed=33, max_iters=1000, stop=P.StoppingRule(mode="max_iters_only"), beta_max=1.0)
+    t1 = P.run(p, P.SolverConfig(algorithm="rabk", row_partition=rp, **mk))
+    t2 = P.run(p, P.SolverConfig(algorithm="rebk", row_partition=rp, col_partition=cp, z0=np.zeros(14), **mk))
+    assert not t2.z.any()
+    assert np.array_equal(t1.x, t2.x)
+
+
+def test_replay_determinism_bitwise():
+    # test_solvers.py:452-459, on a grid-sized problem so many CTAs reduce
+    from paper_2001_04179_b200.workloads import c1_matrix
+
+    g = load("c1_golden.npz")
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(c1_matrix()), b=g["b"], x_star=g["x_star"], b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    cfg = P.SolverConfig(algorithm="rebk", alpha=1.2 * float(g["alpha"]), seed=7, max_iters=300,
+                         row_partition=P.contiguous_partition(2000, 100, "row"),
+                         col_partition=P.contiguous_partition(500, 100, "col"),
+                         stop=P.StoppingRule(tol=1e-300), beta_max=float(g["beta"]))
+    t1, t2 = P.run(prob, cfg), P.run(prob, cfg)
+    assert t1.iters == t2.iters
+    assert t1.final_error == t2.final_error
+    assert np.array_equal(t1.x, t2.x) and np.array_equal(t1.z, t2.z)
+    assert t1.grid_ctas > 1
+
+
+def test_staged_and_unstaged_tiles_agree_bitwise(monkeypatch):
+    from paper_2001_04179_b200.workloads import c1_matrix
+
+    g = load("c1_golden.npz")
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(c1_matrix()), b=g["b"], x_star=g["x_star"], b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=17, max_iters=200,
+                         row_partition=P.contiguous_partition(2000, 100, "row"),
+                         col_partition=P.contiguous_partition(500, 100, "col"),
+                         stop=P.StoppingRule(mode="max_iters_only"), beta_max=float(g["beta"]))
+    t1 = P.run(prob, cfg)
+    monkeypatch.setenv("REBK_NO_STAGE", "1")
+    t2 = P.run(prob, cfg)
+    assert np.array_equal(t1.x, t2.x) and np.array_equal(t1.z, t2.z)
+
+
+def c1_instance():
+    from paper_2001_04179_b200.workloads import c1_matrix
+
+    g = load("c1_golden.npz")
+    a = c1_matrix()
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=g["b"], x_star=g["x_star"], b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    rp, cp = P.contiguous_partition(2000, 100, "row"), P.contiguous_partition(500, 100, "col")
+    cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=int(g["seed"]), max_iters=50_000,
+                         row_partition=rp, col_partition=cp, stop=P.StoppingRule(tol=float(g["tol"])),
+                         beta_max=float(g["beta"]))
+    return g, a, prob, cfg
+
+
+def test_c1_full_run_matches_reference():
+    g, a, prob, cfg = c1_instance()
+    tr = P.run(prob, cfg)
+    k = int(g["iters"])
+    assert tr.converged and tr.iters == k == 547
+    assert rel(tr.x, g[f"x_{k}"]) <= RTOL
+    assert rel(tr.z, g[f"z_{k}"]) <= RTOL
+    assert tr.final_error == pytest.approx(float(g["final_error"]), rel=1e-9)
+    # in-process oracle on the same instance
+    orc = OracleSolver(a, g["b"], np.arange(0, 2001, 100), np.arange(0, 501, 100), float(g["alpha"]))
+    res = orc.run(int(g["seed"]), 50_000, float(g["tol"]), g["x_star"])
+    assert res["iters"] == tr.iters
+    assert rel(tr.x, res["x"]) <= RTOL and rel(tr.z, res["z"]) <= RTOL
+
+
+def test_c1_step_snapshots():
+    g, a, prob, cfg = c1_instance()
+    ctx = P.prepare(prob, cfg)
+    st = ctx.initial_state()
+    for k in range(1, 101):
+        ctx.step(st)
+        if k in (1, 10, 100):
+            assert rel(st.x, g[f"x_{k}"]) <= RTOL
+            assert rel(st.z, g[f"z_{k}"]) <= RTOL
+
+
+def test_device_block_norms_match_host():
+    _, a, prob, cfg = c1_instance()
+    dm = prob.a.device()
+    for axis, ptr, sl in ((0, np.arange(0, 2001, 100), lambda lo, hi: a[lo:hi]),
+                          (1, np.arange(0, 501, 100), lambda lo, hi: a[:, lo:hi])):
+        got = dm.block_frobenius_sq(axis, ptr)
+        want = np.array([np.sum(sl(lo, hi) ** 2) for lo, hi in zip(ptr[:-1], ptr[1:])])
+        np.testing.assert_allclose(got, want, rtol=1e-13)
+
+
+@pytest.mark.slow
+def test_c2_full_run_matches_reference():
+    """BASELINE config 2 (the bench workload): 4000 x 10000, rank 2000,
+    blocks 200/200, alpha = 1/beta_max, to ||x - x*|| <= 1e-6 ||x*||."""
+    from paper_2001_04179_b200.workloads import c2_arrays
+
+    g = load("c2_golden.npz")
+    a, b, xs = c2_arrays()
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=b, x_star=xs, b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    rp, cp = P.contiguous_partition(4000, 200, "row"), P.contiguous_partition(10000, 200, "col")
+    cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=int(g["seed"]), max_iters=50_000,
+                         row_partition=rp, col_partition=cp, stop=P.StoppingRule(tol=float(g["tol"])),
+                         beta_max=float(g["beta"]))
+    ctx = P.prepare(prob, cfg)
+    want = g["picks"].astype(np.int32)
+    c = ctx.make_cfg(stop_mode="max_iters_only", tol=1.0, stride=1, max_iters=len(want),
+                     key=_lib.philox_key(int(g["seed"])))
+    out = np.empty((len(want), 2), dtype=np.int32)
+    _lib.check(_lib.load().rebk_sample_sequence(ctypes.byref(c), 1, len(want),
+                                                 out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))), "sample")
+    assert np.array_equal(out, want)
+    tr = P.run(prob, cfg)
+    k = int(g["iters"])
+    assert tr.converged and tr.iters == k
+    assert rel(tr.x, g[f"x_{k}"]) <= RTOL
+    assert rel(tr.z, g[f"z_{k}"]) <= RTOL
