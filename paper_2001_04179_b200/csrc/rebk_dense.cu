@@ -497,14 +497,24 @@ __global__ void __launch_bounds__(kThreads, 1) rebk_dense_kernel(DenseParams p) 
   __syncthreads();
 }
 
+static cudaError_t set_smem_attr() {
+  static int configured_device = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (configured_device == dev) return cudaSuccess;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  // leave room for the kernel's static shared memory (mbarriers, broadcast)
+  e = cudaFuncSetAttribute(rebk_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+  if (e == cudaSuccess) configured_device = dev;
+  return e;
+}
+
 cudaError_t launch_dense(const DenseParams& p, int G, size_t smem_bytes, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(rebk_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kSmemBudget + 8 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = set_smem_attr();
+  if (e != cudaSuccess) return e;
   DenseParams pc = p;
   void* args[] = {&pc};
   return cudaLaunchCooperativeKernel((const void*)rebk_dense_kernel, dim3(G), dim3(kThreads), args,
@@ -512,8 +522,7 @@ cudaError_t launch_dense(const DenseParams& p, int G, size_t smem_bytes, cudaStr
 }
 
 cudaError_t dense_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm) {
-  cudaError_t e = cudaFuncSetAttribute(rebk_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kSmemBudget + 8 * 1024);
+  cudaError_t e = set_smem_attr();
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, rebk_dense_kernel, kThreads,
                                                        smem_bytes);

@@ -8,7 +8,7 @@ namespace rebk {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 // dynamic shared memory we are willing to ask for (227 KB max per CTA on B200)
-constexpr int kSmemBudget = 220 * 1024;
+constexpr int kSmemBudget = 218 * 1024;
 
 // One iteration's resolved picks (32 bytes): the column block [c_lo, c_hi)
 // with its scale alpha/||A_{:,J}||_F^2 and the row block [r_lo, r_hi) with
