@@ -248,7 +248,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         tr = device_solve()
     log(f"[bench] warm-up solve: ITER={tr.iters} converged={bool(tr.converged)} "
-        f"loop={tr.loop_ms:.3f} ms grid={tr.grid_ctas}")
+        f"loop={tr.loop_ms:.3f} ms grid={tr.grid_ctas} path={tr.kernel_path}")
 
     clocks = ClockSampler(local)
     barrier()
@@ -331,12 +331,15 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {**workload_desc(args.workload, wl), "parallelism": f"replicas x{ws}",
-                       "iters_per_solve": per_solve_iters, "grid_ctas": int(tr.grid_ctas)},
+                       "iters_per_solve": per_solve_iters, "grid_ctas": int(tr.grid_ctas),
+                       "kernel_path": ["rebk_dense_kernel", "rebk_dense_fast_kernel (cluster)",
+                                       "rebk_dense_fast_kernel (cluster, cooperative)"][int(tr.kernel_path)]},
             "time_to_tol_s": ms_max / args.steps / 1e3,
             "achieved_gbps": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "rebk_dense_kernel", "peak_source": peak_src,
+                         "kernel": "rebk_dense_fast_kernel" if tr.kernel_path else "rebk_dense_kernel",
+                         "peak_source": peak_src,
                          "algorithmic_bytes_per_iter": bytes_per_iter,
                          "iters_per_launch": per_solve_iters, "kernel_ms_per_launch": kernel_ms},
             "cpu_baseline": cpu,

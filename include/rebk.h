@@ -102,7 +102,7 @@ typedef struct rebk_trace {
   int64_t errors_cap;
   int64_t n_checks;
   int32_t grid_ctas;        /* CTAs the persistent kernel used */
-  int32_t reserved;
+  int32_t kernel_path;      /* 0 general kernel, 1 clustered fast path, 2 same, cooperative launch */
 } rebk_trace;
 
 /* ---- library / device ---------------------------------------------------- */

@@ -14,7 +14,7 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint3
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librebk.so")
+LIB_PATH = os.environ.get("REBK_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "librebk.so")
 
 REBK_OK = 0
 ERRORS = {
@@ -66,7 +66,7 @@ class RebkTrace(ctypes.Structure):
         ("errors_cap", c_int64),
         ("n_checks", c_int64),
         ("grid_ctas", c_int32),
-        ("reserved", c_int32),
+        ("kernel_path", c_int32),
     ]
 
 

@@ -160,6 +160,91 @@ Geometry plan_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int G, bool ext
   return g;
 }
 
+// ---- fast path (rebk_dense_fast.cu) -------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+
+bool encode_box(CUtensorMap* map, const rebk_ctx* ctx, int box_w, int box_h) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)ctx->n, (cuuint64_t)ctx->m};
+  cuuint64_t gstride[1] = {(cuuint64_t)ctx->lda * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)ctx->A, gdim, gstride, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int round_even(int v) { return (v + 1) & ~1; }
+
+struct FastGeometry {
+  bool ok = false;
+  int G = 0, CS = 0, NC = 0;
+  int nR_max = 0, nC_max = 0, nJ_max = 0, nI_max = 0;
+  int ct_box_w = 0, ct_box_h = 0, rt_box_w = 0, rt_box_h = 0;
+  int pad_nC = 0, pad_nR = 0, pad_ne = 0, pad_in = 0, pad_cin = 0;
+  int ct_off = 0, rt_off = 0, vec_off = 0;
+  size_t smem_bytes = 0;
+};
+
+FastGeometry fast_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int NC, int CS) {
+  FastGeometry f;
+  f.CS = CS;
+  f.NC = NC;
+  f.G = NC * CS;
+  const int G = f.G;
+  for (int q = 0; q < G; ++q) {
+    f.nR_max = std::max(f.nR_max, split_rows(ctx->m, G, q + 1) - split_rows(ctx->m, G, q));
+    f.nC_max = std::max(f.nC_max, split_even(ctx->n, G, q + 1) - split_even(ctx->n, G, q));
+  }
+  f.nI_max = max_block(cfg->n_row_blocks, cfg->row_ptr);
+  f.nJ_max = extended ? max_block(cfg->n_col_blocks, cfg->col_ptr) : 0;
+  f.ct_box_w = extended ? std::max(2, round_even(f.nJ_max)) : 2;
+  f.ct_box_h = extended ? std::max(1, f.nR_max) : 1;
+  f.rt_box_w = std::max(2, round_even(f.nC_max));
+  if (f.rt_box_w % 4 == 0) f.rt_box_w += 2;  // ≡ 2 (mod 4) doubles: conflict-free row-parallel reads
+  f.rt_box_h = f.nI_max;
+  if (f.ct_box_w > 256 || f.ct_box_h > 256 || f.rt_box_w > 256 || f.rt_box_h > 256) return f;
+  const int ne_max = std::max(f.nJ_max, 2 * f.nI_max) + 1;
+  const int sl = (ne_max + CS - 1) / CS;
+  f.pad_nC = round_even(f.nC_max + 1);
+  f.pad_nR = round_even(f.nR_max + 1);
+  f.pad_ne = round_even(ne_max + 1);
+  f.pad_in = round_even(CS * sl);
+  f.pad_cin = round_even(NC * sl);
+  auto al16 = [](size_t v) { return (v + 15) & ~(size_t)15; };  // 128-byte alignment in doubles
+  size_t off = 0;
+  f.ct_off = (int)off;
+  off = al16(off + (size_t)f.ct_box_w * f.ct_box_h);
+  f.rt_off = (int)off;
+  off = al16(off + (size_t)f.rt_box_w * f.rt_box_h);
+  f.vec_off = (int)off;
+  off += 2 * (size_t)f.pad_nC + f.pad_nR + 3 * (size_t)f.pad_ne + f.pad_in + f.pad_cin + 2 * kThreads;
+  f.smem_bytes = off * sizeof(double);
+  f.ok = f.smem_bytes <= (size_t)kSmemBudget;
+  return f;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s ? atoi(s) : dflt;
+}
+
 int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev,
                     double* x_dev, double* z_dev, cudaStream_t stream, rebk_trace* trace) {
   const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
@@ -190,7 +275,38 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   if (G0 > occ * ctx->sm_count) {
     geo = plan_geometry(ctx, cfg, occ * ctx->sm_count, extended);
   }
-  const int G = geo.G;
+  // fast path: clustered kernel (oracle_error / max_iters_only, TMA-able tiles,
+  // at least one full cluster).  The choice depends only on the problem shape,
+  // partitions and stopping mode, so repeated runs take the same path.
+  FastGeometry fg;
+  bool use_fast = false;
+  bool fast_coop = true;
+  CUtensorMap tm_ct, tm_rt;
+  {
+    const int CS = env_int("REBK_CLUSTER", 8);
+    const bool aligned = (ctx->lda % 2 == 0) && ((uintptr_t)ctx->A % 16 == 0);
+    if (env_int("REBK_NO_FAST", 0) == 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY && aligned && CS >= 1 &&
+        G0 >= CS && encode_fn() != nullptr) {
+      int NC = std::max(1, G0 / CS);
+      for (int attempt = 0; attempt < 3 && NC >= 1; ++attempt) {
+        fg = fast_geometry(ctx, cfg, extended, NC, CS);
+        if (!fg.ok) break;
+        int maxc = 0;
+        if (fast_max_clusters(CS, fg.smem_bytes, &maxc) != cudaSuccess || maxc < 1) {
+          fg.ok = false;
+          cudaGetLastError();
+          break;
+        }
+        if (NC <= maxc) break;
+        NC = maxc;
+      }
+      if (fg.ok && fg.NC == NC) {
+        use_fast = encode_box(&tm_ct, ctx, fg.ct_box_w, fg.ct_box_h) &&
+                   encode_box(&tm_rt, ctx, fg.rt_box_w, fg.rt_box_h);
+      }
+    }
+  }
+  const int G = use_fast ? fg.G : geo.G;
 
   DevArena arena;
   arena.stream = stream;
@@ -228,10 +344,23 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   CUDA_TRY(arena.alloc(&d_u, std::max(geo.nJ_max, 1)));
   CUDA_TRY(arena.alloc(&d_r, std::max(geo.nI_max, 1)));
   CUDA_TRY(arena.alloc(&d_errpart, G));
+  LLWord *d_cpu = nullptr, *d_cpr = nullptr;
+  if (use_fast) {
+    CUDA_TRY(arena.alloc(&d_cpu, (size_t)fg.NC * (fg.nJ_max + 1)));
+    CUDA_TRY(arena.alloc(&d_cpr, (size_t)fg.NC * (2 * fg.nI_max + 1)));
+    CUDA_TRY(cudaMemsetAsync(d_cpu, 0, (size_t)fg.NC * (fg.nJ_max + 1) * sizeof(LLWord), stream));
+    CUDA_TRY(cudaMemsetAsync(d_cpr, 0, (size_t)fg.NC * (2 * fg.nI_max + 1) * sizeof(LLWord), stream));
+  }
   if (cfg->stop_mode == REBK_STOP_RESIDUAL_PROXY) CUDA_TRY(arena.alloc(&d_res, ctx->m));
   const int64_t errs_cap = (cfg->record_errors && trace && trace->errors) ? trace->errors_cap : 0;
   if (errs_cap > 0) CUDA_TRY(arena.alloc(&d_errs, errs_cap));
   CUDA_TRY(arena.alloc(&d_ctl, 1));
+  const char* prof_env = getenv("REBK_PROF");
+  long long* d_prof = nullptr;
+  if (prof_env && prof_env[0] == '1') {
+    CUDA_TRY(arena.alloc(&d_prof, (size_t)G * 16));
+    CUDA_TRY(cudaMemsetAsync(d_prof, 0, (size_t)G * 16 * 8, stream));
+  }
   CUDA_TRY(cudaMemsetAsync(d_ctl, 0, sizeof(Control), stream));
 
   SampleParams sp{};
@@ -270,6 +399,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   p.errs_cap = errs_cap;
   p.plan = d_plan;
   p.ctl = d_ctl;
+  p.prof = d_prof;
   p.extended = extended;
   p.stop_mode = cfg->stop_mode;
   p.tol = cfg->tol;
@@ -289,6 +419,31 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   p.rt_off = geo.rt_off;
   p.vec_off = geo.vec_off;
 
+  FastParams fpar{};
+  if (use_fast) {
+    p.nJ_max = fg.nJ_max;
+    p.nI_max = fg.nI_max;
+    p.nR_max = fg.nR_max;
+    p.nC_max = fg.nC_max;
+    p.ct_off = fg.ct_off;
+    p.rt_off = fg.rt_off;
+    p.vec_off = fg.vec_off;
+    p.stage_ct = p.stage_rt = 1;
+    fpar.cpart_u = d_cpu;
+    fpar.cpart_r = d_cpr;
+    fpar.stride_u = fg.nJ_max + 1;
+    fpar.stride_r = 2 * fg.nI_max + 1;
+    fpar.ct_box_w = fg.ct_box_w;
+    fpar.ct_box_h = fg.ct_box_h;
+    fpar.rt_box_w = fg.rt_box_w;
+    fpar.rt_box_h = fg.rt_box_h;
+    fpar.pad_nC = fg.pad_nC;
+    fpar.pad_nR = fg.pad_nR;
+    fpar.pad_ne = fg.pad_ne;
+    fpar.pad_in = fg.pad_in;
+    fpar.pad_cin = fg.pad_cin;
+    fpar.cluster_size = fg.CS;
+  }
   cudaEvent_t ev0, ev1;
   CUDA_TRY(cudaEventCreate(&ev0));
   CUDA_TRY(cudaEventCreate(&ev1));
@@ -300,7 +455,21 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     if (err == cudaSuccess) err = cudaMemsetAsync(&d_ctl->bar, 0, sizeof(unsigned long long), stream);
     p.k_begin = k;
     p.k_end = k + count - 1;
-    if (err == cudaSuccess) err = launch_dense(p, G, geo.smem_bytes, stream);
+    if (err == cudaSuccess) {
+      if (use_fast) {
+        fpar.d = p;
+        err = launch_dense_fast(fpar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
+        if (err != cudaSuccess && fast_coop) {
+          // cooperative + cluster launch refused: the grid is sized to the
+          // co-resident cluster capacity, launch it as a plain cluster grid
+          cudaGetLastError();
+          fast_coop = false;
+          err = launch_dense_fast(fpar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
+        }
+      } else {
+        err = launch_dense(p, G, geo.smem_bytes, stream);
+      }
+    }
     k += std::max<int64_t>(count, 1);
     if (err == cudaSuccess && k <= cfg->max_iters) {
       int32_t done = 0;
@@ -322,6 +491,26 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   if (err != cudaSuccess) return fail(REBK_ECUDA, "REBK run failed: %s", cudaGetErrorString(err));
+  if (ctl.fault) return fail(REBK_ECUDA, "clustered kernel launched without its %d-CTA clusters", fg.CS);
+  if (d_prof) {
+    std::vector<long long> h((size_t)G * 16);
+    cudaMemcpy(h.data(), d_prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx->device);
+    const double it = (double)std::max<int64_t>(1, ctl.iters);
+    fprintf(stderr, "[rebk prof] path=%s ", use_fast ? (fast_coop ? "fast(coop)" : "fast") : "v1");
+    fprintf(stderr, "[rebk prof] G=%d iters=%lld loop=%.3f ms (%.3f us/iter); per-iteration us: mark mean max\n", G,
+            (long long)ctl.iters, ms, 1e3 * ms / it);
+    for (int i = 0; i < 16; ++i) {
+      double mean = 0, mx = 0;
+      for (int q = 0; q < G; ++q) {
+        const double v = (double)h[(size_t)q * 16 + i] / (khz * 1e-3) / it;
+        mean += v / G;
+        mx = std::max(mx, v);
+      }
+      if (mx > 0) fprintf(stderr, "[rebk prof] %2d %8.3f %8.3f\n", i, mean, mx);
+    }
+  }
   if (trace) {
     trace->iters = ctl.iters;
     trace->converged = ctl.converged;
@@ -330,6 +519,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     trace->loop_ms = ms;
     trace->n_checks = ctl.n_checks;
     trace->grid_ctas = G;
+    trace->kernel_path = use_fast ? (fast_coop ? 2 : 1) : 0;
   }
   return REBK_OK;
 }

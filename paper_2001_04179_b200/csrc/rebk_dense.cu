@@ -20,177 +20,10 @@
 #include <stdint.h>
 
 #include "philox.h"
+#include "rebk_device.cuh"
 #include "rebk_internal.h"
 
 namespace rebk {
-
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned long long v;
-    while (true) {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-      if (v >= target) break;
-    }
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-// ------------------------------------------------------------------ loaders
-struct LdShared {
-  static __device__ __forceinline__ double ld(const double* p) { return *p; }
-};
-struct LdNC {  // immutable A: read-only path
-  static __device__ __forceinline__ double ld(const double* p) { return __ldg(p); }
-};
-struct LdCG {  // state written by other CTAs during this launch: L2 only
-  static __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
-};
-
-__device__ __forceinline__ int pow2floor(int v) {
-  int p = 1;
-  while (p * 2 <= v) p *= 2;
-  return p;
-}
-
-// out[c] = Σ_{r<R} T[r*ld + c] · v[r]  (c < C), handed to epi(c, value).
-// The thread layout depends on (R, C) only, so staged and unstaged tiles give
-// identical bits.
-template <typename TA, typename TV, typename Epi>
-__device__ __forceinline__ void tile_colsum(const double* __restrict__ T, int64_t ld, int R, int C,
-                                            const double* __restrict__ v, double* red, Epi epi) {
-  const int tid = threadIdx.x;
-  if (C <= 0) return;
-  if (C >= kThreads / 2) {
-    for (int c = tid; c < C; c += kThreads) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int r = 0;
-      for (; r + 4 <= R; r += 4) {
-        a0 = fma(TA::ld(T + (int64_t)(r + 0) * ld + c), TV::ld(v + r + 0), a0);
-        a1 = fma(TA::ld(T + (int64_t)(r + 1) * ld + c), TV::ld(v + r + 1), a1);
-        a2 = fma(TA::ld(T + (int64_t)(r + 2) * ld + c), TV::ld(v + r + 2), a2);
-        a3 = fma(TA::ld(T + (int64_t)(r + 3) * ld + c), TV::ld(v + r + 3), a3);
-      }
-      for (; r < R; ++r) a0 = fma(TA::ld(T + (int64_t)r * ld + c), TV::ld(v + r), a0);
-      epi(c, (a0 + a1) + (a2 + a3));
-    }
-  } else {
-    const int RG = kThreads / C;  // >= 2 row groups
-    const int c = tid % C, rg = tid / C;
-    double a0 = 0.0, a1 = 0.0;
-    if (rg < RG) {
-      int r = rg;
-      for (; r + RG < R; r += 2 * RG) {
-        a0 = fma(TA::ld(T + (int64_t)r * ld + c), TV::ld(v + r), a0);
-        a1 = fma(TA::ld(T + (int64_t)(r + RG) * ld + c), TV::ld(v + r + RG), a1);
-      }
-      if (r < R) a0 = fma(TA::ld(T + (int64_t)r * ld + c), TV::ld(v + r), a0);
-    }
-    __syncthreads();
-    if (rg < RG) red[tid] = a0 + a1;
-    __syncthreads();
-    if (tid < C) {
-      double s = 0.0;
-      for (int q = 0; q < RG; ++q) s += red[q * C + tid];
-      epi(tid, s);
-    }
-    __syncthreads();
-  }
-}
-
-// out[r] = Σ_{c<C} T[r*ld + c] · v[c]  (r < R), handed to epi(r, value) by
-// one lane per row.  L lanes per row, xor-butterfly reduction (every lane of
-// the group ends with the same bits).
-template <typename TA, typename TV, typename Epi>
-__device__ __forceinline__ void tile_rowdot(const double* __restrict__ T, int64_t ld, int R, int C,
-                                            const double* __restrict__ v, Epi epi) {
-  if (R <= 0) return;
-  const int tid = threadIdx.x;
-  int L = pow2floor(kThreads / R);
-  L = L < 2 ? 2 : (L > 32 ? 32 : L);
-  const int sub = tid % L, rsub = tid / L, rows_per_pass = kThreads / L;
-  for (int r0 = 0; r0 < R; r0 += rows_per_pass) {
-    const int r = r0 + rsub;
-    double a0 = 0.0, a1 = 0.0;
-    if (r < R && C > 0) {
-      const double* row = T + (int64_t)r * ld;
-      int c = sub;
-      for (; c + L < C; c += 2 * L) {
-        a0 = fma(TA::ld(row + c), TV::ld(v + c), a0);
-        a1 = fma(TA::ld(row + c + L), TV::ld(v + c + L), a1);
-      }
-      if (c < C) a0 = fma(TA::ld(row + c), TV::ld(v + c), a0);
-    }
-    double acc = a0 + a1;
-    for (int off = L / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (sub == 0 && r < R) epi(r, acc);
-  }
-}
-
-// Σ_{q<G} part[q]  for one warp, lane-strided then xor butterfly.
-__device__ __forceinline__ double warp_sum_cg(const double* part, int G) {
-  const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (int q = lane; q < G; q += 32) s += __ldcg(part + q);
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  return s;
-}
-
-// block-wide fixed-order sum (all threads must call)
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-  for (int w = 0; w < kWarps; ++w) s += red[w];
-  __syncthreads();
-  return s;
-}
 
 // stage rows [row0, row0+R) x cols [col0, col0+C) of A into tile (ld doubles)
 // with one bulk copy per row; bytes rounded up to 16 (the host guarantees the
@@ -340,6 +173,15 @@ __global__ void __launch_bounds__(kThreads, 1) rebk_dense_kernel(DenseParams p) 
     rt_pending = true;
   };
 
+  long long prof_acc[16];
+  for (int i = 0; i < 16; ++i) prof_acc[i] = 0;
+  long long prof_last = clock64();
+#define PROF(i)                                  \
+  if (p.prof) {                                  \
+    const long long _t = clock64();              \
+    prof_acc[i] += _t - prof_last;               \
+    prof_last = _t;                              \
+  }
   bool finished = false;
   // ---- check(0) (solvers.py:444)
   if (p.k_begin == 1 && checking) {
@@ -366,18 +208,22 @@ __global__ void __launch_bounds__(kThreads, 1) rebk_dense_kernel(DenseParams p) 
 
     __syncthreads();  // previous readers of the row tile are done
     issue_rt(pl);
+    PROF(0);
 
     if (p.extended) {
       // P1: partial u over owned rows
       const double* ct = p.stage_ct ? s_ct : p.A + (int64_t)zr0 * p.lda + cl;
       const int64_t ctld = p.stage_ct ? p.ct_ld : p.lda;
       wait_ct();
+      PROF(1);
       auto up_epi = [&](int c, double val) { __stcg(p.upart + (int64_t)c * G + g, val); };
       if (p.stage_ct)
         tile_colsum<LdShared, LdShared>(ct, ctld, nR, nJ, s_z, s_red, up_epi);
       else
         tile_colsum<LdNC, LdShared>(ct, ctld, nR, nJ, s_z, s_red, up_epi);
+      PROF(2);
       gsync();
+      PROF(3);
       // P2: pending stop decision, then u = Σ_g upart
       if (pending) {
         pending = false;
@@ -390,7 +236,9 @@ __global__ void __launch_bounds__(kThreads, 1) rebk_dense_kernel(DenseParams p) 
         const double s = warp_sum_cg(p.upart + (int64_t)e * G, G);
         if (lane == 0) __stcg(p.u + e, s);
       }
+      PROF(4);
       gsync();
+      PROF(5);
       // P3a: z[zr] -= s_J · A[zr, J] u
       for (int c = tid; c < nJ; c += kThreads) s_u[c] = __ldcg(p.u + c);
       __syncthreads();
@@ -405,18 +253,22 @@ __global__ void __launch_bounds__(kThreads, 1) rebk_dense_kernel(DenseParams p) 
       else
         tile_rowdot<LdNC, LdShared>(ct, ctld, nR, nJ, s_u, z_epi);
     }
+    PROF(6);
     // P3b: partial r over owned columns
     {
       const double* rt = p.stage_rt ? s_rt : p.A + (int64_t)rl * p.lda + xq0;
       const int64_t rtld = p.stage_rt ? p.rt_ld : p.lda;
       wait_rt();
+      PROF(7);
       auto rp_epi = [&](int r, double acc) { __stcg(p.rpart + (int64_t)r * G + g, acc); };
       if (p.stage_rt)
         tile_rowdot<LdShared, LdShared>(rt, rtld, nI, nC, s_x, rp_epi);
       else
         tile_rowdot<LdNC, LdShared>(rt, rtld, nI, nC, s_x, rp_epi);
     }
+    PROF(8);
     gsync();
+    PROF(9);
     // P4: (pending decision for row-only algorithms), r = ((Σ rpart) - b_I) + z_I
     if (!p.extended && pending) {
       pending = false;
@@ -434,7 +286,9 @@ __global__ void __launch_bounds__(kThreads, 1) rebk_dense_kernel(DenseParams p) 
         __stcg(p.r + e, rv);
       }
     }
+    PROF(10);
     gsync();
+    PROF(11);
     // P5: x[xq] -= s_I · A[I, xq]ᵀ r
     for (int c = tid; c < nI; c += kThreads) s_r[c] = __ldcg(p.r + c);
     __syncthreads();
@@ -449,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) rebk_dense_kernel(DenseParams p) 
         tile_colsum<LdNC, LdShared>(rt, rtld, nI, nC, s_r, s_red, x_epi);
     }
     __syncthreads();
+    PROF(12);
     if (check_k) {
       if (oracle) {
         oracle_partial();
@@ -488,6 +343,9 @@ __global__ void __launch_bounds__(kThreads, 1) rebk_dense_kernel(DenseParams p) 
       }
     }
   }
+  if (p.prof && tid == 0)
+    for (int i = 0; i < 16; ++i) p.prof[g * 16 + i] = prof_acc[i];
+#undef PROF
   // write back the owned x slice; drain any bulk copy still in flight
   for (int c = tid; c < nC; c += kThreads) __stcg(p.x + xq0 + c, s_x[c]);
   if (tid == 0) {

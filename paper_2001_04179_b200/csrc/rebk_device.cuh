@@ -1,0 +1,325 @@
+// rebk_device.cuh — device helpers shared by the REBK kernels (sm_100a):
+// grid barrier, mbarrier / bulk-copy / TMA PTX wrappers, tile products.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rebk_internal.h"
+
+namespace rebk {
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned long long v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ loaders
+struct LdShared {
+  static __device__ __forceinline__ double ld(const double* p) { return *p; }
+};
+struct LdNC {  // immutable A: read-only path
+  static __device__ __forceinline__ double ld(const double* p) { return __ldg(p); }
+};
+struct LdCG {  // state written by other CTAs during this launch: L2 only
+  static __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
+};
+
+__device__ __forceinline__ int pow2floor(int v) {
+  int p = 1;
+  while (p * 2 <= v) p *= 2;
+  return p;
+}
+
+// out[c] = Σ_{r<R} T[r*ld + c] · v[r]  (c < C), handed to epi(c, value).
+// The thread layout depends on (R, C) only, so staged and unstaged tiles give
+// identical bits.
+template <typename TA, typename TV, typename Epi>
+__device__ __forceinline__ void tile_colsum(const double* __restrict__ T, int64_t ld, int R, int C,
+                                            const double* __restrict__ v, double* red, Epi epi) {
+  const int tid = threadIdx.x;
+  if (C <= 0) return;
+  if (C >= kThreads / 2) {
+    for (int c = tid; c < C; c += kThreads) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int r = 0;
+      for (; r + 4 <= R; r += 4) {
+        a0 = fma(TA::ld(T + (int64_t)(r + 0) * ld + c), TV::ld(v + r + 0), a0);
+        a1 = fma(TA::ld(T + (int64_t)(r + 1) * ld + c), TV::ld(v + r + 1), a1);
+        a2 = fma(TA::ld(T + (int64_t)(r + 2) * ld + c), TV::ld(v + r + 2), a2);
+        a3 = fma(TA::ld(T + (int64_t)(r + 3) * ld + c), TV::ld(v + r + 3), a3);
+      }
+      for (; r < R; ++r) a0 = fma(TA::ld(T + (int64_t)r * ld + c), TV::ld(v + r), a0);
+      epi(c, (a0 + a1) + (a2 + a3));
+    }
+  } else {
+    const int RG = kThreads / C;  // >= 2 row groups
+    const int c = tid % C, rg = tid / C;
+    double a0 = 0.0, a1 = 0.0;
+    if (rg < RG) {
+      int r = rg;
+      for (; r + RG < R; r += 2 * RG) {
+        a0 = fma(TA::ld(T + (int64_t)r * ld + c), TV::ld(v + r), a0);
+        a1 = fma(TA::ld(T + (int64_t)(r + RG) * ld + c), TV::ld(v + r + RG), a1);
+      }
+      if (r < R) a0 = fma(TA::ld(T + (int64_t)r * ld + c), TV::ld(v + r), a0);
+    }
+    __syncthreads();
+    if (rg < RG) red[tid] = a0 + a1;
+    __syncthreads();
+    if (tid < C) {
+      double s = 0.0;
+      for (int q = 0; q < RG; ++q) s += red[q * C + tid];
+      epi(tid, s);
+    }
+    __syncthreads();
+  }
+}
+
+// out[r] = Σ_{c<C} T[r*ld + c] · v[c]  (r < R), handed to epi(r, value) by
+// one lane per row.  L lanes per row, xor-butterfly reduction (every lane of
+// the group ends with the same bits).
+template <typename TA, typename TV, typename Epi>
+__device__ __forceinline__ void tile_rowdot(const double* __restrict__ T, int64_t ld, int R, int C,
+                                            const double* __restrict__ v, Epi epi) {
+  if (R <= 0) return;
+  const int tid = threadIdx.x;
+  int L = pow2floor(kThreads / R);
+  L = L < 2 ? 2 : (L > 32 ? 32 : L);
+  const int sub = tid % L, rsub = tid / L, rows_per_pass = kThreads / L;
+  for (int r0 = 0; r0 < R; r0 += rows_per_pass) {
+    const int r = r0 + rsub;
+    double a0 = 0.0, a1 = 0.0;
+    if (r < R && C > 0) {
+      const double* row = T + (int64_t)r * ld;
+      int c = sub;
+      for (; c + L < C; c += 2 * L) {
+        a0 = fma(TA::ld(row + c), TV::ld(v + c), a0);
+        a1 = fma(TA::ld(row + c + L), TV::ld(v + c + L), a1);
+      }
+      if (c < C) a0 = fma(TA::ld(row + c), TV::ld(v + c), a0);
+    }
+    double acc = a0 + a1;
+    for (int off = L / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (sub == 0 && r < R) epi(r, acc);
+  }
+}
+
+// Σ_{q<G} part[q]  for one warp, lane-strided then xor butterfly.
+__device__ __forceinline__ double warp_sum_cg(const double* part, int G) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int q = lane; q < G; q += 32) s += __ldcg(part + q);
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
+}
+
+// block-wide fixed-order sum (all threads must call)
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < kWarps; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local_smem, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem), "r"(rank));
+  return r;
+}
+// DSMEM store that counts 8 bytes on the receiver's mbarrier (shared::cluster addresses)
+__device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uint32_t remote_mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(remote_addr),
+               "l"(__double_as_longlong(v)), "r"(remote_mbar)
+               : "memory");
+}
+// {value, seq} published as one 16-byte store; consumers poll the same word
+__device__ __forceinline__ void st_ll(LLWord* w, double v, unsigned long long seq) {
+  asm volatile("{\n\t.reg .b128 t;\n\tmov.b128 t, {%1, %2};\n\tst.relaxed.gpu.global.b128 [%0], t;\n\t}" ::"l"(w),
+               "l"(__double_as_longlong(v)), "l"(seq)
+               : "memory");
+}
+__device__ __forceinline__ double poll_ll(const LLWord* w, unsigned long long seq) {
+  unsigned long long v, s;
+  do {
+    asm volatile("{\n\t.reg .b128 t;\n\tld.relaxed.gpu.global.b128 t, [%2];\n\tmov.b128 {%0, %1}, t;\n\t}"
+                 : "=l"(v), "=l"(s)
+                 : "l"(w)
+                 : "memory");
+  } while (s != seq);
+  return __longlong_as_double(v);
+}
+
+// ---- shared-memory tile products of the fast path ---------------------------
+// out[c] = Σ_{r<R} T[r*ld + c] · v[r] for c < C, T in shared memory (ld even,
+// rows 16-byte aligned).  Threads own column pairs; RG row groups, four
+// independent chains per thread; row-group partials summed in fixed order.
+template <typename Epi>
+__device__ __forceinline__ void colsum2(const double* __restrict__ T, int ld, int R, int C,
+                                        const double* __restrict__ v, double* red, Epi epi) {
+  const int tid = threadIdx.x;
+  if (C <= 0) return;
+  const int CP = (C + 1) >> 1;
+  int RG = kThreads / CP;
+  if (RG > R) RG = R > 0 ? R : 1;
+  const int cp = tid % CP, rg = tid / CP;
+  double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
+  if (rg < RG) {
+    const double* col = T + 2 * cp;
+    int r = rg;
+    for (; r + 3 * RG < R; r += 4 * RG) {
+      const double2 t0 = *reinterpret_cast<const double2*>(col + (size_t)r * ld);
+      const double2 t1 = *reinterpret_cast<const double2*>(col + (size_t)(r + RG) * ld);
+      const double2 t2 = *reinterpret_cast<const double2*>(col + (size_t)(r + 2 * RG) * ld);
+      const double2 t3 = *reinterpret_cast<const double2*>(col + (size_t)(r + 3 * RG) * ld);
+      const double v0 = v[r], v1 = v[r + RG], v2 = v[r + 2 * RG], v3 = v[r + 3 * RG];
+      a0.x = fma(t0.x, v0, a0.x);
+      a0.y = fma(t0.y, v0, a0.y);
+      a1.x = fma(t1.x, v1, a1.x);
+      a1.y = fma(t1.y, v1, a1.y);
+      a2.x = fma(t2.x, v2, a2.x);
+      a2.y = fma(t2.y, v2, a2.y);
+      a3.x = fma(t3.x, v3, a3.x);
+      a3.y = fma(t3.y, v3, a3.y);
+    }
+    for (; r < R; r += RG) {
+      const double2 t0 = *reinterpret_cast<const double2*>(col + (size_t)r * ld);
+      const double v0 = v[r];
+      a0.x = fma(t0.x, v0, a0.x);
+      a0.y = fma(t0.y, v0, a0.y);
+    }
+  }
+  const double sx = (a0.x + a1.x) + (a2.x + a3.x);
+  const double sy = (a0.y + a1.y) + (a2.y + a3.y);
+  if (RG == 1) {
+    if (rg < 1) {
+      epi(2 * cp, sx);
+      if (2 * cp + 1 < C) epi(2 * cp + 1, sy);
+    }
+    __syncthreads();
+    return;
+  }
+  __syncthreads();
+  if (rg < RG) {
+    red[rg * 2 * CP + 2 * cp] = sx;
+    red[rg * 2 * CP + 2 * cp + 1] = sy;
+  }
+  __syncthreads();
+  for (int c = tid; c < C; c += kThreads) {
+    double s = 0.0;
+    for (int q = 0; q < RG; ++q) s += red[q * 2 * CP + c];
+    epi(c, s);
+  }
+  __syncthreads();
+}
+
+// out[r] = Σ_{c<C} T[r*ld + c] · v[c] for r < R.  L lanes per row read
+// 16-byte pairs; xor butterfly inside the lane group.  An odd trailing column
+// is handled by one lane so v needs no padding.
+template <typename Epi>
+__device__ __forceinline__ void rowdot2(const double* __restrict__ T, int ld, int R, int C,
+                                        const double* __restrict__ v, Epi epi) {
+  if (R <= 0) return;
+  const int tid = threadIdx.x;
+  const int CPf = C >> 1;  // full pairs
+  int L = pow2floor(kThreads / R);
+  const int lmax = CPf >= 1 ? pow2floor(CPf) : 1;
+  L = L > 32 ? 32 : L;
+  L = L > lmax ? lmax : L;
+  const int sub = tid % L, rsub = tid / L, rpp = kThreads / L;
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+  for (int r0 = 0; r0 < R; r0 += rpp) {
+    const int r = r0 + rsub;
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+    if (r < R) {
+      const double2* row = reinterpret_cast<const double2*>(T + (size_t)r * ld);
+      int q = sub;
+      for (; q + L < CPf; q += 2 * L) {
+        const double2 t0 = row[q], t1 = row[q + L];
+        const double2 w0 = v2[q], w1 = v2[q + L];
+        c0 = fma(t0.x, w0.x, c0);
+        c1 = fma(t0.y, w0.y, c1);
+        c2 = fma(t1.x, w1.x, c2);
+        c3 = fma(t1.y, w1.y, c3);
+      }
+      if (q < CPf) {
+        const double2 t0 = row[q], w0 = v2[q];
+        c0 = fma(t0.x, w0.x, c0);
+        c1 = fma(t0.y, w0.y, c1);
+      }
+      if ((C & 1) && sub == (CPf % L)) c2 = fma(T[(size_t)r * ld + C - 1], v[C - 1], c2);
+    }
+    double acc = (c0 + c1) + (c2 + c3);
+    for (int off = L / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (sub == 0 && r < R) epi(r, acc);
+  }
+}
+
+}  // namespace rebk

@@ -1,5 +1,6 @@
 // rebk_internal.h — types shared by the sm_100a kernels and the C-ABI layer.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,7 +28,14 @@ struct Control {
   double final_error;
   int64_t n_checks;
   int32_t has_error;
-  int32_t pad;
+  int32_t fault;  // launch-shape mismatch detected on the device
+  unsigned long long xseq;  // exchanges completed (fast path), carried across chunk launches
+};
+
+// 16-byte {value, sequence} word of the fast path's cross-cluster exchange
+struct __align__(16) LLWord {
+  double v;
+  unsigned long long seq;
 };
 
 struct DenseParams {
@@ -50,6 +58,7 @@ struct DenseParams {
   const Plan* plan;  // plan[k - k_begin]
   int64_t k_begin, k_end;  // 1-based iterations handled by this launch
   Control* ctl;
+  long long* prof;  // optional per-CTA phase cycle counters [G][16] (REBK_PROF=1)
   int32_t extended;   // REBK/REK: column sweep on z
   int32_t stop_mode;  // REBK_STOP_*
   double tol;
@@ -63,6 +72,18 @@ struct DenseParams {
   int32_t ct_ld, rt_ld;    // leading dims of the staged tiles (doubles)
   int32_t stage_ct, stage_rt;  // 1 = tile staged in shared memory by TMA bulk copies
   int32_t ct_off, rt_off, vec_off;  // shared-memory carve-up (in doubles)
+};
+
+// fast path (rebk_dense_fast.cu): clustered exchanges, TMA 2D tiles
+struct FastParams {
+  DenseParams d;
+  LLWord* cpart_u;  // [NC][stride_u] cluster partials of the u exchange (+ error entry)
+  LLWord* cpart_r;  // [NC][stride_r] r partials, z_I, error entry
+  int32_t stride_u, stride_r;
+  int32_t ct_box_w, ct_box_h;  // TMA box of the column tile = its smem leading dim / rows
+  int32_t rt_box_w, rt_box_h;
+  int32_t pad_nC, pad_nR, pad_ne, pad_in, pad_cin;  // smem vector sizes (doubles, even)
+  int32_t cluster_size;  // expected cluster size (checked on the device)
 };
 
 struct SampleParams {
@@ -98,6 +119,9 @@ cudaError_t launch_sample_plan(const SampleParams& sp, int64_t k0, int64_t count
                                int32_t* picks_out, cudaStream_t stream);
 cudaError_t launch_dense(const DenseParams& p, int G, size_t smem_bytes, cudaStream_t stream);
 cudaError_t dense_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
+cudaError_t launch_dense_fast(const FastParams& fp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
+                              int cluster_size, size_t smem_bytes, cudaStream_t stream, bool cooperative);
+cudaError_t fast_max_clusters(int cluster_size, size_t smem_bytes, int* clusters);
 cudaError_t launch_block_norms(const double* A, int64_t lda, int64_t m, int64_t n, int axis,
                                int64_t nb, const int64_t* ptr_dev, double* out_dev,
                                cudaStream_t stream);

@@ -103,6 +103,7 @@ class RunTrace:
     x: np.ndarray | None = None
     z: np.ndarray | None = None
     grid_ctas: int = 0
+    kernel_path: int = 0  # 0 general kernel, 1/2 clustered fast path (2: cooperative launch)
 
 
 def _block_beta(a: Matrix, p: Partition) -> float:
@@ -406,6 +407,7 @@ def run(problem: ProblemInstance, config: SolverConfig) -> RunTrace:
         x=x,
         z=z,
         grid_ctas=int(tr.grid_ctas),
+        kernel_path=int(tr.kernel_path),
     )
 
 

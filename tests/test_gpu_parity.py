@@ -314,3 +314,16 @@ def test_c2_full_run_matches_reference():
     assert tr.converged and tr.iters == k
     assert rel(tr.x, g[f"x_{k}"]) <= RTOL
     assert rel(tr.z, g[f"z_{k}"]) <= RTOL
+
+
+def test_fast_path_taken_and_agrees_with_general_kernel(monkeypatch):
+    """C1 runs on the clustered fast kernel; the general kernel (REBK_NO_FAST)
+    reduces in a different fixed order, so the two agree to rounding only."""
+    g, a, prob, cfg = c1_instance()
+    t_fast = P.run(prob, cfg)
+    assert t_fast.kernel_path in (1, 2)
+    monkeypatch.setenv("REBK_NO_FAST", "1")
+    t_gen = P.run(prob, cfg)
+    assert t_gen.kernel_path == 0
+    assert t_fast.iters == t_gen.iters
+    assert rel(t_fast.x, t_gen.x) <= 1e-12 and rel(t_fast.z, t_gen.z) <= 1e-12
