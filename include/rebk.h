@@ -102,7 +102,7 @@ typedef struct rebk_trace {
   int64_t errors_cap;
   int64_t n_checks;
   int32_t grid_ctas;        /* CTAs the persistent kernel used */
-  int32_t kernel_path;      /* 0 general kernel, 1 clustered fast path, 2 same, cooperative launch */
+  int32_t kernel_path;      /* 0 dense general, 1 dense clustered, 2 same (cooperative), 3 sparse */
 } rebk_trace;
 
 /* ---- library / device ---------------------------------------------------- */
@@ -118,6 +118,12 @@ int rebk_ctx_create_dense(const double* a_host, int64_t m, int64_t n, int64_t ld
 /* borrow an existing device array (caller keeps it alive; e.g. a torch tensor) */
 int rebk_ctx_create_dense_device(const double* a_dev, int64_t m, int64_t n, int64_t lda,
                                  int device, rebk_ctx** out);
+/* sparse A (replaces the CSR storage + CSC twin, matrix.py:46-58): CSR with
+ * sorted unique column indices per row (the reference normalises to this,
+ * matrix.py:226-231); the CSC twin is built inside.  The same rebk_run /
+ * rebk_run_device entry points then run the sparse kernel. */
+int rebk_ctx_create_csr(const int64_t* indptr, const int32_t* indices, const double* data, int64_t m,
+                        int64_t n, int64_t nnz, int device, rebk_ctx** out);
 int rebk_ctx_destroy(rebk_ctx* ctx);
 int rebk_ctx_shape(const rebk_ctx* ctx, int64_t* m, int64_t* n);
 

@@ -153,15 +153,28 @@ def blocks_from_ptr(ptr) -> list:
     return [range(int(lo), int(hi)) for lo, hi in zip(ptr[:-1], ptr[1:])]
 
 
-def block_weights(a: np.ndarray, blocks, axis: str) -> np.ndarray:
-    """||block||_F^2 as the reference computes it: BLAS dot of the C-order
-    flattening of the block (matrix.py:174-177)."""
+def block_weights(a, blocks, axis: str, csr=None, csc=None) -> np.ndarray:
+    """||block||_F^2 as the reference computes it (matrix.py:170-189): BLAS
+    dot of the C-order flattening of a dense block; for sparse storage the
+    dot of the CSR (rows) / CSC (columns) value slices."""
     out = []
     for blk in blocks:
         s = _sel(blk)
-        sub = a[s, :] if axis == "row" else a[:, s]
-        flat = np.ravel(sub)
-        out.append(float(flat @ flat))
+        if csr is None:
+            sub = a[s, :] if axis == "row" else a[:, s]
+            flat = np.ravel(sub)
+            out.append(float(flat @ flat))
+            continue
+        store = csr if axis == "row" else csc
+        if isinstance(s, slice):
+            chunk = store.data[store.indptr[s.start]:store.indptr[s.stop]]
+            out.append(float(chunk @ chunk))
+        else:
+            tot = 0.0
+            for i in s:
+                chunk = store.data[store.indptr[i]:store.indptr[i + 1]]
+                tot += float(chunk @ chunk)
+            out.append(tot)
     return np.asarray(out)
 
 
@@ -187,24 +200,44 @@ class OracleSolver:
     def __init__(self, a: np.ndarray, b: np.ndarray, row_blocks, col_blocks=None, alpha: float = 1.0,
                  algorithm: str = "rebk"):
         """row_blocks / col_blocks: block pointers (int array of length
-        nb+1) or a list of index blocks (ranges or int arrays)."""
-        self.a = np.ascontiguousarray(a, dtype=np.float64)
+        nb+1) or a list of index blocks (ranges or int arrays).  `a` is a
+        dense array or a scipy sparse matrix (CSR + CSC twin, as the
+        reference stores it, matrix.py:46-58)."""
+        import scipy.sparse as sp
+
+        self.sparse = sp.issparse(a)
+        if self.sparse:
+            csr = sp.csr_matrix(a, dtype=np.float64, copy=True)
+            csr.sum_duplicates()
+            csr.eliminate_zeros()
+            csr.sort_indices()
+            self.csr, self.csc = csr, csr.tocsc()
+            self.a = None
+        else:
+            self.csr = self.csc = None
+            self.a = np.ascontiguousarray(a, dtype=np.float64)
         self.b = np.asarray(b, dtype=np.float64)
         self.algorithm = algorithm
         self.extended = algorithm in ("rebk", "rek")
         if isinstance(row_blocks, np.ndarray) and row_blocks.dtype != object:
             row_blocks = blocks_from_ptr(row_blocks)
         self.row_sel = [_sel(bk) for bk in row_blocks]
-        self.row_blocks = [self.a[s, :] for s in self.row_sel]
-        self.row_sampler = Sampler(block_weights(self.a, row_blocks, "row"))
+        if self.sparse:
+            self.row_blocks = [self.csr[s, :] for s in self.row_sel]
+        else:
+            self.row_blocks = [self.a[s, :] for s in self.row_sel]
+        self.row_sampler = Sampler(block_weights(self.a, row_blocks, "row", self.csr, self.csc))
         self.row_scales = [float(alpha / w) for w in self.row_sampler.weights]
         self.b_blocks = [self.b[s] for s in self.row_sel]
         if self.extended:
             if isinstance(col_blocks, np.ndarray) and col_blocks.dtype != object:
                 col_blocks = blocks_from_ptr(col_blocks)
             self.col_sel = [_sel(bk) for bk in col_blocks]
-            self.col_blocks = [self.a[:, s] for s in self.col_sel]
-            self.col_sampler = Sampler(block_weights(self.a, col_blocks, "col"))
+            if self.sparse:
+                self.col_blocks = [self.csc[:, s] for s in self.col_sel]
+            else:
+                self.col_blocks = [self.a[:, s] for s in self.col_sel]
+            self.col_sampler = Sampler(block_weights(self.a, col_blocks, "col", self.csr, self.csc))
             self.col_scales = [float(alpha / w) for w in self.col_sampler.weights]
 
     def picks(self, rng, count: int) -> np.ndarray:
@@ -235,21 +268,24 @@ class OracleSolver:
         """run() of solvers.py:425-474; returns a dict with the trace fields,
         the final iterates and the pick sequence."""
         rng = rng if rng is not None else OracleRng(seed)
-        x = np.zeros(self.a.shape[1]) if x0 is None else np.array(x0, dtype=np.float64)
+        shape = self.csr.shape if self.sparse else self.a.shape
+        x = np.zeros(shape[1]) if x0 is None else np.array(x0, dtype=np.float64)
         z = None
         if self.extended:
             z = self.b.copy() if z0 is None else np.array(z0, dtype=np.float64)
         xs = None if x_star is None else np.asarray(x_star, dtype=np.float64)
-        scale = float(np.sqrt(float(self.a.ravel() @ self.a.ravel())) * np.linalg.norm(self.b)) or 1.0
+        fro = self.csr.data if self.sparse else self.a.ravel()
+        scale = float(np.sqrt(float(fro @ fro)) * np.linalg.norm(self.b)) or 1.0
+        mat, matT = (self.csr, self.csc.T) if self.sparse else (self.a, self.a.T)
 
         def err_of():
             if mode == "oracle_error":
                 return float(np.linalg.norm(x - xs))
             if mode == "residual_proxy":
-                r = self.a @ x - self.b
+                r = mat @ x - self.b
                 if z is not None:
                     r += z
-                return float(np.linalg.norm(self.a.T @ r)) / scale
+                return float(np.linalg.norm(matT @ r)) / scale
             return None
 
         errors, ckpts, picks = [], [], []

@@ -21,12 +21,31 @@
 
 using namespace rebk;
 
+// Per-partition segment lists of the sparse kernel (built once, cached).
+struct CsrSegPlan {
+  std::vector<int64_t> row_ptr, col_ptr;  // the partition (cache key) and the grid size
+  int G = 0;
+  int64_t *cseg_off = nullptr, *cseg_lo = nullptr, *cseg_hi = nullptr, *cseg_cta = nullptr;
+  int32_t* cseg_row = nullptr;
+  int64_t *rseg_off = nullptr, *rseg_lo = nullptr, *rseg_hi = nullptr, *rseg_cta = nullptr;
+  int32_t* rseg_col = nullptr;
+};
+
 struct rebk_ctx {
   int device;
+  int kind;  // 0 dense, 1 CSR
   int64_t m, n, lda;
-  const double* A;    // device
+  const double* A;    // device (dense)
   double* A_owned;    // non-null when the ctx allocated A
   int sm_count;
+  // CSR + CSC twin (device) and host copies for building segment lists
+  int64_t nnz = 0;
+  int64_t *csr_ptr = nullptr, *csc_ptr = nullptr;
+  int32_t *csr_col = nullptr, *csc_row = nullptr;
+  double *csr_val = nullptr, *csc_val = nullptr;
+  std::vector<int64_t> h_csr_ptr, h_csc_ptr;
+  std::vector<int32_t> h_csr_col, h_csc_row;
+  std::vector<CsrSegPlan*> seg_cache;
 };
 
 namespace {
@@ -245,6 +264,304 @@ int env_int(const char* name, int dflt) {
   return s ? atoi(s) : dflt;
 }
 
+// ---- sparse path ---------------------------------------------------------------
+bool same_vec(const std::vector<int64_t>& a, const int64_t* b, int64_t n) {
+  if ((int64_t)a.size() != n) return false;
+  for (int64_t i = 0; i < n; ++i)
+    if (a[i] != b[i]) return false;
+  return true;
+}
+
+template <typename T>
+cudaError_t upload_vec(T** dst, const std::vector<T>& v) {
+  cudaError_t e = cudaMalloc(dst, std::max<size_t>(v.size(), 1) * sizeof(T));
+  if (e == cudaSuccess && !v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+void free_seg_plan(CsrSegPlan* sp) {
+  if (!sp) return;
+  cudaFree(sp->cseg_off); cudaFree(sp->cseg_lo); cudaFree(sp->cseg_hi); cudaFree(sp->cseg_cta); cudaFree(sp->cseg_row);
+  cudaFree(sp->rseg_off); cudaFree(sp->rseg_lo); cudaFree(sp->rseg_hi); cudaFree(sp->rseg_cta); cudaFree(sp->rseg_col);
+  delete sp;
+}
+
+// Segment lists of one partition: for every column block, the rows with
+// nonzeros in it and their [lo, hi) range in the CSR arrays (sorted by row);
+// for every row block, the columns with nonzeros in it and their range in the
+// CSC arrays (sorted by column); plus each CTA's first segment.
+int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, CsrSegPlan** out) {
+  const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
+  for (CsrSegPlan* c : ctx->seg_cache) {
+    if (c->G == G && same_vec(c->row_ptr, cfg->row_ptr, s + 1) &&
+        (!extended || same_vec(c->col_ptr, cfg->col_ptr, t + 1))) {
+      *out = c;
+      return REBK_OK;
+    }
+  }
+  const int64_t m = ctx->m, n = ctx->n;
+  CsrSegPlan* sp = new CsrSegPlan();
+  sp->G = G;
+  sp->row_ptr.assign(cfg->row_ptr, cfg->row_ptr + s + 1);
+  if (extended) sp->col_ptr.assign(cfg->col_ptr, cfg->col_ptr + t + 1);
+  // column blocks -> row segments into CSR
+  std::vector<int64_t> coff(t + 1, 0), clo, chi, ccta;
+  std::vector<int32_t> crow;
+  if (extended) {
+    std::vector<int32_t> blk_of_col(n);
+    for (int64_t b = 0; b < t; ++b)
+      for (int64_t j = cfg->col_ptr[b]; j < cfg->col_ptr[b + 1]; ++j) blk_of_col[j] = (int32_t)b;
+    std::vector<int64_t> cnt(t, 0);
+    for (int64_t i = 0; i < m; ++i) {
+      int32_t prev = -1;
+      for (int64_t e = ctx->h_csr_ptr[i]; e < ctx->h_csr_ptr[i + 1]; ++e) {
+        const int32_t b = blk_of_col[ctx->h_csr_col[e]];
+        if (b != prev) ++cnt[b];
+        prev = b;
+      }
+    }
+    for (int64_t b = 0; b < t; ++b) coff[b + 1] = coff[b] + cnt[b];
+    const int64_t ns = coff[t];
+    clo.resize(ns); chi.resize(ns); crow.resize(ns);
+    std::vector<int64_t> fill(coff.begin(), coff.end() - 1);
+    for (int64_t i = 0; i < m; ++i) {
+      int32_t prev = -1;
+      int64_t cur = -1;
+      for (int64_t e = ctx->h_csr_ptr[i]; e < ctx->h_csr_ptr[i + 1]; ++e) {
+        const int32_t b = blk_of_col[ctx->h_csr_col[e]];
+        if (b != prev) {
+          cur = fill[b]++;
+          crow[cur] = (int32_t)i;
+          clo[cur] = e;
+        }
+        chi[cur] = e + 1;
+        prev = b;
+      }
+    }
+    ccta.resize(t * (G + 1));
+    for (int64_t b = 0; b < t; ++b)
+      for (int q = 0; q <= G; ++q) {
+        const int32_t r0 = split_rows(m, G, q);
+        ccta[b * (G + 1) + q] =
+            std::lower_bound(crow.begin() + coff[b], crow.begin() + coff[b + 1], r0) - crow.begin();
+      }
+  }
+  // row blocks -> column segments into CSC
+  std::vector<int64_t> roff(s + 1, 0), rlo, rhi, rcta;
+  std::vector<int32_t> rcol;
+  {
+    std::vector<int32_t> blk_of_row(m);
+    for (int64_t b = 0; b < s; ++b)
+      for (int64_t i = cfg->row_ptr[b]; i < cfg->row_ptr[b + 1]; ++i) blk_of_row[i] = (int32_t)b;
+    std::vector<int64_t> cnt(s, 0);
+    for (int64_t j = 0; j < n; ++j) {
+      int32_t prev = -1;
+      for (int64_t e = ctx->h_csc_ptr[j]; e < ctx->h_csc_ptr[j + 1]; ++e) {
+        const int32_t b = blk_of_row[ctx->h_csc_row[e]];
+        if (b != prev) ++cnt[b];
+        prev = b;
+      }
+    }
+    for (int64_t b = 0; b < s; ++b) roff[b + 1] = roff[b] + cnt[b];
+    const int64_t ns = roff[s];
+    rlo.resize(ns); rhi.resize(ns); rcol.resize(ns);
+    std::vector<int64_t> fill(roff.begin(), roff.end() - 1);
+    for (int64_t j = 0; j < n; ++j) {
+      int32_t prev = -1;
+      int64_t cur = -1;
+      for (int64_t e = ctx->h_csc_ptr[j]; e < ctx->h_csc_ptr[j + 1]; ++e) {
+        const int32_t b = blk_of_row[ctx->h_csc_row[e]];
+        if (b != prev) {
+          cur = fill[b]++;
+          rcol[cur] = (int32_t)j;
+          rlo[cur] = e;
+        }
+        rhi[cur] = e + 1;
+        prev = b;
+      }
+    }
+    rcta.resize(s * (G + 1));
+    for (int64_t b = 0; b < s; ++b)
+      for (int q = 0; q <= G; ++q) {
+        const int32_t c0 = split_rows(n, G, q);
+        rcta[b * (G + 1) + q] =
+            std::lower_bound(rcol.begin() + roff[b], rcol.begin() + roff[b + 1], c0) - rcol.begin();
+      }
+  }
+  cudaError_t e = cudaSuccess;
+  if (!e) e = upload_vec(&sp->cseg_off, coff);
+  if (!e) e = upload_vec(&sp->cseg_lo, clo);
+  if (!e) e = upload_vec(&sp->cseg_hi, chi);
+  if (!e) e = upload_vec(&sp->cseg_row, crow);
+  if (!e) e = upload_vec(&sp->cseg_cta, ccta);
+  if (!e) e = upload_vec(&sp->rseg_off, roff);
+  if (!e) e = upload_vec(&sp->rseg_lo, rlo);
+  if (!e) e = upload_vec(&sp->rseg_hi, rhi);
+  if (!e) e = upload_vec(&sp->rseg_col, rcol);
+  if (!e) e = upload_vec(&sp->rseg_cta, rcta);
+  if (e) {
+    free_seg_plan(sp);
+    return fail(REBK_ENOMEM, "segment lists upload failed: %s", cudaGetErrorString(e));
+  }
+  ctx->seg_cache.push_back(sp);
+  *out = sp;
+  return REBK_OK;
+}
+
+int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev, double* x_dev,
+                 double* z_dev, cudaStream_t stream, rebk_trace* trace) {
+  const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  int occ = 0;
+  CUDA_TRY(csr_kernel_occupancy(&occ));
+  int G = cfg->grid_ctas > 0 ? cfg->grid_ctas : grid_override();
+  if (G <= 0) G = (int)std::min<int64_t>(std::max<int64_t>(1, (ctx->nnz + 8191) / 8192), (int64_t)ctx->sm_count);
+  G = std::max(1, std::min(G, occ * ctx->sm_count));
+  CsrSegPlan* sp = nullptr;
+  int rc = build_seg_plan(ctx, cfg, extended, G, &sp);
+  if (rc) return rc;
+
+  DevArena arena;
+  arena.stream = stream;
+  const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
+  int64_t *d_row_ptr, *d_col_ptr = nullptr;
+  double *d_row_cum, *d_row_scale, *d_col_cum = nullptr, *d_col_scale = nullptr;
+  CUDA_TRY(arena.alloc(&d_row_ptr, s + 1));
+  CUDA_TRY(arena.alloc(&d_row_cum, s));
+  CUDA_TRY(arena.alloc(&d_row_scale, s));
+  CUDA_TRY(cudaMemcpyAsync(d_row_ptr, cfg->row_ptr, (s + 1) * 8, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(d_row_cum, cfg->row_cum, s * 8, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(d_row_scale, cfg->row_scale, s * 8, cudaMemcpyHostToDevice, stream));
+  if (extended) {
+    CUDA_TRY(arena.alloc(&d_col_ptr, t + 1));
+    CUDA_TRY(arena.alloc(&d_col_cum, t));
+    CUDA_TRY(arena.alloc(&d_col_scale, t));
+    CUDA_TRY(cudaMemcpyAsync(d_col_ptr, cfg->col_ptr, (t + 1) * 8, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d_col_cum, cfg->col_cum, t * 8, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d_col_scale, cfg->col_scale, t * 8, cudaMemcpyHostToDevice, stream));
+  }
+  int32_t* d_picks = nullptr;
+  if (cfg->picks && cfg->max_iters > 0) {
+    CUDA_TRY(arena.alloc(&d_picks, 2 * cfg->max_iters));
+    CUDA_TRY(cudaMemcpyAsync(d_picks, cfg->picks, 2 * cfg->max_iters * sizeof(int32_t), cudaMemcpyHostToDevice,
+                             stream));
+  }
+  const int nJ_max = extended ? max_block(t, cfg->col_ptr) : 1;
+  const int nI_max = max_block(s, cfg->row_ptr);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(cfg->max_iters, (int64_t)1 << 20));
+  Plan* d_plan;
+  double *d_u, *d_r, *d_errpart, *d_res = nullptr, *d_errs = nullptr;
+  Control* d_ctl;
+  CUDA_TRY(arena.alloc(&d_plan, chunk));
+  CUDA_TRY(arena.alloc(&d_u, std::max(nJ_max, 1)));
+  CUDA_TRY(arena.alloc(&d_r, std::max(nI_max, 1)));
+  CUDA_TRY(arena.alloc(&d_errpart, G));
+  if (cfg->stop_mode == REBK_STOP_RESIDUAL_PROXY) CUDA_TRY(arena.alloc(&d_res, ctx->m));
+  const int64_t errs_cap = (cfg->record_errors && trace && trace->errors) ? trace->errors_cap : 0;
+  if (errs_cap > 0) CUDA_TRY(arena.alloc(&d_errs, errs_cap));
+  CUDA_TRY(arena.alloc(&d_ctl, 1));
+  CUDA_TRY(cudaMemsetAsync(d_ctl, 0, sizeof(Control), stream));
+
+  SampleParams smp{};
+  smp.key0 = cfg->philox_key[0];
+  smp.key1 = cfg->philox_key[1];
+  smp.draw_offset = cfg->draw_offset;
+  smp.extended = extended;
+  smp.n_row_blocks = (int32_t)s;
+  smp.n_col_blocks = (int32_t)t;
+  smp.row_ptr = d_row_ptr;
+  smp.row_cum = d_row_cum;
+  smp.row_total = cfg->row_total;
+  smp.row_scale = d_row_scale;
+  smp.col_ptr = d_col_ptr;
+  smp.col_cum = d_col_cum;
+  smp.col_total = cfg->col_total;
+  smp.col_scale = d_col_scale;
+  smp.picks = d_picks;
+
+  CsrParams p{};
+  p.m = (int32_t)ctx->m;
+  p.n = (int32_t)ctx->n;
+  p.csr_ptr = ctx->csr_ptr;
+  p.csr_col = ctx->csr_col;
+  p.csr_val = ctx->csr_val;
+  p.csc_ptr = ctx->csc_ptr;
+  p.csc_row = ctx->csc_row;
+  p.csc_val = ctx->csc_val;
+  p.cseg_off = sp->cseg_off;
+  p.cseg_row = sp->cseg_row;
+  p.cseg_lo = sp->cseg_lo;
+  p.cseg_hi = sp->cseg_hi;
+  p.cseg_cta = sp->cseg_cta;
+  p.rseg_off = sp->rseg_off;
+  p.rseg_col = sp->rseg_col;
+  p.rseg_lo = sp->rseg_lo;
+  p.rseg_hi = sp->rseg_hi;
+  p.rseg_cta = sp->rseg_cta;
+  p.b = b_dev;
+  p.xs = xs_dev;
+  p.x = x_dev;
+  p.z = z_dev;
+  p.u = d_u;
+  p.r = d_r;
+  p.errpart = d_errpart;
+  p.res = d_res;
+  p.errs = d_errs;
+  p.errs_cap = errs_cap;
+  p.plan = d_plan;
+  p.ctl = d_ctl;
+  p.extended = extended;
+  p.stop_mode = cfg->stop_mode;
+  p.tol = cfg->tol;
+  p.stride = cfg->check_stride;
+  p.max_iters = cfg->max_iters;
+  p.res_scale = cfg->residual_scale > 0.0 ? cfg->residual_scale : 1.0;
+  p.record = errs_cap > 0;
+
+  cudaEvent_t ev0, ev1;
+  CUDA_TRY(cudaEventCreate(&ev0));
+  CUDA_TRY(cudaEventCreate(&ev1));
+  cudaError_t err = cudaEventRecord(ev0, stream);
+  int64_t k = 1;
+  do {
+    const int64_t count = std::min(chunk, cfg->max_iters - k + 1);
+    if (err == cudaSuccess) err = launch_sample_plan(smp, k, count, d_plan, nullptr, stream);
+    if (err == cudaSuccess) err = cudaMemsetAsync(&d_ctl->bar, 0, sizeof(unsigned long long), stream);
+    p.k_begin = k;
+    p.k_end = k + count - 1;
+    if (err == cudaSuccess) err = launch_csr(p, G, stream);
+    k += std::max<int64_t>(count, 1);
+    if (err == cudaSuccess && k <= cfg->max_iters) {
+      int32_t done = 0;
+      err = cudaMemcpyAsync(&done, &d_ctl->done, sizeof done, cudaMemcpyDeviceToHost, stream);
+      if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
+      if (done) break;
+    }
+  } while (err == cudaSuccess && k <= cfg->max_iters);
+  if (err == cudaSuccess) err = cudaEventRecord(ev1, stream);
+  Control ctl{};
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&ctl, d_ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream);
+  if (err == cudaSuccess && errs_cap > 0)
+    err = cudaMemcpyAsync(trace->errors, d_errs, errs_cap * sizeof(double), cudaMemcpyDeviceToHost, stream);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
+  float ms = 0.f;
+  if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, ev0, ev1);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  if (err != cudaSuccess) return fail(REBK_ECUDA, "sparse REBK run failed: %s", cudaGetErrorString(err));
+  if (trace) {
+    trace->iters = ctl.iters;
+    trace->converged = ctl.converged;
+    trace->has_error = ctl.has_error;
+    trace->final_error = ctl.final_error;
+    trace->loop_ms = ms;
+    trace->n_checks = ctl.n_checks;
+    trace->grid_ctas = G;
+    trace->kernel_path = 3;
+  }
+  return REBK_OK;
+}
+
 int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev,
                     double* x_dev, double* z_dev, cudaStream_t stream, rebk_trace* trace) {
   const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
@@ -263,6 +580,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     if (rc) return rc;
   }
   if (ctx->m > INT32_MAX || ctx->n > INT32_MAX) return fail(REBK_EINVAL, "matrix dimension exceeds 2^31");
+  if (ctx->kind == 1) return run_csr_impl(ctx, cfg, b_dev, xs_dev, x_dev, z_dev, stream, trace);
 
   CUDA_TRY(cudaSetDevice(ctx->device));
 
@@ -611,12 +929,74 @@ int rebk_ctx_create_dense_device(const double* a_dev, int64_t m, int64_t n, int6
   return REBK_OK;
 }
 
+int rebk_ctx_create_csr(const int64_t* indptr, const int32_t* indices, const double* data, int64_t m, int64_t n,
+                        int64_t nnz, int device, rebk_ctx** out) {
+  if (!out || !indptr || (nnz > 0 && (!indices || !data))) return fail(REBK_EINVAL, "null argument");
+  if (m < 1 || n < 1) return fail(REBK_EINVAL, "matrix must be 2-D and nonempty");
+  if (m > INT32_MAX || n > INT32_MAX) return fail(REBK_EINVAL, "matrix dimension exceeds 2^31");
+  if (indptr[0] != 0 || indptr[m] != nnz) return fail(REBK_EINVAL, "indptr does not describe nnz entries");
+  for (int64_t i = 0; i < m; ++i) {
+    if (indptr[i + 1] < indptr[i]) return fail(REBK_EINVAL, "indptr must be nondecreasing");
+    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+      if (indices[e] < 0 || indices[e] >= n) return fail(REBK_EINVAL, "column index out of range");
+      if (e > indptr[i] && indices[e] <= indices[e - 1])
+        return fail(REBK_EINVAL, "column indices must be sorted and unique within a row");
+    }
+  }
+  rebk_ctx* c = new rebk_ctx{};
+  int rc = ctx_common(c, device);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  c->kind = 1;
+  c->m = m;
+  c->n = n;
+  c->lda = n;
+  c->nnz = nnz;
+  c->h_csr_ptr.assign(indptr, indptr + m + 1);
+  c->h_csr_col.assign(indices, indices + nnz);
+  // CSC twin (counting sort by column: rows stay ascending within a column)
+  c->h_csc_ptr.assign(n + 1, 0);
+  for (int64_t e = 0; e < nnz; ++e) c->h_csc_ptr[indices[e] + 1]++;
+  for (int64_t j = 0; j < n; ++j) c->h_csc_ptr[j + 1] += c->h_csc_ptr[j];
+  c->h_csc_row.resize(nnz);
+  std::vector<double> csc_val(nnz);
+  {
+    std::vector<int64_t> fill(c->h_csc_ptr.begin(), c->h_csc_ptr.end() - 1);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+        const int64_t q = fill[indices[e]]++;
+        c->h_csc_row[q] = (int32_t)i;
+        csc_val[q] = data[e];
+      }
+  }
+  std::vector<double> csr_val(data, data + nnz);
+  cudaError_t e = upload_vec(&c->csr_ptr, c->h_csr_ptr);
+  if (!e) e = upload_vec(&c->csr_col, c->h_csr_col);
+  if (!e) e = upload_vec(&c->csr_val, csr_val);
+  if (!e) e = upload_vec(&c->csc_ptr, c->h_csc_ptr);
+  if (!e) e = upload_vec(&c->csc_row, c->h_csc_row);
+  if (!e) e = upload_vec(&c->csc_val, csc_val);
+  if (e) {
+    rebk_ctx_destroy(c);
+    return fail(REBK_ENOMEM, "CSR upload failed: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return REBK_OK;
+}
+
 int rebk_ctx_destroy(rebk_ctx* ctx) {
   if (!ctx) return REBK_OK;
-  if (ctx->A_owned) {
-    cudaSetDevice(ctx->device);
-    cudaFree(ctx->A_owned);
-  }
+  cudaSetDevice(ctx->device);
+  if (ctx->A_owned) cudaFree(ctx->A_owned);
+  cudaFree(ctx->csr_ptr);
+  cudaFree(ctx->csr_col);
+  cudaFree(ctx->csr_val);
+  cudaFree(ctx->csc_ptr);
+  cudaFree(ctx->csc_row);
+  cudaFree(ctx->csc_val);
+  for (CsrSegPlan* sp : ctx->seg_cache) free_seg_plan(sp);
   delete ctx;
   return REBK_OK;
 }
@@ -736,6 +1116,7 @@ int rebk_sample_sequence(const rebk_cfg* cfg, int64_t k0, int64_t count, int32_t
 
 int rebk_block_frobenius_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* ptr, double* out) {
   if (!ctx || !ptr || !out || nb < 1 || (axis != 0 && axis != 1)) return fail(REBK_EINVAL, "bad argument");
+  if (ctx->kind != 0) return fail(REBK_EINVAL, "device block norms are implemented for dense matrices");
   const int64_t len = axis == 0 ? ctx->m : ctx->n;
   if (ptr[0] != 0 || ptr[nb] != len) return fail(REBK_EINVAL, "partition does not cover the axis");
   CUDA_TRY(cudaSetDevice(ctx->device));

@@ -1,0 +1,243 @@
+// rebk_csr.cu — persistent REBK kernel for sparse A (CSR + CSC twin), sm_100a.
+//
+// The reference keeps a CSR matrix and its CSC twin (matrix.py:46-58) and
+// applies the four block products through scipy's sparsetools
+// (solvers.py:283-295):
+//   u = A_Jᵀ z      csr_matvec of the transposed CSC slice: per column j of J,
+//                   a sequential sum over its nonzeros in row order;
+//   z -= s (A_J u)  csc_matvec: row i accumulates over the columns of J in
+//                   column order, then z_i - s*y_i;
+//   r = A_I x       csr_matvec: per row, sequential over its columns;
+//   x -= s (A_Iᵀ r) csc_matvec of the transposed CSR slice: column j
+//                   accumulates over the rows of I in row order.
+// Here every product is a GATHER (no atomics): per-block segment lists
+// (built once per partition on the host) give each row of a column block
+// its [lo, hi) range in the CSR arrays and each column of a row block its
+// range in the CSC arrays.  Sums run in scipy's order with unfused
+// multiply/add, so the iterates reproduce scipy bit for bit.
+//
+// Per iteration, 2 grid barriers (the dependency chain u -> z -> r -> x):
+//   P(k): stop decision for k-1; z update of the owned rows (u_k) except rows
+//         of I; for each row of I: r_i and its own z update (no cross-thread
+//         read of z).
+//   Q(k): x update of the owned columns (r_k); error partial; u_{k+1}.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rebk_device.cuh"
+#include "rebk_internal.h"
+
+namespace rebk {
+
+__device__ __forceinline__ double madd(double acc, double a, double b) {
+  return __dadd_rn(acc, __dmul_rn(a, b));  // no FMA contraction: scipy's order and rounding
+}
+
+__global__ void __launch_bounds__(kThreads) rebk_csr_kernel(CsrParams p) {
+  __shared__ double s_red[kWarps];
+  __shared__ double s_bcast[2];
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int64_t gtid = (int64_t)g * kThreads + tid, gthreads = (int64_t)G * kThreads;
+  Control* ctl = p.ctl;
+  if (*((volatile int32_t*)&ctl->done)) return;
+
+  const int xq0 = split_rows(p.n, G, g), xq1 = split_rows(p.n, G, g + 1);
+  const int zr0 = split_rows(p.m, G, g), zr1 = split_rows(p.m, G, g + 1);
+
+  unsigned long long bar_target = 0;
+  auto gsync = [&]() {
+    bar_target += (unsigned long long)G;
+    grid_barrier(&ctl->bar, bar_target);
+  };
+  const bool checking = p.stop_mode != 2;
+  const bool oracle = p.stop_mode == 0;
+
+  auto oracle_partial = [&]() {
+    double acc = 0.0;
+    for (int j = xq0 + tid; j < xq1; j += kThreads) {
+      const double d = __ldcg(p.x + j) - __ldg(p.xs + j);
+      acc = fma(d, d, acc);
+    }
+    const double s = block_sum(acc, s_red);
+    if (tid == 0) __stcg(p.errpart + g, s);
+  };
+  // ||Aᵀ(Ax - b + z)|| / scale (solvers.py:410-419) through csr/csc matvecs
+  auto residual_partials = [&]() {
+    for (int64_t i = gtid; i < p.m; i += gthreads) {
+      double acc = 0.0;
+      for (int64_t e = p.csr_ptr[i]; e < p.csr_ptr[i + 1]; ++e) acc = madd(acc, p.csr_val[e], __ldcg(p.x + p.csr_col[e]));
+      double v = __dsub_rn(acc, __ldg(p.b + i));
+      if (p.extended) v = __dadd_rn(v, __ldcg(p.z + i));
+      __stcg(p.res + i, v);
+    }
+    gsync();
+    double acc2 = 0.0;
+    for (int j = xq0 + tid; j < xq1; j += kThreads) {
+      double gj = 0.0;
+      for (int64_t e = p.csc_ptr[j]; e < p.csc_ptr[j + 1]; ++e) gj = madd(gj, p.csc_val[e], __ldcg(p.res + p.csc_row[e]));
+      acc2 = fma(gj, gj, acc2);
+    }
+    const double s = block_sum(acc2, s_red);
+    if (tid == 0) __stcg(p.errpart + g, s);
+  };
+  auto decide = [&](int64_t k) -> bool {
+    if (warp == 0) {
+      double s = 0.0;
+      for (int q = lane; q < G; q += 32) s += __ldcg(p.errpart + q);
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) s_bcast[0] = s;
+    }
+    __syncthreads();
+    double err = sqrt(s_bcast[0]);
+    if (!oracle) err = err / p.res_scale;
+    const bool conv = err <= p.tol;
+    if (g == 0 && tid == 0) {
+      const int64_t nc = ctl->n_checks;
+      if (p.record && nc < p.errs_cap) p.errs[nc] = err;
+      ctl->n_checks = nc + 1;
+      ctl->final_error = err;
+      ctl->has_error = 1;
+      if (conv) {
+        ctl->converged = 1;
+        ctl->iters = k;
+        ctl->done = 1;
+      }
+    }
+    __syncthreads();
+    return conv;
+  };
+  // u_j = Σ_i A_ij z_i over CSC column j, for the column block of `pl`
+  auto compute_u = [&](const Plan& pl) {
+    for (int64_t j = pl.c_lo + gtid; j < pl.c_hi; j += gthreads) {
+      double acc = 0.0;
+      for (int64_t e = p.csc_ptr[j]; e < p.csc_ptr[j + 1]; ++e) acc = madd(acc, p.csc_val[e], __ldcg(p.z + p.csc_row[e]));
+      __stcg(p.u + (j - pl.c_lo), acc);
+    }
+  };
+
+  bool finished = false;
+  if (p.k_begin == 1 && checking) {
+    if (oracle) {
+      oracle_partial();
+      gsync();
+    } else {
+      residual_partials();
+      gsync();
+    }
+    if (decide(0)) finished = true;
+  }
+  if (!finished && p.extended && p.k_begin <= p.k_end) {
+    compute_u(p.plan[0]);
+    gsync();
+  }
+
+  bool pending = false;
+  int64_t pending_k = 0;
+  for (int64_t k = p.k_begin; !finished && k <= p.k_end; ++k) {
+    const Plan pl = p.plan[k - p.k_begin];
+    const bool check_k = checking && (k % p.stride == 0);
+    // ---- P(k)
+    if (pending) {
+      pending = false;
+      if (decide(pending_k)) {
+        finished = true;
+        break;
+      }
+    }
+    const double cs = pl.c_scale, rs = pl.r_scale;
+    if (p.extended) {
+      const int64_t s0 = p.cseg_cta[(int64_t)pl.cb * (G + 1) + g];
+      const int64_t s1 = p.cseg_cta[(int64_t)pl.cb * (G + 1) + g + 1];
+      for (int64_t sg = s0 + tid; sg < s1; sg += kThreads) {
+        const int i = p.cseg_row[sg];
+        if (i >= pl.r_lo && i < pl.r_hi) continue;  // done by the row-sweep threads below
+        double acc = 0.0;
+        for (int64_t e = p.cseg_lo[sg]; e < p.cseg_hi[sg]; ++e)
+          acc = madd(acc, p.csr_val[e], __ldcg(p.u + (p.csr_col[e] - pl.c_lo)));
+        __stcg(p.z + i, __dsub_rn(__ldcg(p.z + i), __dmul_rn(cs, acc)));
+      }
+    }
+    for (int64_t i = pl.r_lo + gtid; i < pl.r_hi; i += gthreads) {
+      double ax = 0.0, au = 0.0;
+      for (int64_t e = p.csr_ptr[i]; e < p.csr_ptr[i + 1]; ++e) {
+        const int c = p.csr_col[e];
+        const double a = p.csr_val[e];
+        ax = madd(ax, a, __ldcg(p.x + c));
+        if (p.extended && c >= pl.c_lo && c < pl.c_hi) au = madd(au, a, __ldcg(p.u + (c - pl.c_lo)));
+      }
+      double rv = __dsub_rn(ax, __ldg(p.b + i));
+      if (p.extended) {
+        const double zn = __dsub_rn(__ldcg(p.z + i), __dmul_rn(cs, au));
+        __stcg(p.z + i, zn);
+        rv = __dadd_rn(rv, zn);
+      }
+      __stcg(p.r + (i - pl.r_lo), rv);
+    }
+    gsync();
+    // ---- Q(k)
+    {
+      const int64_t s0 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g];
+      const int64_t s1 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g + 1];
+      for (int64_t sg = s0 + tid; sg < s1; sg += kThreads) {
+        const int j = p.rseg_col[sg];
+        double acc = 0.0;
+        for (int64_t e = p.rseg_lo[sg]; e < p.rseg_hi[sg]; ++e)
+          acc = madd(acc, p.csc_val[e], __ldcg(p.r + (p.csc_row[e] - pl.r_lo)));
+        __stcg(p.x + j, __dsub_rn(__ldcg(p.x + j), __dmul_rn(rs, acc)));
+      }
+    }
+    __syncthreads();
+    if (check_k) {
+      if (oracle) {
+        oracle_partial();
+        pending = true;
+        pending_k = k;
+      } else {
+        gsync();
+        residual_partials();
+        gsync();
+        if (decide(k)) {
+          finished = true;
+          break;
+        }
+      }
+    }
+    if (p.extended && k < p.k_end) compute_u(p.plan[k + 1 - p.k_begin]);
+    gsync();
+  }
+
+  if (!finished) {
+    if (pending) {
+      if (decide(pending_k)) finished = true;  // errpart was published before the loop's last barrier
+    }
+    if (!finished && p.k_end == p.max_iters) {
+      if (checking && (p.max_iters % p.stride) != 0) {
+        if (oracle) {
+          oracle_partial();
+          gsync();
+        } else {
+          residual_partials();
+          gsync();
+        }
+        decide(p.max_iters);
+      }
+      if (g == 0 && tid == 0) {
+        if (!ctl->converged) ctl->iters = p.max_iters;
+        ctl->done = 1;
+      }
+    }
+  }
+}
+
+cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream) {
+  CsrParams pc = p;
+  void* args[] = {&pc};
+  return cudaLaunchCooperativeKernel((const void*)rebk_csr_kernel, dim3(G), dim3(kThreads), args, 0, stream);
+}
+
+cudaError_t csr_kernel_occupancy(int* blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, rebk_csr_kernel, kThreads, 0);
+}
+
+}  // namespace rebk

@@ -444,6 +444,9 @@ __global__ void sample_plan_kernel(SampleParams sp, int64_t k0, int64_t count, P
     pl.r_lo = (int32_t)sp.row_ptr[i];
     pl.r_hi = (int32_t)sp.row_ptr[i + 1];
     pl.r_scale = sp.row_scale[i];
+    pl.cb = j;
+    pl.rb = i;
+    pl.pad0 = pl.pad1 = 0;
     plan[idx] = pl;
   }
   if (picks_out) {

@@ -17,6 +17,8 @@ constexpr int kSmemBudget = 218 * 1024;
 struct Plan {
   int32_t c_lo, c_hi, r_lo, r_hi;
   double c_scale, r_scale;
+  int32_t cb, rb;  // block indices (the sparse kernel indexes its per-block segment lists)
+  int32_t pad0, pad1;
 };
 
 // Device-resident run control (one per rebk_run).
@@ -86,6 +88,50 @@ struct FastParams {
   int32_t cluster_size;  // expected cluster size (checked on the device)
 };
 
+// Sparse (CSR + CSC twin) persistent kernel (rebk_csr.cu).
+struct CsrParams {
+  int32_t m, n;
+  const int64_t* csr_ptr;  // [m+1]
+  const int32_t* csr_col;  // [nnz]
+  const double* csr_val;
+  const int64_t* csc_ptr;  // [n+1]
+  const int32_t* csc_row;
+  const double* csc_val;
+  // per column block J: segments (row, [lo, hi) into the CSR arrays) sorted by row
+  const int64_t* cseg_off;  // [t+1]
+  const int32_t* cseg_row;
+  const int64_t* cseg_lo;
+  const int64_t* cseg_hi;
+  const int64_t* cseg_cta;  // [t][G+1] first segment of each CTA's z-row slice
+  // per row block I: segments (col, [lo, hi) into the CSC arrays) sorted by column
+  const int64_t* rseg_off;  // [s+1]
+  const int32_t* rseg_col;
+  const int64_t* rseg_lo;
+  const int64_t* rseg_hi;
+  const int64_t* rseg_cta;  // [s][G+1] first segment of each CTA's x-column slice
+  const double* b;
+  const double* xs;
+  double* x;
+  double* z;
+  double* u;        // [nJ_max] column-sweep coefficients (global)
+  double* r;        // [nI_max]
+  double* errpart;  // [G]
+  double* res;      // [m] residual-proxy scratch
+  double* errs;
+  int64_t errs_cap;
+  const Plan* plan;
+  int64_t k_begin, k_end;
+  Control* ctl;
+  int32_t extended;
+  int32_t stop_mode;
+  double tol;
+  int64_t stride;
+  int64_t max_iters;
+  double res_scale;
+  int32_t record;
+  int32_t pad;
+};
+
 struct SampleParams {
   uint64_t key0, key1;
   uint64_t draw_offset;
@@ -122,6 +168,8 @@ cudaError_t dense_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
 cudaError_t launch_dense_fast(const FastParams& fp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
                               int cluster_size, size_t smem_bytes, cudaStream_t stream, bool cooperative);
 cudaError_t fast_max_clusters(int cluster_size, size_t smem_bytes, int* clusters);
+cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream);
+cudaError_t csr_kernel_occupancy(int* blocks_per_sm);
 cudaError_t launch_block_norms(const double* A, int64_t lda, int64_t m, int64_t n, int axis,
                                int64_t nb, const int64_t* ptr_dev, double* out_dev,
                                cudaStream_t stream);

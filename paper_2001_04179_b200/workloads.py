@@ -50,8 +50,12 @@ class Workload:
 
     @property
     def algorithmic_bytes_per_iter(self) -> float:
-        """8 (m |J| + |I| n): the two selected blocks read once."""
+        """8 (m |J| + |I| n): the two selected blocks read once (SURVEY §8d);
+        sparse: 12 B per stored entry of the two blocks (value + index)."""
         m, n = self.problem.a.shape
+        if self.problem.a.is_sparse:
+            nnz = self.problem.a.nnz
+            return 12.0 * nnz * (max(self.col_partition.block_sizes()) / n + max(self.row_partition.block_sizes()) / m)
         tj = max(self.col_partition.block_sizes())
         ti = max(self.row_partition.block_sizes())
         return 8.0 * (m * tj + ti * n)
@@ -103,6 +107,56 @@ def c2_arrays(seed: int = 0):
     return a, b, x_star
 
 
+def c4_matrix(seed: int = 0):
+    """C4's A: scipy.sparse.random(200000, 50000, density 1e-3, N(0,1) values)
+    drawn from numpy default_rng(seed); returns (csr, rng)
+    with the generator positioned after A so x / w follow the recipe."""
+    import scipy.sparse as sparse
+
+    g = np.random.default_rng(seed)
+    s = sparse.random(200000, 50000, density=1e-3, format="csr", random_state=g, data_rvs=g.standard_normal)
+    if np.any(np.diff(s.indptr) == 0) or np.any(np.bincount(s.indices, minlength=50000) == 0):
+        raise RuntimeError("empty row/column in the C4 draw: resampling not implemented for this seed")
+    return s, g
+
+
+def c4_arrays(seed: int = 0):
+    """C4: sparse 200000 x 50000 (1e7 nnz); b = A x + r, r = (I - A A+) w
+    (via LSQR) scaled to 0.1 ||A x||; x* = LSQR(A, b)."""
+    from scipy.sparse.linalg import lsqr
+
+    s, g = c4_matrix(seed)
+    xs = g.standard_normal(50000)
+    w = g.standard_normal(200000)
+    y = lsqr(s, w, atol=1e-15, btol=1e-15, iter_lim=2000)[0]
+    r = w - s @ y
+    ax = s @ xs
+    r *= 0.1 * np.linalg.norm(ax) / np.linalg.norm(r)
+    b = ax + r
+    x_star = lsqr(s, b, atol=1e-15, btol=1e-15, iter_lim=2000)[0]
+    return s, b, x_star
+
+
+def power_beta(mat, p: Partition, iters: int = 40, seed: int = 0) -> float:
+    """max over blocks of sigma_1(block)^2 / ||block||_F^2 by power iteration
+    (a cheap stand-in for the reference's rate constants on big sparse
+    blocks; only used to pick the stepsize of the synthetic workloads)."""
+    rng = np.random.default_rng(seed)
+    worst = 0.0
+    for idx in p.blocks:
+        view = mat.block(p.axis, idx)
+        blk = view.materialize()
+        fro = mat.block_frobenius_sq(view)
+        v = rng.standard_normal(blk.shape[1])
+        lam = 0.0
+        for _ in range(iters):
+            w = blk.T @ (blk @ v)
+            lam = float(np.linalg.norm(w))
+            v = w / lam
+        worst = max(worst, lam / fro)
+    return worst
+
+
 def make_workload(name: str, a: np.ndarray, b: np.ndarray, x_star: np.ndarray, tau_row: int,
                   tau_col: int, rel_tol: float = 1e-6, beta_max: float | None = None,
                   alpha_factor: float = 1.0, seed: int = 17) -> Workload:
@@ -121,4 +175,15 @@ def build(name: str, **kw) -> Workload:
     if name == "c2":
         a, b, xs = c2_arrays()
         return make_workload("c2", a, b, xs, 200, 200, **kw)
+    if name == "c4":
+        s, b, xs = c4_arrays()
+        mat = Matrix.from_sparse(s)
+        rp = contiguous_partition(200000, 2000, "row")
+        cp = contiguous_partition(50000, 1000, "col")
+        beta = kw.pop("beta_max", None) or max(power_beta(mat, rp), power_beta(mat, cp))
+        prob = ProblemInstance(a=mat, b=b, x_star=xs, b_perp=None,
+                               meta=ProblemMeta(declared_rank=50000, kappa_bound=None, consistent=False, seed=0,
+                                                residual_norm=0.0))
+        return Workload("c4", prob, rp, cp, kw.pop("alpha_factor", 1.0) / beta, beta, kw.pop("rel_tol", 1e-6),
+                        kw.pop("seed", 17))
     raise KeyError(f"unknown workload {name!r}")

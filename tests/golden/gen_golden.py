@@ -100,8 +100,14 @@ def small_case(name, a, b, algo, alpha, seed, row_p=None, col_p=None, max_iters=
                                                     col_partition=col_p, max_iters=max(ks), z0=z0,
                                                     stop=K.StoppingRule(mode="max_iters_only")), ks)
     npk = max(tr.iters, max(ks))
+    sparse_extra = {}
+    if problem.a.is_sparse:
+        c = problem.a._csr
+        sparse_extra = dict(a_indptr=c.indptr.astype(np.int64), a_indices=c.indices.astype(np.int32),
+                            a_data=c.data, a_shape=np.asarray(c.shape))
     out = dict(
-        a=problem.a.to_dense(), b=problem.b, x_star=np.asarray(problem.x_star), algorithm=algo, alpha=alpha,
+        **sparse_extra,
+        a=problem.a.to_dense() if not problem.a.is_sparse else np.zeros((0, 0)), b=problem.b, x_star=np.asarray(problem.x_star), algorithm=algo, alpha=alpha,
         seed=seed, max_iters=max_iters, tol=tol, stride=stride, mode=mode,
         row_blocks=np.asarray([np.asarray(bk, dtype=np.int64) for bk in ctx.row_partition.blocks], dtype=object),
         iters=tr.iters, converged=tr.converged, final_error=np.nan if tr.final_error is None else tr.final_error,
@@ -189,6 +195,69 @@ def small_cases():
                problem=p, stride=5)
 
 
+def sparse_cases():
+    import scipy.sparse as sparse
+
+    def sparse_problem(m, n, dens, seed, consistent=False):
+        g = np.random.default_rng(seed)
+        sm = sparse.random(m, n, density=dens, format="csr", random_state=g, data_rvs=g.standard_normal)
+        # no empty rows/columns (a zero-norm singleton block could never be sampled)
+        sm = sm + sparse.eye(m, n, format="csr") * 0.5
+        mat = K.Matrix.from_sparse(sm)
+        xg = g.standard_normal(n)
+        b = mat.matvec(xg) + (0.0 if consistent else 0.3 * g.standard_normal(m))
+        prob = K.ProblemInstance(a=mat, b=b, x_star=None, b_perp=None, meta=K.ProblemMeta(0, None, False, 0, 0.0))
+        prob.ensure_oracle()
+        return prob
+
+    p = sparse_problem(60, 40, 0.1, 70)
+    rp, cp = K.contiguous_partition(60, 7, "row"), K.contiguous_partition(40, 6, "col")
+    beta = compute_beta_max(p.a, rp, cp)[2]
+    small_case("sp_60x40_rebk", None, None, "rebk", 1.0 / beta, 5, rp, cp, max_iters=6000, tol=1e-10, problem=p,
+               stride=2)
+    small_case("sp_60x40_rek", None, None, "rek", 1.0, 8, None, None, max_iters=300, mode="max_iters_only",
+               problem=p, ks=(1, 10, 100, 300))
+    small_case("sp_60x40_rabk_residual", None, None, "rabk", 1.0, 9, rp, None, max_iters=3000, tol=1e-6,
+               mode="residual_proxy", problem=sparse_problem(60, 40, 0.1, 71, consistent=True), stride=4)
+    p = sparse_problem(300, 500, 0.02, 72)
+    rp, cp = K.contiguous_partition(300, 32, "row"), K.contiguous_partition(500, 50, "col")
+    beta = compute_beta_max(p.a, rp, cp)[2]
+    small_case("sp_300x500_rebk", None, None, "rebk", 1.0 / beta, 10, rp, cp, max_iters=20000, tol=1e-8, problem=p,
+               stride=1)
+
+
+def c4():
+    from paper_2001_04179_b200 import Matrix as M2, contiguous_partition as cpart
+
+    t0 = time.time()
+    s, b, xs = workloads.c4_arrays()
+    print(f"c4 built ({time.time() - t0:.1f}s)")
+    m2 = M2.from_sparse(s)
+    beta = max(workloads.power_beta(m2, cpart(200000, 2000, "row")), workloads.power_beta(m2, cpart(50000, 1000, "col")))
+    print(f"c4 beta_max={beta}")
+    mat = K.Matrix.from_sparse(s)
+    prob = K.ProblemInstance(a=mat, b=b, x_star=xs, b_perp=None, meta=K.ProblemMeta(0, None, False, 0, 0.0))
+    rp = K.contiguous_partition(200000, 2000, "row")
+    cp = K.contiguous_partition(50000, 1000, "col")
+    alpha = 1.0 / beta
+    tol = 1e-6 * float(np.linalg.norm(xs))
+    cfg = K.SolverConfig(algorithm="rebk", alpha=alpha, seed=17, row_partition=rp, col_partition=cp,
+                         max_iters=50_000, stop=K.StoppingRule(tol=tol), beta_max=beta)
+    tr = K.run(prob, cfg)
+    print(f"c4: ITER={tr.iters} conv={tr.converged} err={tr.final_error} wall={tr.wall_time:.2f}s")
+    ks = (1, 10, 100, tr.iters)
+    ctx, xs_, zs_ = snapshots(prob, K.SolverConfig(algorithm="rebk", alpha=alpha, seed=17, row_partition=rp,
+                                                   col_partition=cp, max_iters=tr.iters, beta_max=beta,
+                                                   stop=K.StoppingRule(mode="max_iters_only")), ks)
+    out = dict(alpha=alpha, beta=beta, seed=17, tol=tol, iters=tr.iters, final_error=tr.final_error,
+               ref_wall=tr.wall_time, picks=ref_picks(ctx, 17, tr.iters).astype(np.int16), ks=np.asarray(ks),
+               x_star=xs, b=b, row_cum=ctx.row_sampler.cumulative, col_cum=ctx.col_sampler.cumulative)
+    for k in ks:
+        out[f"x_{k}"] = xs_[k]
+        out[f"z_{k}"] = zs_[k]
+    np.savez_compressed(os.path.join(HERE, "c4_golden.npz"), **out)
+
+
 def big_case(name, a, b, x_star, tau_r, tau_c, beta, seed=17, rel=1e-6, max_iters=50_000,
              ks=(1, 10, 100), store_b=False):
     mat = K.Matrix.from_dense(a)
@@ -242,8 +311,13 @@ def c2():
 if __name__ == "__main__":
     philox_fixture()
     small_cases()
+    sparse_cases()
     if "--small-only" in sys.argv:
+        sys.exit(0)
+    if "--c4-only" in sys.argv:
+        c4()
         sys.exit(0)
     c1()
     if "--skip-c2" not in sys.argv:
         c2()
+    c4()

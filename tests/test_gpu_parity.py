@@ -39,8 +39,15 @@ def load(name):
 
 
 def case_problem(g):
-    a = g["a"]
-    prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=g["b"], x_star=g["x_star"], b_perp=None,
+    if "a_indptr" in g.files:
+        import scipy.sparse as sp
+
+        a = sp.csr_matrix((g["a_data"], g["a_indices"], g["a_indptr"]), shape=tuple(g["a_shape"]))
+        mat = P.Matrix.from_sparse(a)
+    else:
+        a = g["a"]
+        mat = P.Matrix.from_dense(a)
+    prob = P.ProblemInstance(a=mat, b=g["b"], x_star=g["x_star"], b_perp=None,
                              meta=P.ProblemMeta(0, None, False, 0, 0.0))
     algo = str(g["algorithm"])
     rb = [np.asarray(b, dtype=np.int64) for b in g["row_blocks"]]
@@ -327,3 +334,44 @@ def test_fast_path_taken_and_agrees_with_general_kernel(monkeypatch):
     assert t_gen.kernel_path == 0
     assert t_fast.iters == t_gen.iters
     assert rel(t_fast.x, t_gen.x) <= 1e-12 and rel(t_fast.z, t_gen.z) <= 1e-12
+
+
+def test_sparse_cases_bitwise_equal_to_reference():
+    """The sparse kernel sums in scipy's order with unfused multiply/add, so
+    its iterates equal the reference's bit for bit (tolerance kept as a
+    fallback assertion only in the message)."""
+    for case in [c for c in CASES if c.startswith("case_sp_")]:
+        g = load(case)
+        prob, cfg = case_problem(g)
+        ctx = P.prepare(prob, cfg)
+        st = ctx.initial_state()
+        ks = set(int(k) for k in g["ks"])
+        for k in range(1, max(ks) + 1):
+            ctx.step(st)
+            if k in ks:
+                assert np.array_equal(st.x, g[f"x_{k}"]), (case, k, rel(st.x, g[f"x_{k}"]))
+                if st.z is not None:
+                    assert np.array_equal(st.z, g[f"z_{k}"]), (case, k, rel(st.z, g[f"z_{k}"]))
+
+
+@pytest.mark.slow
+def test_c4_sparse_full_run_matches_reference():
+    """BASELINE config 4: CSR 200000 x 50000, 1e7 nnz, blocks 2000/1000."""
+    if not os.path.exists(os.path.join(GOLD, "c4_golden.npz")):
+        pytest.skip("c4 golden vectors not generated")
+    from paper_2001_04179_b200.workloads import c4_matrix
+
+    g = load("c4_golden.npz")
+    s, _ = c4_matrix()
+    prob = P.ProblemInstance(a=P.Matrix.from_sparse(s), b=g["b"], x_star=g["x_star"], b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    rp, cp = P.contiguous_partition(200000, 2000, "row"), P.contiguous_partition(50000, 1000, "col")
+    cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=int(g["seed"]), max_iters=50_000,
+                         row_partition=rp, col_partition=cp, stop=P.StoppingRule(tol=float(g["tol"])),
+                         beta_max=float(g["beta"]))
+    tr = P.run(prob, cfg)
+    k = int(g["iters"])
+    assert tr.kernel_path == 3
+    assert tr.converged and tr.iters == k
+    assert rel(tr.x, g[f"x_{k}"]) <= RTOL
+    assert rel(tr.z, g[f"z_{k}"]) <= RTOL

@@ -50,10 +50,19 @@ def _blocks(arr):
     return [np.asarray(b, dtype=np.int64) for b in arr]
 
 
+def case_matrix(g):
+    """Dense array, or the CSR matrix for the sparse cases."""
+    if "a_indptr" in g.files:
+        import scipy.sparse as sp
+
+        return sp.csr_matrix((g["a_data"], g["a_indices"], g["a_indptr"]), shape=tuple(g["a_shape"]))
+    return g["a"]
+
+
 def _oracle_for(g):
     algo = str(g["algorithm"])
     col = _blocks(g["col_blocks"]) if "col_blocks" in g.files else None
-    return OracleSolver(g["a"], g["b"], _blocks(g["row_blocks"]), col, float(g["alpha"]), algo)
+    return OracleSolver(case_matrix(g), g["b"], _blocks(g["row_blocks"]), col, float(g["alpha"]), algo)
 
 
 CASES = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLD, "case_*.npz")))
@@ -79,7 +88,7 @@ def test_oracle_matches_reference_case(case):
     npk = min(len(res["picks"]), len(g["picks"]))
     assert np.array_equal(res["picks"][:npk], g["picks"][:npk])
     # per-step snapshots
-    x = np.zeros(g["a"].shape[1])
+    x = np.zeros(case_matrix(g).shape[1])
     z = (g["b"].copy() if z0 is None else np.array(z0)) if orc.extended else None
     picks = orc.picks(OracleRng(int(g["seed"])), int(max(g["ks"])))
     for k in range(1, int(max(g["ks"])) + 1):
@@ -110,3 +119,24 @@ def test_oracle_c1_against_reference_run():
     assert rel <= 1e-12
     relz = np.linalg.norm(res["z"] - g[f"z_{k}"]) / np.linalg.norm(g[f"z_{k}"])
     assert relz <= 1e-12
+
+
+@pytest.mark.slow
+def test_oracle_c4_against_reference_run():
+    """C4 (sparse 200000 x 50000, 1e7 nnz, blocks 2000/1000): same ITER,
+    same block sequence, same iterates as the reference."""
+    if not os.path.exists(os.path.join(GOLD, "c4_golden.npz")):
+        pytest.skip("c4 golden vectors not generated")
+    from paper_2001_04179_b200.workloads import c4_matrix
+
+    g = _load("c4_golden.npz")
+    s, _ = c4_matrix()
+    orc = OracleSolver(s, g["b"], np.arange(0, 200001, 2000), np.arange(0, 50001, 1000), float(g["alpha"]))
+    assert np.array_equal(orc.row_sampler.cumulative, g["row_cum"])
+    assert np.array_equal(orc.col_sampler.cumulative, g["col_cum"])
+    res = orc.run(int(g["seed"]), 50_000, float(g["tol"]), g["x_star"], rng=None)
+    assert res["iters"] == int(g["iters"])
+    assert np.array_equal(res["picks"], g["picks"].astype(np.int64))
+    k = int(g["iters"])
+    assert np.linalg.norm(res["x"] - g[f"x_{k}"]) <= 1e-12 * np.linalg.norm(g[f"x_{k}"])
+    assert np.linalg.norm(res["z"] - g[f"z_{k}"]) <= 1e-12 * np.linalg.norm(g[f"z_{k}"])
