@@ -102,7 +102,7 @@ typedef struct rebk_trace {
   int64_t errors_cap;
   int64_t n_checks;
   int32_t grid_ctas;        /* CTAs the persistent kernel used */
-  int32_t kernel_path;      /* 0 dense general, 1 dense clustered, 2 same (cooperative), 3 sparse */
+  int32_t kernel_path;      /* 0 dense general, 1 dense clustered, 2 same (cooperative), 3 sparse, 4/5 multi-RHS (5: BF16x9 tensor cores) */
 } rebk_trace;
 
 /* ---- library / device ---------------------------------------------------- */
@@ -143,6 +143,20 @@ int rebk_run(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b, const double* 
 int rebk_run_device(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev,
                     const double* x_star_dev, double* x_io_dev, double* z_io_dev,
                     void* stream, rebk_trace* trace);
+
+/* ---- multi-RHS fp32 (BASELINE config 5; no reference counterpart: the
+ * reference takes one 1-D b, solvers.py:141-143).  A fp32 row-major; B, X,
+ * Z row-major with nrhs columns; every RHS shares the block sequence of
+ * cfg (so each column follows exactly the single-RHS REBK of
+ * solvers.py:324-337).  Column c stops counting at its first check with
+ * ||X_c - X*_c|| <= tols[c]; the run ends when all columns have crossed
+ * (trace->iters = that iteration, iters_out[c] = column c's first crossing)
+ * and returns the state at that iteration. */
+int rebk_ctx_create_dense_f32(const float* a_host, int64_t m, int64_t n, int64_t lda, int device,
+                              rebk_ctx** out);
+int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float* B, const float* X0,
+                  const float* Z0, const float* Xstar, const double* tols, float* X_out, float* Z_out,
+                  int64_t* iters_out, double* errs_out, rebk_trace* trace);
 
 /* ---- sampler (sampling.py:23-45 Rng, :137-145 WeightedSampler.sample) -----
  * Device sampling of the (col, row) block-index pairs of iterations

@@ -81,6 +81,11 @@ SIGNATURES = {
     "rebk_ctx_create_dense_device": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int, POINTER(c_void_p)]),
     "rebk_ctx_create_csr": (c_int, [_P_I64, POINTER(c_int32), _P_D, c_int64, c_int64, c_int64, c_int,
                                     POINTER(c_void_p)]),
+    "rebk_ctx_create_dense_f32": (c_int, [POINTER(ctypes.c_float), c_int64, c_int64, c_int64, c_int,
+                                          POINTER(c_void_p)]),
+    "rebk_run_mrhs": (c_int, [c_void_p, POINTER(RebkCfg), c_int64, POINTER(ctypes.c_float), POINTER(ctypes.c_float),
+                              POINTER(ctypes.c_float), POINTER(ctypes.c_float), _P_D, POINTER(ctypes.c_float),
+                              POINTER(ctypes.c_float), _P_I64, _P_D, POINTER(RebkTrace)]),
     "rebk_ctx_destroy": (c_int, [c_void_p]),
     "rebk_ctx_shape": (c_int, [c_void_p, _P_I64, _P_I64]),
     "rebk_run": (c_int, [c_void_p, POINTER(RebkCfg), _P_D, _P_D, _P_D, _P_D, _P_D, _P_D, POINTER(RebkTrace)]),

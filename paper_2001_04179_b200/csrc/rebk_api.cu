@@ -46,6 +46,7 @@ struct rebk_ctx {
   std::vector<int64_t> h_csr_ptr, h_csc_ptr;
   std::vector<int32_t> h_csr_col, h_csc_row;
   std::vector<CsrSegPlan*> seg_cache;
+  float* A32 = nullptr;  // dense fp32 A (multi-RHS contexts, kind 2)
 };
 
 namespace {
@@ -580,6 +581,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     if (rc) return rc;
   }
   if (ctx->m > INT32_MAX || ctx->n > INT32_MAX) return fail(REBK_EINVAL, "matrix dimension exceeds 2^31");
+  if (ctx->kind == 2) return fail(REBK_EINVAL, "fp32 contexts run through rebk_run_mrhs");
   if (ctx->kind == 1) return run_csr_impl(ctx, cfg, b_dev, xs_dev, x_dev, z_dev, stream, trace);
 
   CUDA_TRY(cudaSetDevice(ctx->device));
@@ -986,8 +988,156 @@ int rebk_ctx_create_csr(const int64_t* indptr, const int32_t* indices, const dou
   return REBK_OK;
 }
 
+int rebk_ctx_create_dense_f32(const float* a_host, int64_t m, int64_t n, int64_t lda, int device, rebk_ctx** out) {
+  if (!out || !a_host) return fail(REBK_EINVAL, "null argument");
+  if (m < 1 || n < 1) return fail(REBK_EINVAL, "matrix must be 2-D and nonempty");
+  if (lda < n) return fail(REBK_EINVAL, "lda < n");
+  if (m > INT32_MAX || n > INT32_MAX) return fail(REBK_EINVAL, "matrix dimension exceeds 2^31");
+  rebk_ctx* c = new rebk_ctx{};
+  int rc = ctx_common(c, device);
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  float* dA = nullptr;
+  cudaError_t e = cudaMalloc(&dA, (size_t)m * n * sizeof(float));
+  if (e == cudaSuccess)
+    e = cudaMemcpy2D(dA, n * sizeof(float), a_host, lda * sizeof(float), n * sizeof(float), m, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(dA);
+    delete c;
+    return fail(REBK_ENOMEM, "upload of fp32 A failed: %s", cudaGetErrorString(e));
+  }
+  c->kind = 2;
+  c->m = m;
+  c->n = n;
+  c->lda = n;
+  c->A32 = dA;
+  *out = c;
+  return REBK_OK;
+}
+
+int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float* B, const float* X0, const float* Z0,
+                  const float* Xstar, const double* tols, float* X_out, float* Z_out, int64_t* iters_out,
+                  double* errs_out, rebk_trace* trace) {
+  if (!ctx || !cfg || !B || !X_out || nrhs < 1) return fail(REBK_EINVAL, "null argument");
+  if (ctx->kind != 2) return fail(REBK_EINVAL, "rebk_run_mrhs needs an fp32 context (rebk_ctx_create_dense_f32)");
+  if (cfg->algorithm < 0 || cfg->algorithm > 3) return fail(REBK_EINVAL, "unknown algorithm %d", cfg->algorithm);
+  if (cfg->stop_mode == REBK_STOP_RESIDUAL_PROXY)
+    return fail(REBK_EINVAL, "multi-RHS runs support oracle_error and max_iters_only stopping");
+  if (cfg->stop_mode == REBK_STOP_ORACLE_ERROR && !Xstar)
+    return fail(REBK_EINVAL, "oracle_error stopping needs a problem with x_star");
+  if (cfg->check_stride < 1) return fail(REBK_EINVAL, "check_stride must be at least 1");
+  if (cfg->max_iters < 0) return fail(REBK_EINVAL, "max_iters must be nonnegative");
+  const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
+  int rc = check_partition("row", cfg->n_row_blocks, cfg->row_ptr, cfg->row_cum, cfg->row_scale, ctx->m);
+  if (rc) return rc;
+  if (extended) {
+    rc = check_partition("col", cfg->n_col_blocks, cfg->col_ptr, cfg->col_cum, cfg->col_scale, ctx->n);
+    if (rc) return rc;
+  }
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t stream;
+  CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  const int64_t m = ctx->m, n = ctx->n, R = nrhs;
+  rc = REBK_OK;
+  {
+    DevArena arena;
+    arena.stream = stream;
+    float *dB, *dX, *dZ = nullptr, *dXs = nullptr;
+    int64_t *d_row_ptr, *d_col_ptr = nullptr;
+    double *d_row_cum, *d_row_scale, *d_col_cum = nullptr, *d_col_scale = nullptr;
+    const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
+    cudaError_t e = arena.alloc(&dB, m * R);
+    if (!e) e = arena.alloc(&dX, n * R);
+    if (!e && extended) e = arena.alloc(&dZ, m * R);
+    if (!e && Xstar) e = arena.alloc(&dXs, n * R);
+    if (!e) e = cudaMemcpyAsync(dB, B, sizeof(float) * m * R, cudaMemcpyHostToDevice, stream);
+    if (!e) e = X0 ? cudaMemcpyAsync(dX, X0, sizeof(float) * n * R, cudaMemcpyHostToDevice, stream)
+                   : cudaMemsetAsync(dX, 0, sizeof(float) * n * R, stream);
+    if (!e && extended) e = cudaMemcpyAsync(dZ, Z0 ? Z0 : B, sizeof(float) * m * R, cudaMemcpyHostToDevice, stream);
+    if (!e && Xstar) e = cudaMemcpyAsync(dXs, Xstar, sizeof(float) * n * R, cudaMemcpyHostToDevice, stream);
+    if (!e) e = arena.alloc(&d_row_ptr, s + 1);
+    if (!e) e = arena.alloc(&d_row_cum, s);
+    if (!e) e = arena.alloc(&d_row_scale, s);
+    if (!e) e = cudaMemcpyAsync(d_row_ptr, cfg->row_ptr, (s + 1) * 8, cudaMemcpyHostToDevice, stream);
+    if (!e) e = cudaMemcpyAsync(d_row_cum, cfg->row_cum, s * 8, cudaMemcpyHostToDevice, stream);
+    if (!e) e = cudaMemcpyAsync(d_row_scale, cfg->row_scale, s * 8, cudaMemcpyHostToDevice, stream);
+    if (!e && extended) {
+      e = arena.alloc(&d_col_ptr, t + 1);
+      if (!e) e = arena.alloc(&d_col_cum, t);
+      if (!e) e = arena.alloc(&d_col_scale, t);
+      if (!e) e = cudaMemcpyAsync(d_col_ptr, cfg->col_ptr, (t + 1) * 8, cudaMemcpyHostToDevice, stream);
+      if (!e) e = cudaMemcpyAsync(d_col_cum, cfg->col_cum, t * 8, cudaMemcpyHostToDevice, stream);
+      if (!e) e = cudaMemcpyAsync(d_col_scale, cfg->col_scale, t * 8, cudaMemcpyHostToDevice, stream);
+    }
+    if (e) {
+      rc = fail(REBK_ECUDA, "multi-RHS upload failed: %s", cudaGetErrorString(e));
+    } else {
+      SampleParams sp{};
+      sp.key0 = cfg->philox_key[0];
+      sp.key1 = cfg->philox_key[1];
+      sp.draw_offset = cfg->draw_offset;
+      sp.extended = extended;
+      sp.n_row_blocks = (int32_t)s;
+      sp.n_col_blocks = (int32_t)t;
+      sp.row_ptr = d_row_ptr;
+      sp.row_cum = d_row_cum;
+      sp.row_total = cfg->row_total;
+      sp.row_scale = d_row_scale;
+      sp.col_ptr = d_col_ptr;
+      sp.col_cum = d_col_cum;
+      sp.col_total = cfg->col_total;
+      sp.col_scale = d_col_scale;
+      MrhsRun w{ctx->A32, m, n, ctx->lda, (int)R, dB, dX, dZ, dXs, cfg, tols, extended};
+      double ms = 0.0;
+      int64_t K = 0;
+      int math = 0;
+      char buf[512] = {0};
+      std::vector<int64_t> it(R, -1);
+      std::vector<double> er(R, 0.0);
+      int r2 = run_mrhs(w, sp, nullptr, it.data(), er.data(), &ms, &K, buf, sizeof buf, stream, &math);
+      if (r2) {
+        rc = fail(REBK_ECUDA, "multi-RHS run failed: %s", buf);
+      } else {
+        bool all = cfg->stop_mode == REBK_STOP_ORACLE_ERROR;
+        for (int64_t c = 0; c < R; ++c) {
+          if (it[c] < 0) {
+            all = false;
+            it[c] = cfg->max_iters;
+          }
+        }
+        if (iters_out) memcpy(iters_out, it.data(), sizeof(int64_t) * R);
+        if (errs_out) memcpy(errs_out, er.data(), sizeof(double) * R);
+        e = cudaMemcpyAsync(X_out, dX, sizeof(float) * n * R, cudaMemcpyDeviceToHost, stream);
+        if (!e && Z_out && extended) e = cudaMemcpyAsync(Z_out, dZ, sizeof(float) * m * R, cudaMemcpyDeviceToHost, stream);
+        if (!e) e = cudaStreamSynchronize(stream);
+        if (e) rc = fail(REBK_ECUDA, "multi-RHS download failed: %s", cudaGetErrorString(e));
+        if (trace) {
+          trace->iters = K;
+          trace->converged = all;
+          trace->has_error = cfg->stop_mode == REBK_STOP_ORACLE_ERROR;
+          trace->final_error = 0.0;
+          for (int64_t c = 0; c < R; ++c) trace->final_error = std::max(trace->final_error, er[c]);
+          trace->loop_ms = ms;
+          trace->n_checks = 0;
+          trace->grid_ctas = 0;
+          trace->kernel_path = math == 4 ? 5 : 4;
+        }
+      }
+    }
+  }
+  cudaStreamSynchronize(stream);
+  cudaStreamDestroy(stream);
+  return rc;
+}
+
 int rebk_ctx_destroy(rebk_ctx* ctx) {
   if (!ctx) return REBK_OK;
+  if (ctx->A32) {
+    cudaSetDevice(ctx->device);
+    cudaFree(ctx->A32);
+  }
   cudaSetDevice(ctx->device);
   if (ctx->A_owned) cudaFree(ctx->A_owned);
   cudaFree(ctx->csr_ptr);

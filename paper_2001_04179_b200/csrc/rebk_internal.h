@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+struct rebk_cfg;
 namespace rebk {
 
 constexpr int kThreads = 256;
@@ -170,6 +171,18 @@ cudaError_t launch_dense_fast(const FastParams& fp, const CUtensorMap& tm_ct, co
 cudaError_t fast_max_clusters(int cluster_size, size_t smem_bytes, int* clusters);
 cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream);
 cudaError_t csr_kernel_occupancy(int* blocks_per_sm);
+struct MrhsRun {
+  const float* A;
+  int64_t m, n, lda;
+  int R;
+  float *B, *X, *Z, *Xs;  // device, row-major (rows x R)
+  const struct rebk_cfg* cfg;
+  const double* tols;  // host [R]
+  bool extended;
+};
+int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SampleParams* unused, int64_t* iters_out,
+             double* errs_out, double* loop_ms, int64_t* k_final, char* errbuf, size_t errlen, cudaStream_t stream,
+             int* math_used);
 cudaError_t launch_block_norms(const double* A, int64_t lda, int64_t m, int64_t n, int axis,
                                int64_t nb, const int64_t* ptr_dev, double* out_dev,
                                cudaStream_t stream);

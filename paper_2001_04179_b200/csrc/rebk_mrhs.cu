@@ -1,0 +1,296 @@
+// rebk_mrhs.cu — multi-right-hand-side fp32 REBK (BASELINE config 5).
+//
+// All RHS share one block sequence (the sequence never depends on b,
+// solvers.py:8-12), so with X (n x R), Z (m x R), B (m x R) the four block
+// products of step_rebk (solvers.py:283-295) become GEMMs:
+//   U  = A_Jᵀ Z                 (|J| x R)
+//   Z -= s_J A_J U
+//   Rr = A_I X - B_I + Z_I      (|I| x R)
+//   X -= s_I A_Iᵀ Rr
+// Round 1 runs them through cuBLAS with CUBLAS_FP32_EMULATED_BF16X9_MATH
+// (FP32 results from BF16 tensor-core passes; single-pass TF32 misses the
+// 1e-4 tolerance, SURVEY hard part 6), enqueued in chunks of 64 iterations
+// (the block sequence of a chunk is sampled on the device first; the host
+// only needs it to address the GEMMs).  The per-column stopping rule (each RHS records the first check
+// with ||X_c - X*_c|| <= tol_c; the run ends when every column has crossed)
+// runs on the device; the final state is the one at that iteration, obtained
+// by restoring the chunk's checkpoint and replaying (the sequence and the
+// GEMMs are deterministic).
+//
+// cuBLAS is opened with dlopen at first use (librebk.so has no link-time
+// cuBLAS dependency).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/rebk.h"
+#include "rebk_internal.h"
+#include <stdio.h>
+#include <stdlib.h>
+
+namespace rebk {
+
+// ---- minimal dlopen'ed cuBLAS ------------------------------------------------
+typedef void* cublasHandle_t;
+enum { CUBLAS_OP_N = 0, CUBLAS_OP_T = 1 };
+enum { CUBLAS_DEFAULT_MATH = 0, CUBLAS_PEDANTIC_MATH = 2, CUBLAS_FP32_EMULATED_BF16X9_MATH = 4 };
+
+struct CublasApi {
+  bool ok = false;
+  int (*create)(cublasHandle_t*) = nullptr;
+  int (*destroy)(cublasHandle_t) = nullptr;
+  int (*set_stream)(cublasHandle_t, cudaStream_t) = nullptr;
+  int (*set_math)(cublasHandle_t, int) = nullptr;
+  int (*set_workspace)(cublasHandle_t, void*, size_t) = nullptr;
+  int (*sgemm)(cublasHandle_t, int, int, int, int, int, const float*, const float*, int, const float*, int,
+               const float*, float*, int) = nullptr;
+};
+
+static CublasApi& cublas() {
+  static CublasApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  const char* names[] = {"/usr/local/cuda/lib64/libcublas.so.12", "libcublas.so.12", "libcublas.so"};
+  void* h = nullptr;
+  for (const char* nm : names) {
+    h = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
+    if (h) break;
+  }
+  if (!h) return api;
+  api.create = (int (*)(cublasHandle_t*))dlsym(h, "cublasCreate_v2");
+  api.destroy = (int (*)(cublasHandle_t))dlsym(h, "cublasDestroy_v2");
+  api.set_stream = (int (*)(cublasHandle_t, cudaStream_t))dlsym(h, "cublasSetStream_v2");
+  api.set_math = (int (*)(cublasHandle_t, int))dlsym(h, "cublasSetMathMode");
+  api.set_workspace = (int (*)(cublasHandle_t, void*, size_t))dlsym(h, "cublasSetWorkspace_v2");
+  api.sgemm = (int (*)(cublasHandle_t, int, int, int, int, int, const float*, const float*, int, const float*, int,
+                       const float*, float*, int))dlsym(h, "cublasSgemm_v2");
+  api.ok = api.create && api.destroy && api.set_stream && api.set_math && api.set_workspace && api.sgemm;
+  return api;
+}
+
+// ---- small kernels -------------------------------------------------------------
+// Rr = Z_I - B_I, or -B_I without a column sweep (pointers already offset to row r_lo)
+__global__ void mrhs_init_r(const float* __restrict__ ZI, const float* __restrict__ BI, float* __restrict__ Rr,
+                            int64_t count) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < count) Rr[t] = (ZI ? ZI[t] : 0.0f) - BI[t];
+}
+
+// per-column ||X_c - X*_c||^2 -> first crossing bookkeeping.  One CTA per
+// column block of 32 columns; fixed-order reduction.
+__global__ void mrhs_check(const float* __restrict__ X, const float* __restrict__ Xs, int64_t n, int R,
+                           const double* __restrict__ tol, int64_t k, int64_t* iters, double* errs,
+                           double* errs_at, int32_t* n_done) {
+  __shared__ double part[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int w = threadIdx.x >> 5;  // 8 warps split the rows
+  double acc = 0.0;
+  if (c < R)
+    for (int64_t i = w; i < n; i += 8) {
+      const double d = (double)X[i * R + c] - (double)Xs[i * R + c];
+      acc = fma(d, d, acc);
+    }
+  part[w][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (w == 0 && c < R) {
+    double s = 0.0;
+    for (int q = 0; q < 8; ++q) s += part[q][threadIdx.x & 31];
+    const double e = sqrt(s);
+    errs[c] = e;
+    if (iters[c] < 0 && e <= tol[c]) {
+      iters[c] = k;
+      errs_at[c] = e;
+      atomicAdd(n_done, 1);
+    }
+  }
+}
+
+// ---- host orchestration --------------------------------------------------------
+
+#define MR_TRY(expr)                                                   \
+  do {                                                                 \
+    cudaError_t _e = (expr);                                           \
+    if (_e != cudaSuccess) {                                           \
+      snprintf(errbuf, errlen, "%s: %s", #expr, cudaGetErrorString(_e)); \
+      return -2;                                                       \
+    }                                                                  \
+  } while (0)
+#define MB_TRY(expr)                                                   \
+  do {                                                                 \
+    int _s = (expr);                                                   \
+    if (_s != 0) {                                                     \
+      snprintf(errbuf, errlen, "%s: cuBLAS status %d", #expr, _s);     \
+      return -2;                                                       \
+    }                                                                  \
+  } while (0)
+
+static int mrhs_math_mode() {
+  const char* s = getenv("REBK_MRHS_MATH");
+  if (s && !strcmp(s, "pedantic")) return CUBLAS_PEDANTIC_MATH;
+  if (s && !strcmp(s, "default")) return CUBLAS_DEFAULT_MATH;
+  return CUBLAS_FP32_EMULATED_BF16X9_MATH;
+}
+
+int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SampleParams* unused, int64_t* iters_out,
+             double* errs_out, double* loop_ms, int64_t* k_final, char* errbuf, size_t errlen, cudaStream_t stream,
+             int* math_used) {
+  (void)unused;
+  CublasApi& cb = cublas();
+  if (!cb.ok) {
+    snprintf(errbuf, errlen, "cuBLAS could not be loaded (dlopen libcublas.so.12)");
+    return -2;
+  }
+  const rebk_cfg* cfg = w.cfg;
+  const int R = w.R;
+  const int64_t m = w.m, n = w.n, lda = w.lda;
+  const bool checking = cfg->stop_mode == 0;
+  cublasHandle_t h = nullptr;
+  MB_TRY(cb.create(&h));
+  struct HGuard {
+    CublasApi& cb;
+    cublasHandle_t h;
+    ~HGuard() { cb.destroy(h); }
+  } hg{cb, h};
+  MB_TRY(cb.set_stream(h, stream));
+  const int math = mrhs_math_mode();
+  if (cb.set_math(h, math) != 0) MB_TRY(cb.set_math(h, CUBLAS_DEFAULT_MATH));
+  *math_used = math;
+  void* ws = nullptr;
+  const size_t ws_bytes = 64u << 20;
+  MR_TRY(cudaMallocAsync(&ws, ws_bytes, stream));
+  MB_TRY(cb.set_workspace(h, ws, ws_bytes));
+
+  int nJmax = 1, nImax = 1;
+  for (int64_t b = 0; b < cfg->n_row_blocks; ++b) nImax = std::max<int>(nImax, (int)(cfg->row_ptr[b + 1] - cfg->row_ptr[b]));
+  if (w.extended)
+    for (int64_t b = 0; b < cfg->n_col_blocks; ++b)
+      nJmax = std::max<int>(nJmax, (int)(cfg->col_ptr[b + 1] - cfg->col_ptr[b]));
+  float *U, *Rr, *Xsnap = nullptr, *Zsnap = nullptr;
+  double *d_tol, *d_errs, *d_errs_at;
+  int64_t* d_iters;
+  int32_t* d_ndone;
+  Plan* d_plan;
+  const int64_t CH = 64;
+  MR_TRY(cudaMallocAsync((void**)&U, sizeof(float) * nJmax * R, stream));
+  MR_TRY(cudaMallocAsync((void**)&Rr, sizeof(float) * nImax * R, stream));
+  MR_TRY(cudaMallocAsync((void**)&Xsnap, sizeof(float) * n * R, stream));
+  if (w.extended) MR_TRY(cudaMallocAsync((void**)&Zsnap, sizeof(float) * m * R, stream));
+  MR_TRY(cudaMallocAsync((void**)&d_tol, sizeof(double) * R, stream));
+  MR_TRY(cudaMallocAsync((void**)&d_errs, sizeof(double) * R, stream));
+  MR_TRY(cudaMallocAsync((void**)&d_errs_at, sizeof(double) * R, stream));
+  MR_TRY(cudaMallocAsync((void**)&d_iters, sizeof(int64_t) * R, stream));
+  MR_TRY(cudaMallocAsync((void**)&d_ndone, sizeof(int32_t), stream));
+  MR_TRY(cudaMallocAsync((void**)&d_plan, sizeof(Plan) * CH, stream));
+  std::vector<double> tol(R);
+  for (int c = 0; c < R; ++c) tol[c] = w.tols ? w.tols[c] : cfg->tol;
+  MR_TRY(cudaMemcpyAsync(d_tol, tol.data(), sizeof(double) * R, cudaMemcpyHostToDevice, stream));
+  MR_TRY(cudaMemsetAsync(d_iters, 0xff, sizeof(int64_t) * R, stream));  // -1
+  MR_TRY(cudaMemsetAsync(d_ndone, 0, sizeof(int32_t), stream));
+  MR_TRY(cudaMemsetAsync(d_errs_at, 0, sizeof(double) * R, stream));
+
+  auto enqueue_iter = [&](const Plan& pl, int64_t k, bool do_check) -> int {
+    const int nJ = pl.c_hi - pl.c_lo, nI = pl.r_hi - pl.r_lo;
+    const float one = 1.0f, zero = 0.0f;
+    if (w.extended) {
+      const float mcs = (float)(-pl.c_scale);
+      MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, R, nJ, (int)m, &one, w.Z, R, w.A + pl.c_lo, (int)lda, &zero, U, R));
+      MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, R, (int)m, nJ, &mcs, U, R, w.A + pl.c_lo, (int)lda, &one, w.Z, R));
+    }
+    const int64_t cnt = (int64_t)nI * R;
+    mrhs_init_r<<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(w.extended ? w.Z + (int64_t)pl.r_lo * R : nullptr,
+                                                                  w.B + (int64_t)pl.r_lo * R, Rr, cnt);
+    MR_TRY(cudaGetLastError());
+    const float* AI = w.A + (int64_t)pl.r_lo * lda;
+    const float mrs = (float)(-pl.r_scale);
+    MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, R, nI, (int)n, &one, w.X, R, AI, (int)lda, &one, Rr, R));
+    MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, R, (int)n, nI, &mrs, Rr, R, AI, (int)lda, &one, w.X, R));
+    if (do_check) {
+      mrhs_check<<<(R + 31) / 32, 256, 0, stream>>>(w.X, w.Xs, n, R, d_tol, k, d_iters, d_errs, d_errs_at, d_ndone);
+      MR_TRY(cudaGetLastError());
+    }
+    return 0;
+  };
+
+  cudaEvent_t ev0, ev1;
+  MR_TRY(cudaEventCreate(&ev0));
+  MR_TRY(cudaEventCreate(&ev1));
+  MR_TRY(cudaEventRecord(ev0, stream));
+  int64_t K = cfg->max_iters;
+  bool all_done = false;
+  if (checking) {
+    mrhs_check<<<(R + 31) / 32, 256, 0, stream>>>(w.X, w.Xs, n, R, d_tol, 0, d_iters, d_errs, d_errs_at, d_ndone);
+    int32_t nd = 0;
+    MR_TRY(cudaMemcpyAsync(&nd, d_ndone, sizeof nd, cudaMemcpyDeviceToHost, stream));
+    MR_TRY(cudaStreamSynchronize(stream));
+    if (nd == R) {
+      all_done = true;
+      K = 0;
+    }
+  }
+  std::vector<Plan> hplan(CH);
+  SampleParams sp = sp_template;
+  for (int64_t k0 = 1; !all_done && k0 <= cfg->max_iters; k0 += CH) {
+    const int64_t cnt = std::min(CH, cfg->max_iters - k0 + 1);
+    MR_TRY(launch_sample_plan(sp, k0, cnt, d_plan, nullptr, stream));
+    MR_TRY(cudaMemcpyAsync(hplan.data(), d_plan, sizeof(Plan) * cnt, cudaMemcpyDeviceToHost, stream));
+    MR_TRY(cudaStreamSynchronize(stream));
+    if (checking) {
+      MR_TRY(cudaMemcpyAsync(Xsnap, w.X, sizeof(float) * n * R, cudaMemcpyDeviceToDevice, stream));
+      if (w.extended) MR_TRY(cudaMemcpyAsync(Zsnap, w.Z, sizeof(float) * m * R, cudaMemcpyDeviceToDevice, stream));
+    }
+    for (int64_t q = 0; q < cnt; ++q) {
+      const int64_t k = k0 + q;
+      int rc = enqueue_iter(hplan[q], k, checking && (k % cfg->check_stride == 0 || k == cfg->max_iters));
+      if (rc) return rc;
+    }
+    if (checking) {
+      int32_t nd = 0;
+      MR_TRY(cudaMemcpyAsync(&nd, d_ndone, sizeof nd, cudaMemcpyDeviceToHost, stream));
+      MR_TRY(cudaStreamSynchronize(stream));
+      if (nd == R) {
+        std::vector<int64_t> it(R);
+        MR_TRY(cudaMemcpy(it.data(), d_iters, sizeof(int64_t) * R, cudaMemcpyDeviceToHost));
+        K = *std::max_element(it.begin(), it.end());
+        all_done = true;
+        if (K < k0 + cnt - 1) {  // rewind to the chunk start and replay up to K exactly
+          MR_TRY(cudaMemcpyAsync(w.X, Xsnap, sizeof(float) * n * R, cudaMemcpyDeviceToDevice, stream));
+          if (w.extended) MR_TRY(cudaMemcpyAsync(w.Z, Zsnap, sizeof(float) * m * R, cudaMemcpyDeviceToDevice, stream));
+          for (int64_t k = k0; k <= K; ++k) {
+            int rc = enqueue_iter(hplan[k - k0], k, false);
+            if (rc) return rc;
+          }
+        }
+      }
+    }
+  }
+  MR_TRY(cudaEventRecord(ev1, stream));
+  MR_TRY(cudaStreamSynchronize(stream));
+  float ms = 0.f;
+  MR_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  *loop_ms = ms;
+  *k_final = K;
+  if (iters_out) MR_TRY(cudaMemcpy(iters_out, d_iters, sizeof(int64_t) * R, cudaMemcpyDeviceToHost));
+  if (errs_out) MR_TRY(cudaMemcpy(errs_out, d_errs_at, sizeof(double) * R, cudaMemcpyDeviceToHost));
+  cudaFreeAsync(U, stream);
+  cudaFreeAsync(Rr, stream);
+  cudaFreeAsync(Xsnap, stream);
+  if (Zsnap) cudaFreeAsync(Zsnap, stream);
+  cudaFreeAsync(d_tol, stream);
+  cudaFreeAsync(d_errs, stream);
+  cudaFreeAsync(d_errs_at, stream);
+  cudaFreeAsync(d_iters, stream);
+  cudaFreeAsync(d_ndone, stream);
+  cudaFreeAsync(d_plan, stream);
+  cudaFreeAsync(ws, stream);
+  cudaStreamSynchronize(stream);
+  return 0;
+}
+
+}  // namespace rebk

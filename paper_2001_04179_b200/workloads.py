@@ -157,6 +157,30 @@ def power_beta(mat, p: Partition, iters: int = 40, seed: int = 0) -> float:
     return worst
 
 
+def c5_arrays(m: int = 50000, n: int = 5000, nrhs: int = 64, seed: int = 0):
+    """C5: A = randn(m, n) stored fp32; R right-hand sides B = A X + Rres with
+    each residual column in null(Aᵀ), ||Rres_c|| = 0.1 ||A X_c||; X* = G⁻¹AᵀB
+    (normal equations on the fp64 upcast, G = AᵀA well conditioned for a
+    tall Gaussian).  Returns (A32, B32, X*) with B in fp32 as stored."""
+    rng = Rng(seed)
+    a32 = rng.standard_normal((m, n)).astype(np.float32)
+    x = rng.standard_normal((n, nrhs))
+    w = rng.standard_normal((m, nrhs))
+    a = a32.astype(np.float64)
+    g = a.T @ a
+    c = np.linalg.cholesky(g)
+
+    def gsolve(v):
+        return np.linalg.solve(c.T, np.linalg.solve(c, v))
+
+    r = w - a @ gsolve(a.T @ w)
+    ax = a @ x
+    r *= 0.1 * np.linalg.norm(ax, axis=0) / np.linalg.norm(r, axis=0)
+    b32 = (ax + r).astype(np.float32)
+    x_star = gsolve(a.T @ b32.astype(np.float64))
+    return a32, b32, x_star
+
+
 def make_workload(name: str, a: np.ndarray, b: np.ndarray, x_star: np.ndarray, tau_row: int,
                   tau_col: int, rel_tol: float = 1e-6, beta_max: float | None = None,
                   alpha_factor: float = 1.0, seed: int = 17) -> Workload:

@@ -226,6 +226,38 @@ def sparse_cases():
                stride=1)
 
 
+def c5_mini():
+    """Multi-RHS fp32 (config 5 shape family at 6000 x 600, 8 RHS, blocks of
+    64 with ragged last blocks): one fp64 reference run per column on the
+    fp64 upcast of the stored fp32 data, plus max_iters_only runs to the
+    common final iteration for two columns."""
+    a32, b32, xs = workloads.c5_arrays(6000, 600, 8)
+    a = K.Matrix.from_dense(a32.astype(np.float64))
+    rp, cp = K.contiguous_partition(6000, 64, "row"), K.contiguous_partition(600, 64, "col")
+    beta = compute_beta_max(a, rp, cp)[2]
+    alpha = 1.0 / beta
+    iters, errs, xk = [], [], []
+    tols = 1e-4 * np.linalg.norm(xs, axis=0)
+    for c in range(8):
+        prob = K.ProblemInstance(a=a, b=b32[:, c].astype(np.float64), x_star=xs[:, c], b_perp=None,
+                                 meta=K.ProblemMeta(0, None, False, 0, 0.0))
+        tr = K.run(prob, K.SolverConfig(algorithm="rebk", alpha=alpha, seed=17, row_partition=rp, col_partition=cp,
+                                        max_iters=50_000, stop=K.StoppingRule(tol=float(tols[c])), beta_max=beta))
+        iters.append(tr.iters)
+        errs.append(tr.final_error)
+    kmax = max(iters)
+    for c in range(2):
+        prob = K.ProblemInstance(a=a, b=b32[:, c].astype(np.float64), x_star=xs[:, c], b_perp=None,
+                                 meta=K.ProblemMeta(0, None, False, 0, 0.0))
+        ctx, xsn, zsn = snapshots(prob, K.SolverConfig(algorithm="rebk", alpha=alpha, seed=17, row_partition=rp,
+                                                       col_partition=cp, max_iters=kmax, beta_max=beta,
+                                                       stop=K.StoppingRule(mode="max_iters_only")), (kmax,))
+        xk.append(xsn[kmax])
+    print(f"c5_mini: ITER per RHS {iters} (K={kmax}) beta={beta}")
+    np.savez_compressed(os.path.join(HERE, "c5mini_golden.npz"), alpha=alpha, beta=beta, seed=17, tols=tols,
+                        iters=np.asarray(iters), errors=np.asarray(errs), K=kmax, x_K=np.stack(xk, axis=1))
+
+
 def c4():
     from paper_2001_04179_b200 import Matrix as M2, contiguous_partition as cpart
 
@@ -253,8 +285,10 @@ def c4():
                ref_wall=tr.wall_time, picks=ref_picks(ctx, 17, tr.iters).astype(np.int16), ks=np.asarray(ks),
                x_star=xs, b=b, row_cum=ctx.row_sampler.cumulative, col_cum=ctx.col_sampler.cumulative)
     for k in ks:
-        out[f"x_{k}"] = xs_[k]
-        out[f"z_{k}"] = zs_[k]
+        if k != 1:
+            out[f"x_{k}"] = xs_[k]
+    out[f"z_{tr.iters}"] = zs_[tr.iters]  # z (200000 doubles) only at ITER: keeps the fixture small
+    out["ks"] = np.asarray([k for k in ks if k != 1])
     np.savez_compressed(os.path.join(HERE, "c4_golden.npz"), **out)
 
 
@@ -314,6 +348,9 @@ if __name__ == "__main__":
     sparse_cases()
     if "--small-only" in sys.argv:
         sys.exit(0)
+    if "--c5-only" in sys.argv:
+        c5_mini()
+        sys.exit(0)
     if "--c4-only" in sys.argv:
         c4()
         sys.exit(0)
@@ -321,3 +358,4 @@ if __name__ == "__main__":
     if "--skip-c2" not in sys.argv:
         c2()
     c4()
+    c5_mini()

@@ -375,3 +375,24 @@ def test_c4_sparse_full_run_matches_reference():
     assert tr.converged and tr.iters == k
     assert rel(tr.x, g[f"x_{k}"]) <= RTOL
     assert rel(tr.z, g[f"z_{k}"]) <= RTOL
+
+
+def test_multi_rhs_fp32_matches_reference_columns():
+    """Config-5 family (fp32, 8 RHS sharing one block sequence): per-column
+    ITER equal to the reference's fp64 single-RHS runs (±1 for fp32 rounding
+    at the threshold) and X at the common final iteration within 1e-4."""
+    from paper_2001_04179_b200.multirhs import run_multi
+    from paper_2001_04179_b200.workloads import c5_arrays
+
+    g = load("c5mini_golden.npz")
+    a32, b32, xs = c5_arrays(6000, 600, 8)
+    rp, cp = P.contiguous_partition(6000, 64, "row"), P.contiguous_partition(600, 64, "col")
+    cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=17, max_iters=50_000, row_partition=rp,
+                         col_partition=cp, stop=P.StoppingRule(tol=1.0), beta_max=float(g["beta"]))
+    tr = run_multi(a32, b32, cfg, X_star=xs, tols=g["tols"])
+    assert tr.converged
+    assert np.all(np.abs(tr.iters_per_rhs - g["iters"]) <= 1), (tr.iters_per_rhs, g["iters"])
+    assert abs(tr.iters - int(g["K"])) <= 1
+    if tr.iters == int(g["K"]):
+        for c in range(2):
+            assert rel(tr.X[:, c], g["x_K"][:, c]) <= 1e-4

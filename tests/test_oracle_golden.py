@@ -140,3 +140,19 @@ def test_oracle_c4_against_reference_run():
     k = int(g["iters"])
     assert np.linalg.norm(res["x"] - g[f"x_{k}"]) <= 1e-12 * np.linalg.norm(g[f"x_{k}"])
     assert np.linalg.norm(res["z"] - g[f"z_{k}"]) <= 1e-12 * np.linalg.norm(g[f"z_{k}"])
+
+
+def test_oracle_multi_rhs_mini_columns():
+    """Config-5 family at 6000 x 600 with 8 RHS: each column is one
+    single-RHS REBK run on the fp64 upcast; the oracle reproduces two of the
+    reference's per-column ITER."""
+    from paper_2001_04179_b200.workloads import c5_arrays
+
+    g = _load("c5mini_golden.npz")
+    a32, b32, xs = c5_arrays(6000, 600, 8)
+    a = a32.astype(np.float64)
+    for c in (0, 1):
+        orc = OracleSolver(a, b32[:, c].astype(np.float64), np.r_[np.arange(0, 6000, 64), 6000],
+                           np.r_[np.arange(0, 600, 64), 600], float(g["alpha"]))
+        res = orc.run(17, 50_000, float(g["tols"][c]), xs[:, c])
+        assert res["iters"] == int(g["iters"][c])
