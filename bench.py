@@ -58,12 +58,16 @@ def workload_desc(name, wl):
     desc = {
         "c1": "C1 dense fp64 2000x500 randn, inconsistent",
         "c2": "C2 dense fp64 4000x10000 rank 2000 (U diag(s) V^T, s~U[1,10]), inconsistent",
+        "c4": "C4 sparse fp64 CSR 200000x50000, 1e7 nnz, inconsistent",
     }[name]
+    a_bytes = (wl.problem.a.nnz * 12 * 2) if wl.problem.a.is_sparse else m * n * 8
+    l2 = (f"inputs larger than L2: A = {a_bytes / 1e6:.0f} MB > 126 MB L2, no flush" if a_bytes > 126e6
+          else f"A = {a_bytes / 1e6:.0f} MB is L2-resident (no flush; L2 roofline applies)")
     return {
         "workload": f"{desc}; row/col blocks {tr}/{tc}; alpha=1/beta_max; stop ||x-x*||/||x*||<1e-6; seed 17",
         "m": m, "n": n, "row_block": tr, "col_block": tc,
         "alpha": wl.alpha, "beta_max": wl.beta_max,
-        "l2_policy": f"inputs larger than L2: A = {m * n * 8 / 1e6:.0f} MB > 126 MB L2, no flush",
+        "l2_policy": l2,
     }
 
 
@@ -283,7 +287,7 @@ def run_ours(args):
 
     # e2e through the public API from pinned host buffers, A re-uploaded each step
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not prob.a.is_sparse:
         a_pin = torch.from_numpy(prob.a.to_dense()).pin_memory()
         b_pin = torch.from_numpy(prob.b).pin_memory()
         xs_pin = torch.from_numpy(np.asarray(prob.x_star)).pin_memory()
@@ -333,12 +337,14 @@ def run_ours(args):
             "config": {**workload_desc(args.workload, wl), "parallelism": f"replicas x{ws}",
                        "iters_per_solve": per_solve_iters, "grid_ctas": int(tr.grid_ctas),
                        "kernel_path": ["rebk_dense_kernel", "rebk_dense_fast_kernel (cluster)",
-                                       "rebk_dense_fast_kernel (cluster, cooperative)"][int(tr.kernel_path)]},
+                                       "rebk_dense_fast_kernel (cluster, cooperative)",
+                                       "rebk_csr_kernel"][int(tr.kernel_path)]},
             "time_to_tol_s": ms_max / args.steps / 1e3,
             "achieved_gbps": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "rebk_dense_fast_kernel" if tr.kernel_path else "rebk_dense_kernel",
+                         "kernel": ["rebk_dense_kernel", "rebk_dense_fast_kernel", "rebk_dense_fast_kernel",
+                                    "rebk_csr_kernel"][int(tr.kernel_path)],
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_iter": bytes_per_iter,
                          "iters_per_launch": per_solve_iters, "kernel_ms_per_launch": kernel_ms},
@@ -354,13 +360,58 @@ def run_ours(args):
     return 0
 
 
+def run_ours_c5(args):
+    """Config 5 (fp32, 64 RHS): value = REBK iterations/s of the whole batch
+    (each iteration advances all 64 right-hand sides)."""
+    from paper_2001_04179_b200 import contiguous_partition, SolverConfig, StoppingRule, Matrix, compute_beta_max
+    from paper_2001_04179_b200.multirhs import DeviceMatrix32, run_multi
+    from paper_2001_04179_b200.workloads import c5_arrays
+
+    t0 = time.time()
+    a32, b32, xs = c5_arrays()
+    a64 = Matrix.from_dense(a32.astype(np.float64))
+    rp, cp = contiguous_partition(50000, 256, "row"), contiguous_partition(5000, 256, "col")
+    beta = compute_beta_max(a64, rp, cp)[2]
+    log(f"[bench] built c5 ({time.time() - t0:.1f}s), beta_max={beta:.6g}")
+    cfg = SolverConfig(algorithm="rebk", alpha=1.0 / beta, seed=17, max_iters=args.max_iters, row_partition=rp,
+                       col_partition=cp, stop=StoppingRule(tol=1.0), beta_max=beta)
+    tols = 1e-4 * np.linalg.norm(xs, axis=0)
+    dm = DeviceMatrix32(a32)
+    tr = None
+    for _ in range(max(args.warmup, 1)):
+        tr = run_multi(a32, b32, cfg, X_star=xs, tols=tols, device_matrix=dm, a64=a64)
+    log(f"[bench] c5 warm-up: K={tr.iters} per-RHS ITER {tr.iters_per_rhs.min()}..{tr.iters_per_rhs.max()} "
+        f"loop {tr.wall_time * 1e3:.1f} ms path={tr.kernel_path}")
+    its, secs = 0, 0.0
+    for _ in range(args.steps):
+        tr = run_multi(a32, b32, cfg, X_star=xs, tols=tols, device_matrix=dm, a64=a64)
+        its += tr.iters
+        secs += tr.wall_time
+    value = its / secs
+    bytes_per_iter = 4.0 * (50000 * 256 + 256 * 5000) + 2 * 4.0 * 64 * (50000 + 5000)
+    flops_per_iter = 4 * 2.0 * 256 * 64 * 50000 / 2 + 4 * 2.0 * 256 * 64 * 5000 / 2
+    line = {
+        "metric": METRIC + " (64 RHS per iteration)", "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C5 dense fp32 50000x5000, 64 RHS sharing one block sequence, blocks 256/256, "
+                               "alpha=1/beta_max, stop per column ||x-x*||/||x*||<1e-4", "K": tr.iters,
+                   "kernel_path": tr.kernel_path},
+        "time_to_tol_s": secs / args.steps,
+        "achieved_gbps": bytes_per_iter * value / 1e9,
+        "achieved_tflops": flops_per_iter * value / 1e12,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4", "c5"])
     ap.add_argument("--max-iters", type=int, default=50_000)
     ap.add_argument("--ref-iters", type=int, default=2000, help="iterations per CPU reference sample")
     ap.add_argument("--no-e2e", action="store_true")
@@ -368,6 +419,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.workload == "c5":
+        return run_ours_c5(args)
     return run_ours(args)
 
 

@@ -29,16 +29,61 @@
 
 namespace rebk {
 
+// latency-bound gathers: run 1024 threads per SM (4x the dense kernels)
+constexpr int kCsrThreads = 1024;
+constexpr int kCsrWarps = kCsrThreads / 32;
+
+// fixed-order CTA sum for kCsrThreads threads
+__device__ __forceinline__ double csr_block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < kCsrWarps; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+// in-order sum of the 32 lane values `prod` (lanes [0, cnt)) onto sum
+__device__ __forceinline__ double ordered_lane_sum(double sum, double prod, int cnt) {
+  if (cnt == 32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, prod, j));
+  } else {
+    for (int j = 0; j < cnt; ++j) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, prod, j));
+  }
+  return sum;
+}
+
 __device__ __forceinline__ double madd(double acc, double a, double b) {
   return __dadd_rn(acc, __dmul_rn(a, b));  // no FMA contraction: scipy's order and rounding
 }
 
-__global__ void __launch_bounds__(kThreads) rebk_csr_kernel(CsrParams p) {
-  __shared__ double s_red[kWarps];
+// Σ_{e in [lo,hi)} val[e] * vec[idx[e] - off] in index order, by one warp:
+// lanes form the products in parallel (the gathers overlap), every lane then
+// adds them in order, so all lanes hold the same, scipy-ordered sum.
+__device__ __forceinline__ double warp_ordered_dot(const double* __restrict__ val, const int32_t* __restrict__ idx,
+                                                   const double* vec, int off, int64_t lo, int64_t hi) {
+  const int lane = threadIdx.x & 31;
+  double sum = 0.0;
+  for (int64_t base = lo; base < hi; base += 32) {
+    const int64_t e = base + lane;
+    double prod = 0.0;
+    if (e < hi) prod = __dmul_rn(val[e], __ldcg(vec + (idx[e] - off)));
+    const int cnt = (int)((hi - base) < 32 ? (hi - base) : 32);
+    sum = ordered_lane_sum(sum, prod, cnt);
+  }
+  return sum;
+}
+
+__global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
+  __shared__ double s_red[kCsrWarps];
   __shared__ double s_bcast[2];
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int64_t gtid = (int64_t)g * kThreads + tid, gthreads = (int64_t)G * kThreads;
+  const int64_t gtid = (int64_t)g * kCsrThreads + tid, gthreads = (int64_t)G * kCsrThreads;
   Control* ctl = p.ctl;
   if (*((volatile int32_t*)&ctl->done)) return;
 
@@ -55,11 +100,11 @@ __global__ void __launch_bounds__(kThreads) rebk_csr_kernel(CsrParams p) {
 
   auto oracle_partial = [&]() {
     double acc = 0.0;
-    for (int j = xq0 + tid; j < xq1; j += kThreads) {
+    for (int j = xq0 + tid; j < xq1; j += kCsrThreads) {
       const double d = __ldcg(p.x + j) - __ldg(p.xs + j);
       acc = fma(d, d, acc);
     }
-    const double s = block_sum(acc, s_red);
+    const double s = csr_block_sum(acc, s_red);
     if (tid == 0) __stcg(p.errpart + g, s);
   };
   // ||Aᵀ(Ax - b + z)|| / scale (solvers.py:410-419) through csr/csc matvecs
@@ -73,12 +118,12 @@ __global__ void __launch_bounds__(kThreads) rebk_csr_kernel(CsrParams p) {
     }
     gsync();
     double acc2 = 0.0;
-    for (int j = xq0 + tid; j < xq1; j += kThreads) {
+    for (int j = xq0 + tid; j < xq1; j += kCsrThreads) {
       double gj = 0.0;
       for (int64_t e = p.csc_ptr[j]; e < p.csc_ptr[j + 1]; ++e) gj = madd(gj, p.csc_val[e], __ldcg(p.res + p.csc_row[e]));
       acc2 = fma(gj, gj, acc2);
     }
-    const double s = block_sum(acc2, s_red);
+    const double s = csr_block_sum(acc2, s_red);
     if (tid == 0) __stcg(p.errpart + g, s);
   };
   auto decide = [&](int64_t k) -> bool {
@@ -108,11 +153,12 @@ __global__ void __launch_bounds__(kThreads) rebk_csr_kernel(CsrParams p) {
     return conv;
   };
   // u_j = Σ_i A_ij z_i over CSC column j, for the column block of `pl`
+  // (one warp per column; products gathered in parallel, summed in order)
+  const int64_t gwarp = (int64_t)g * kCsrWarps + warp, gwarps = (int64_t)G * kCsrWarps;
   auto compute_u = [&](const Plan& pl) {
-    for (int64_t j = pl.c_lo + gtid; j < pl.c_hi; j += gthreads) {
-      double acc = 0.0;
-      for (int64_t e = p.csc_ptr[j]; e < p.csc_ptr[j + 1]; ++e) acc = madd(acc, p.csc_val[e], __ldcg(p.z + p.csc_row[e]));
-      __stcg(p.u + (j - pl.c_lo), acc);
+    for (int64_t j = pl.c_lo + gwarp; j < pl.c_hi; j += gwarps) {
+      const double acc = warp_ordered_dot(p.csc_val, p.csc_row, p.z, 0, p.csc_ptr[j], p.csc_ptr[j + 1]);
+      if (lane == 0) __stcg(p.u + (j - pl.c_lo), acc);
     }
   };
 
@@ -149,7 +195,7 @@ __global__ void __launch_bounds__(kThreads) rebk_csr_kernel(CsrParams p) {
     if (p.extended) {
       const int64_t s0 = p.cseg_cta[(int64_t)pl.cb * (G + 1) + g];
       const int64_t s1 = p.cseg_cta[(int64_t)pl.cb * (G + 1) + g + 1];
-      for (int64_t sg = s0 + tid; sg < s1; sg += kThreads) {
+      for (int64_t sg = s0 + tid; sg < s1; sg += kCsrThreads) {
         const int i = p.cseg_row[sg];
         if (i >= pl.r_lo && i < pl.r_hi) continue;  // done by the row-sweep threads below
         double acc = 0.0;
@@ -158,28 +204,40 @@ __global__ void __launch_bounds__(kThreads) rebk_csr_kernel(CsrParams p) {
         __stcg(p.z + i, __dsub_rn(__ldcg(p.z + i), __dmul_rn(cs, acc)));
       }
     }
-    for (int64_t i = pl.r_lo + gtid; i < pl.r_hi; i += gthreads) {
+    // rows of I: one warp per row; r_i and the row's own z update
+    for (int64_t i = pl.r_lo + gwarp; i < pl.r_hi; i += gwarps) {
       double ax = 0.0, au = 0.0;
-      for (int64_t e = p.csr_ptr[i]; e < p.csr_ptr[i + 1]; ++e) {
-        const int c = p.csr_col[e];
-        const double a = p.csr_val[e];
-        ax = madd(ax, a, __ldcg(p.x + c));
-        if (p.extended && c >= pl.c_lo && c < pl.c_hi) au = madd(au, a, __ldcg(p.u + (c - pl.c_lo)));
+      const int64_t lo = p.csr_ptr[i], hi = p.csr_ptr[i + 1];
+      for (int64_t base = lo; base < hi; base += 32) {
+        const int64_t e = base + lane;
+        double px = 0.0, pu = 0.0;
+        if (e < hi) {
+          const int c = p.csr_col[e];
+          const double a = p.csr_val[e];
+          px = __dmul_rn(a, __ldcg(p.x + c));
+          if (p.extended && c >= pl.c_lo && c < pl.c_hi) pu = __dmul_rn(a, __ldcg(p.u + (c - pl.c_lo)));
+        }
+        const int cnt = (int)((hi - base) < 32 ? (hi - base) : 32);
+        ax = ordered_lane_sum(ax, px, cnt);
+        // entries outside J contribute +0.0, an exact no-op on the running sum
+        if (p.extended) au = ordered_lane_sum(au, pu, cnt);
       }
-      double rv = __dsub_rn(ax, __ldg(p.b + i));
-      if (p.extended) {
-        const double zn = __dsub_rn(__ldcg(p.z + i), __dmul_rn(cs, au));
-        __stcg(p.z + i, zn);
-        rv = __dadd_rn(rv, zn);
+      if (lane == 0) {
+        double rv = __dsub_rn(ax, __ldg(p.b + i));
+        if (p.extended) {
+          const double zn = __dsub_rn(__ldcg(p.z + i), __dmul_rn(cs, au));
+          __stcg(p.z + i, zn);
+          rv = __dadd_rn(rv, zn);
+        }
+        __stcg(p.r + (i - pl.r_lo), rv);
       }
-      __stcg(p.r + (i - pl.r_lo), rv);
     }
     gsync();
     // ---- Q(k)
     {
       const int64_t s0 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g];
       const int64_t s1 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g + 1];
-      for (int64_t sg = s0 + tid; sg < s1; sg += kThreads) {
+      for (int64_t sg = s0 + tid; sg < s1; sg += kCsrThreads) {
         const int j = p.rseg_col[sg];
         double acc = 0.0;
         for (int64_t e = p.rseg_lo[sg]; e < p.rseg_hi[sg]; ++e)
@@ -233,11 +291,11 @@ __global__ void __launch_bounds__(kThreads) rebk_csr_kernel(CsrParams p) {
 cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream) {
   CsrParams pc = p;
   void* args[] = {&pc};
-  return cudaLaunchCooperativeKernel((const void*)rebk_csr_kernel, dim3(G), dim3(kThreads), args, 0, stream);
+  return cudaLaunchCooperativeKernel((const void*)rebk_csr_kernel, dim3(G), dim3(kCsrThreads), args, 0, stream);
 }
 
 cudaError_t csr_kernel_occupancy(int* blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, rebk_csr_kernel, kThreads, 0);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, rebk_csr_kernel, kCsrThreads, 0);
 }
 
 }  // namespace rebk

@@ -7,11 +7,11 @@
 //   Z -= s_J A_J U
 //   Rr = A_I X - B_I + Z_I      (|I| x R)
 //   X -= s_I A_Iᵀ Rr
-// Round 1 runs them through cuBLAS with CUBLAS_FP32_EMULATED_BF16X9_MATH
-// (FP32 results from BF16 tensor-core passes; single-pass TF32 misses the
-// 1e-4 tolerance, SURVEY hard part 6), enqueued in chunks of 64 iterations
-// (the block sequence of a chunk is sampled on the device first; the host
-// only needs it to address the GEMMs).  The per-column stopping rule (each RHS records the first check
+// Round 1 runs them through cuBLAS FP32 GEMMs (optionally the BF16x9 FP32
+// emulation on tensor cores; single-pass TF32 misses the 1e-4 tolerance,
+// SURVEY hard part 6), split-K for the two reductions, captured as one CUDA graph per chunk
+// of 64 iterations (the block sequence of a chunk is sampled on the device
+// first; the host only needs it to address the GEMMs).  The per-column stopping rule (each RHS records the first check
 // with ||X_c - X*_c|| <= tol_c; the run ends when every column has crossed)
 // runs on the device; the final state is the one at that iteration, obtained
 // by restoring the chunk's checkpoint and replaying (the sequence and the
@@ -48,6 +48,8 @@ struct CublasApi {
   int (*set_workspace)(cublasHandle_t, void*, size_t) = nullptr;
   int (*sgemm)(cublasHandle_t, int, int, int, int, int, const float*, const float*, int, const float*, int,
                const float*, float*, int) = nullptr;
+  int (*sgemm_sb)(cublasHandle_t, int, int, int, int, int, const float*, const float*, int, long long, const float*,
+                  int, long long, const float*, float*, int, long long, int) = nullptr;
 };
 
 static CublasApi& cublas() {
@@ -69,7 +71,11 @@ static CublasApi& cublas() {
   api.set_workspace = (int (*)(cublasHandle_t, void*, size_t))dlsym(h, "cublasSetWorkspace_v2");
   api.sgemm = (int (*)(cublasHandle_t, int, int, int, int, int, const float*, const float*, int, const float*, int,
                        const float*, float*, int))dlsym(h, "cublasSgemm_v2");
-  api.ok = api.create && api.destroy && api.set_stream && api.set_math && api.set_workspace && api.sgemm;
+  api.sgemm_sb = (int (*)(cublasHandle_t, int, int, int, int, int, const float*, const float*, int, long long,
+                          const float*, int, long long, const float*, float*, int, long long, int))
+      dlsym(h, "cublasSgemmStridedBatched");
+  api.ok = api.create && api.destroy && api.set_stream && api.set_math && api.set_workspace && api.sgemm &&
+           api.sgemm_sb;
   return api;
 }
 
@@ -81,32 +87,55 @@ __global__ void mrhs_init_r(const float* __restrict__ ZI, const float* __restric
   if (t < count) Rr[t] = (ZI ? ZI[t] : 0.0f) - BI[t];
 }
 
-// per-column ||X_c - X*_c||^2 -> first crossing bookkeeping.  One CTA per
-// column block of 32 columns; fixed-order reduction.
-__global__ void mrhs_check(const float* __restrict__ X, const float* __restrict__ Xs, int64_t n, int R,
-                           const double* __restrict__ tol, int64_t k, int64_t* iters, double* errs,
-                           double* errs_at, int32_t* n_done) {
-  __shared__ double part[8][33];
+// out[e] = init[e] + Σ_{b<nb} part[b][e]  (fixed order: split-K reduction)
+__global__ void mrhs_reduce_parts(const float* __restrict__ part, int nb, int64_t len, const float* __restrict__ init,
+                                  float* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= len) return;
+  float acc = init ? init[e] : 0.0f;
+#pragma unroll 8
+  for (int b = 0; b < nb; ++b) acc += part[(int64_t)b * len + e];
+  out[e] = acc;
+}
+
+// per-column ||X_c - X*_c||^2, two deterministic stages: partial sums over
+// row chunks of 256 rows (grid: column groups of 32 x row chunks), then one
+// thread per column sums the chunks in order and does the crossing logic.
+constexpr int kCheckRows = 256;
+__global__ void mrhs_check_part(const float* __restrict__ X, const float* __restrict__ Xs, int64_t n, int R,
+                                double* __restrict__ part) {
+  __shared__ double sp[8][33];
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int w = threadIdx.x >> 5;  // 8 warps split the rows
+  const int w = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.y * kCheckRows;
+  const int64_t r1 = r0 + kCheckRows < n ? r0 + kCheckRows : n;
   double acc = 0.0;
   if (c < R)
-    for (int64_t i = w; i < n; i += 8) {
+    for (int64_t i = r0 + w; i < r1; i += 8) {
       const double d = (double)X[i * R + c] - (double)Xs[i * R + c];
       acc = fma(d, d, acc);
     }
-  part[w][threadIdx.x & 31] = acc;
+  sp[w][threadIdx.x & 31] = acc;
   __syncthreads();
   if (w == 0 && c < R) {
     double s = 0.0;
-    for (int q = 0; q < 8; ++q) s += part[q][threadIdx.x & 31];
-    const double e = sqrt(s);
-    errs[c] = e;
-    if (iters[c] < 0 && e <= tol[c]) {
-      iters[c] = k;
-      errs_at[c] = e;
-      atomicAdd(n_done, 1);
-    }
+    for (int q = 0; q < 8; ++q) s += sp[q][threadIdx.x & 31];
+    part[(int64_t)blockIdx.y * R + c] = s;
+  }
+}
+
+__global__ void mrhs_check_final(const double* __restrict__ part, int nchunks, int R, const double* __restrict__ tol,
+                                 int64_t k, int64_t* iters, double* errs, double* errs_at, int32_t* n_done) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= R) return;
+  double s = 0.0;
+  for (int q = 0; q < nchunks; ++q) s += part[(int64_t)q * R + c];
+  const double e = sqrt(s);
+  errs[c] = e;
+  if (iters[c] < 0 && e <= tol[c]) {
+    iters[c] = k;
+    errs_at[c] = e;
+    atomicAdd(n_done, 1);
   }
 }
 
@@ -129,11 +158,14 @@ __global__ void mrhs_check(const float* __restrict__ X, const float* __restrict_
     }                                                                  \
   } while (0)
 
+// Default FP32 (SIMT) GEMMs: measured faster end to end than the BF16x9
+// emulation here (the emulation adds an inf/NaN scan and patch kernels per
+// GEMM, profiles/r01_c5_launches.txt).  REBK_MRHS_MATH=bf16x9 selects it.
 static int mrhs_math_mode() {
   const char* s = getenv("REBK_MRHS_MATH");
-  if (s && !strcmp(s, "pedantic")) return CUBLAS_PEDANTIC_MATH;
+  if (s && !strcmp(s, "bf16x9")) return CUBLAS_FP32_EMULATED_BF16X9_MATH;
   if (s && !strcmp(s, "default")) return CUBLAS_DEFAULT_MATH;
-  return CUBLAS_FP32_EMULATED_BF16X9_MATH;
+  return CUBLAS_PEDANTIC_MATH;
 }
 
 int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SampleParams* unused, int64_t* iters_out,
@@ -186,6 +218,23 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
   MR_TRY(cudaMallocAsync((void**)&d_iters, sizeof(int64_t) * R, stream));
   MR_TRY(cudaMallocAsync((void**)&d_ndone, sizeof(int32_t), stream));
   MR_TRY(cudaMallocAsync((void**)&d_plan, sizeof(Plan) * CH, stream));
+  const int nchk = (int)((n + kCheckRows - 1) / kCheckRows);
+  double* d_cpart;
+  MR_TRY(cudaMallocAsync((void**)&d_cpart, sizeof(double) * nchk * R, stream));
+  auto launch_check = [&](int64_t k) -> cudaError_t {
+    mrhs_check_part<<<dim3((R + 31) / 32, nchk), 256, 0, stream>>>(w.X, w.Xs, n, R, d_cpart);
+    mrhs_check_final<<<(R + 127) / 128, 128, 0, stream>>>(d_cpart, nchk, R, d_tol, k, d_iters, d_errs, d_errs_at,
+                                                           d_ndone);
+    return cudaGetLastError();
+  };
+  // split-K: the two reductions (over m for U, over n for Rr) have tiny
+  // outputs (R x |J|, R x |I|), so one GEMM would occupy a handful of SMs;
+  // batch them over K chunks and sum the partials in a fixed order.
+  const int64_t kc_m = 2048, kc_n = 512;
+  const int64_t nb_m = std::max<int64_t>(1, m / kc_m), nb_n = std::max<int64_t>(1, n / kc_n);
+  float* P;
+  const int64_t plen = std::max<int64_t>((int64_t)nJmax * R * (nb_m + 1), (int64_t)nImax * R * (nb_n + 1));
+  MR_TRY(cudaMallocAsync((void**)&P, sizeof(float) * plen, stream));
   std::vector<double> tol(R);
   for (int c = 0; c < R; ++c) tol[c] = w.tols ? w.tols[c] : cfg->tol;
   MR_TRY(cudaMemcpyAsync(d_tol, tol.data(), sizeof(double) * R, cudaMemcpyHostToDevice, stream));
@@ -198,7 +247,17 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
     const float one = 1.0f, zero = 0.0f;
     if (w.extended) {
       const float mcs = (float)(-pl.c_scale);
-      MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, R, nJ, (int)m, &one, w.Z, R, w.A + pl.c_lo, (int)lda, &zero, U, R));
+      // U = Σ_chunks Z_chunkᵀ-rows x A_J chunk (split over m), then the z update
+      const int64_t ulen = (int64_t)nJ * R;
+      MB_TRY(cb.sgemm_sb(h, CUBLAS_OP_N, CUBLAS_OP_T, R, nJ, (int)kc_m, &one, w.Z, R, kc_m * R, w.A + pl.c_lo,
+                         (int)lda, kc_m * lda, &zero, P, R, ulen, (int)nb_m));
+      const int64_t rem = m - nb_m * kc_m;
+      if (rem > 0)
+        MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, R, nJ, (int)rem, &one, w.Z + nb_m * kc_m * R, R,
+                        w.A + pl.c_lo + nb_m * kc_m * lda, (int)lda, &zero, P + nb_m * ulen, R));
+      mrhs_reduce_parts<<<(unsigned)((ulen + 255) / 256), 256, 0, stream>>>(P, (int)(nb_m + (rem > 0)), ulen, nullptr,
+                                                                            U);
+      MR_TRY(cudaGetLastError());
       MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, R, (int)m, nJ, &mcs, U, R, w.A + pl.c_lo, (int)lda, &one, w.Z, R));
     }
     const int64_t cnt = (int64_t)nI * R;
@@ -207,12 +266,19 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
     MR_TRY(cudaGetLastError());
     const float* AI = w.A + (int64_t)pl.r_lo * lda;
     const float mrs = (float)(-pl.r_scale);
-    MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, R, nI, (int)n, &one, w.X, R, AI, (int)lda, &one, Rr, R));
-    MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, R, (int)n, nI, &mrs, Rr, R, AI, (int)lda, &one, w.X, R));
-    if (do_check) {
-      mrhs_check<<<(R + 31) / 32, 256, 0, stream>>>(w.X, w.Xs, n, R, d_tol, k, d_iters, d_errs, d_errs_at, d_ndone);
+    {
+      // Rr += Σ_chunks X_chunk x A_I chunk (split over n)
+      MB_TRY(cb.sgemm_sb(h, CUBLAS_OP_N, CUBLAS_OP_N, R, nI, (int)kc_n, &one, w.X, R, kc_n * R, AI, (int)lda, kc_n,
+                         &zero, P, R, cnt, (int)nb_n));
+      const int64_t rem = n - nb_n * kc_n;
+      if (rem > 0)
+        MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, R, nI, (int)rem, &one, w.X + nb_n * kc_n * R, R,
+                        AI + nb_n * kc_n, (int)lda, &zero, P + nb_n * cnt, R));
+      mrhs_reduce_parts<<<(unsigned)((cnt + 255) / 256), 256, 0, stream>>>(P, (int)(nb_n + (rem > 0)), cnt, Rr, Rr);
       MR_TRY(cudaGetLastError());
     }
+    MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, R, (int)n, nI, &mrs, Rr, R, AI, (int)lda, &one, w.X, R));
+    if (do_check) MR_TRY(launch_check(k));
     return 0;
   };
 
@@ -223,7 +289,7 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
   int64_t K = cfg->max_iters;
   bool all_done = false;
   if (checking) {
-    mrhs_check<<<(R + 31) / 32, 256, 0, stream>>>(w.X, w.Xs, n, R, d_tol, 0, d_iters, d_errs, d_errs_at, d_ndone);
+    MR_TRY(launch_check(0));
     int32_t nd = 0;
     MR_TRY(cudaMemcpyAsync(&nd, d_ndone, sizeof nd, cudaMemcpyDeviceToHost, stream));
     MR_TRY(cudaStreamSynchronize(stream));
@@ -243,10 +309,30 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
       MR_TRY(cudaMemcpyAsync(Xsnap, w.X, sizeof(float) * n * R, cudaMemcpyDeviceToDevice, stream));
       if (w.extended) MR_TRY(cudaMemcpyAsync(Zsnap, w.Z, sizeof(float) * m * R, cudaMemcpyDeviceToDevice, stream));
     }
+    // one CUDA graph per chunk: the ~8 launches of an iteration cost more
+    // host time than the GPU spends on them
+    const bool use_graph = !getenv("REBK_MRHS_NO_GRAPH");
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    if (use_graph) MR_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     for (int64_t q = 0; q < cnt; ++q) {
       const int64_t k = k0 + q;
       int rc = enqueue_iter(hplan[q], k, checking && (k % cfg->check_stride == 0 || k == cfg->max_iters));
-      if (rc) return rc;
+      if (rc) {
+        if (use_graph) {
+          cudaStreamEndCapture(stream, &graph);
+          if (graph) cudaGraphDestroy(graph);
+        }
+        return rc;
+      }
+    }
+    if (use_graph) {
+      MR_TRY(cudaStreamEndCapture(stream, &graph));
+      MR_TRY(cudaGraphInstantiate(&gexec, graph, 0));
+      MR_TRY(cudaGraphLaunch(gexec, stream));
+      MR_TRY(cudaStreamSynchronize(stream));
+      cudaGraphExecDestroy(gexec);
+      cudaGraphDestroy(graph);
     }
     if (checking) {
       int32_t nd = 0;
@@ -288,6 +374,8 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
   cudaFreeAsync(d_iters, stream);
   cudaFreeAsync(d_ndone, stream);
   cudaFreeAsync(d_plan, stream);
+  cudaFreeAsync(P, stream);
+  cudaFreeAsync(d_cpart, stream);
   cudaFreeAsync(ws, stream);
   cudaStreamSynchronize(stream);
   return 0;
