@@ -158,6 +158,22 @@ int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float*
                   const float* Z0, const float* Xstar, const double* tols, float* X_out, float* Z_out,
                   int64_t* iters_out, double* errs_out, rebk_trace* trace);
 
+/* ---- row-sharded multi-GPU pieces (BASELINE config 3).  ctx
+ * holds this rank's rows of A; all buffers are device buffers on `stream`.
+ * Between colstep and zupdate the caller allreduces u (|J| doubles), between
+ * rowstep and xupdate it allreduces dx (n doubles), on its communicator.
+ * Together they are one step_rebk (solvers.py:324-337) on the sharded A.
+ * Fixed-order reductions; the ctx's scratch makes these calls non-reentrant
+ * per ctx. */
+int rebk_shard_colstep(rebk_ctx* ctx, int64_t c_lo, int64_t c_hi, const double* z_dev, double* u_dev,
+                       void* stream);
+int rebk_shard_zupdate(rebk_ctx* ctx, int64_t c_lo, int64_t c_hi, double scale, const double* u_dev,
+                       double* z_dev, void* stream);
+int rebk_shard_rowstep(rebk_ctx* ctx, const int64_t* rows_dev, int64_t nrows, const double* x_dev,
+                       const double* b_dev, const double* z_dev, double* dx_dev, void* stream);
+int rebk_shard_xupdate(int64_t n, double scale, const double* dx_dev, double* x_dev, void* stream);
+int rebk_shard_err2(int64_t n, const double* x_dev, const double* xs_dev, double* out_dev, void* stream);
+
 /* ---- sampler (sampling.py:23-45 Rng, :137-145 WeightedSampler.sample) -----
  * Device sampling of the (col, row) block-index pairs of iterations
  * [k0, k0+count) (k is 1-based), written to picks_out[2*count] (host). */

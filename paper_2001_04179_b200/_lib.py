@@ -91,6 +91,11 @@ SIGNATURES = {
     "rebk_run": (c_int, [c_void_p, POINTER(RebkCfg), _P_D, _P_D, _P_D, _P_D, _P_D, _P_D, POINTER(RebkTrace)]),
     "rebk_run_device": (c_int, [c_void_p, POINTER(RebkCfg), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                 POINTER(RebkTrace)]),
+    "rebk_shard_colstep": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
+    "rebk_shard_zupdate": (c_int, [c_void_p, c_int64, c_int64, c_double, c_void_p, c_void_p, c_void_p]),
+    "rebk_shard_rowstep": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "rebk_shard_xupdate": (c_int, [c_int64, c_double, c_void_p, c_void_p, c_void_p]),
+    "rebk_shard_err2": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "rebk_sample_sequence": (c_int, [POINTER(RebkCfg), c_int64, c_int64, POINTER(c_int32)]),
     "rebk_block_frobenius_sq": (c_int, [c_void_p, c_int, c_int64, _P_I64, _P_D]),
     "rebk_philox_key": (c_int, [POINTER(c_uint32), c_int64, POINTER(c_uint32), c_int64, POINTER(c_uint64)]),

@@ -47,6 +47,8 @@ struct rebk_ctx {
   std::vector<int32_t> h_csr_col, h_csc_row;
   std::vector<CsrSegPlan*> seg_cache;
   float* A32 = nullptr;  // dense fp32 A (multi-RHS contexts, kind 2)
+  double* shard_scratch = nullptr;  // rebk_shard_* partials (not reentrant per ctx)
+  size_t shard_scratch_len = 0;
 };
 
 namespace {
@@ -1132,8 +1134,71 @@ int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float*
   return rc;
 }
 
+static int shard_scratch(rebk_ctx* ctx, size_t len, double** out) {
+  if (ctx->shard_scratch_len < len) {
+    cudaFree(ctx->shard_scratch);
+    ctx->shard_scratch = nullptr;
+    ctx->shard_scratch_len = 0;
+    CUDA_TRY(cudaMalloc(&ctx->shard_scratch, len * sizeof(double)));
+    ctx->shard_scratch_len = len;
+  }
+  *out = ctx->shard_scratch;
+  return REBK_OK;
+}
+
+int rebk_shard_colstep(rebk_ctx* ctx, int64_t c_lo, int64_t c_hi, const double* z_dev, double* u_dev, void* stream) {
+  if (!ctx || ctx->kind != 0 || !z_dev || !u_dev || c_lo < 0 || c_hi > ctx->n || c_hi <= c_lo)
+    return fail(REBK_EINVAL, "rebk_shard_colstep: bad argument");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  double* scr = nullptr;
+  const int64_t nparts = (ctx->m + 63) / 64;
+  int rc = shard_scratch(ctx, (size_t)nparts * (size_t)(c_hi - c_lo) + ctx->m, &scr);
+  if (rc) return rc;
+  CUDA_TRY(shard_colstep(ctx->A, ctx->lda, ctx->m, c_lo, (int)(c_hi - c_lo), z_dev, u_dev, scr, (cudaStream_t)stream));
+  return REBK_OK;
+}
+
+int rebk_shard_zupdate(rebk_ctx* ctx, int64_t c_lo, int64_t c_hi, double scale, const double* u_dev, double* z_dev,
+                       void* stream) {
+  if (!ctx || ctx->kind != 0 || !z_dev || !u_dev || c_lo < 0 || c_hi > ctx->n || c_hi <= c_lo)
+    return fail(REBK_EINVAL, "rebk_shard_zupdate: bad argument");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(shard_zupd(ctx->A, ctx->lda, ctx->m, c_lo, (int)(c_hi - c_lo), scale, u_dev, z_dev, (cudaStream_t)stream));
+  return REBK_OK;
+}
+
+int rebk_shard_rowstep(rebk_ctx* ctx, const int64_t* rows_dev, int64_t nrows, const double* x_dev, const double* b_dev,
+                       const double* z_dev, double* dx_dev, void* stream) {
+  if (!ctx || ctx->kind != 0 || (nrows > 0 && !rows_dev) || !x_dev || !b_dev || !dx_dev || nrows < 0)
+    return fail(REBK_EINVAL, "rebk_shard_rowstep: bad argument");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  double* scr = nullptr;
+  const int64_t nparts = (ctx->m + 63) / 64;
+  int rc = shard_scratch(ctx, std::max<size_t>((size_t)nrows, 1) + (size_t)nparts, &scr);
+  if (rc) return rc;
+  CUDA_TRY(shard_rowstep(ctx->A, ctx->lda, ctx->n, rows_dev, nrows, x_dev, b_dev, z_dev, scr, dx_dev,
+                         (cudaStream_t)stream));
+  return REBK_OK;
+}
+
+int rebk_shard_xupdate(int64_t n, double scale, const double* dx_dev, double* x_dev, void* stream) {
+  if (n < 1 || !dx_dev || !x_dev) return fail(REBK_EINVAL, "rebk_shard_xupdate: bad argument");
+  CUDA_TRY(shard_xupd(n, scale, dx_dev, x_dev, (cudaStream_t)stream));
+  return REBK_OK;
+}
+
+int rebk_shard_err2(int64_t n, const double* x_dev, const double* xs_dev, double* out_dev, void* stream) {
+  if (n < 1 || !x_dev || !xs_dev || !out_dev) return fail(REBK_EINVAL, "rebk_shard_err2: bad argument");
+  CUDA_TRY(shard_err(n, x_dev, xs_dev, out_dev, (cudaStream_t)stream));
+  return REBK_OK;
+}
+
 int rebk_ctx_destroy(rebk_ctx* ctx) {
   if (!ctx) return REBK_OK;
+  if (ctx->shard_scratch) {
+    cudaSetDevice(ctx->device);
+    cudaFree(ctx->shard_scratch);
+  }
   if (ctx->A32) {
     cudaSetDevice(ctx->device);
     cudaFree(ctx->A32);

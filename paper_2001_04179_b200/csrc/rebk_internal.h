@@ -183,6 +183,15 @@ struct MrhsRun {
 int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SampleParams* unused, int64_t* iters_out,
              double* errs_out, double* loop_ms, int64_t* k_final, char* errbuf, size_t errlen, cudaStream_t stream,
              int* math_used);
+// row-sharded multi-GPU pieces (rebk_shard.cu)
+cudaError_t shard_colstep(const double* A, int64_t lda, int64_t m, int64_t c_lo, int nJ, const double* z, double* u,
+                          double* scratch, cudaStream_t st);
+cudaError_t shard_zupd(const double* A, int64_t lda, int64_t m, int64_t c_lo, int nJ, double s, const double* u,
+                       double* z, cudaStream_t st);
+cudaError_t shard_rowstep(const double* A, int64_t lda, int64_t n, const int64_t* rows, int64_t nrows, const double* x,
+                          const double* b, const double* z, double* r_scratch, double* dx, cudaStream_t st);
+cudaError_t shard_xupd(int64_t n, double s, const double* dx, double* x, cudaStream_t st);
+cudaError_t shard_err(int64_t n, const double* x, const double* xs, double* out, cudaStream_t st);
 cudaError_t launch_block_norms(const double* A, int64_t lda, int64_t m, int64_t n, int axis,
                                int64_t nb, const int64_t* ptr_dev, double* out_dev,
                                cudaStream_t stream);

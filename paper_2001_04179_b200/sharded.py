@@ -1,0 +1,217 @@
+"""Row-sharded REBK over P ranks (BASELINE config 3).
+
+Layout: every row block I_b is split across all ranks — local row q of
+I_b lives on rank floor(q * P / |I_b|) — so the row step is balanced and no
+rank ever needs another rank's rows.  z and b follow the rows; x is
+replicated.  One iteration (step_rebk, solvers.py:324-337):
+
+    u_p  = A_p[:, J]ᵀ z_p          -> allreduce(u)   (|J| doubles)
+    z_p -= s_J A_p[:, J] u
+    dx_p = A_p[I_p, :]ᵀ (A_p[I_p, :] x - b_p + z_p)
+                                   -> allreduce(dx)  (n doubles)
+    x   -= s_I dx
+
+The stop check needs no communication (x is replicated, every rank computes
+the same ||x - x*||).  The block sequence is shared: every rank expands the
+same Philox stream.
+
+The per-rank arithmetic is a backend: :class:`CudaShardBackend` (librebk's
+``rebk_shard_*`` kernels, device buffers, allreduce over NCCL via
+torch.distributed).  Tests drive the same loop with a CPU restatement under
+gloo (oracle/shard_oracle.py) to check the sharding logic.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+def owned_rows(row_ptr: np.ndarray, nranks: int, rank: int) -> tuple[np.ndarray, np.ndarray]:
+    """Global rows owned by `rank` (sorted) and, per row block, the [lo, hi)
+    range of those rows in the rank's local ordering."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    rows, ranges = [], np.zeros((row_ptr.size - 1, 2), dtype=np.int64)
+    pos = 0
+    for b in range(row_ptr.size - 1):
+        lo, nb = int(row_ptr[b]), int(row_ptr[b + 1] - row_ptr[b])
+        q0 = -(-rank * nb // nranks)          # ceil(rank * nb / P)
+        q1 = -(-(rank + 1) * nb // nranks)
+        rows.append(np.arange(lo + q0, lo + q1, dtype=np.int64))
+        ranges[b] = (pos, pos + (q1 - q0))
+        pos += q1 - q0
+    return np.concatenate(rows) if rows else np.zeros(0, dtype=np.int64), ranges
+
+
+@dataclass
+class ShardPlan:
+    """Everything every rank shares: partitions, scales, the pick sequence."""
+
+    row_ptr: np.ndarray
+    col_ptr: np.ndarray | None
+    row_scale: np.ndarray
+    col_scale: np.ndarray | None
+    picks: np.ndarray  # (max_iters, 2): column block (or -1), row block
+
+
+def plan_from_context(ctx, max_iters: int) -> ShardPlan:
+    """Shared plan from a SolverContext built on the full matrix (the
+    reference's sampler arrays), with the pick sequence expanded on the
+    device from the run's Philox stream."""
+    cfg = ctx.make_cfg(stop_mode="max_iters_only", tol=1.0, stride=1, max_iters=max_iters,
+                       key=_lib.philox_key(ctx.config.seed))
+    picks = np.empty((max_iters, 2), dtype=np.int32)
+    if max_iters:
+        rc = _lib.load().rebk_sample_sequence(ctypes.byref(cfg), 1, max_iters,
+                                              picks.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+        _lib.check(rc, "rebk_sample_sequence")
+    return ShardPlan(ctx._row_ptr, ctx._col_ptr if ctx.extended else None, ctx._row_scale,
+                     ctx._col_scale if ctx.extended else None, picks)
+
+
+class CudaShardBackend:
+    """This rank's rows of A on its GPU; all state in device memory."""
+
+    def __init__(self, a_local: np.ndarray, b_local: np.ndarray, x_star: np.ndarray | None, extended: bool,
+                 device: int = 0):
+        import torch
+
+        from .matrix import DeviceMatrix
+
+        self.torch = torch
+        self.dev = torch.device("cuda", device)
+        self.lib = _lib.load()
+        self.m_local, self.n = a_local.shape
+        self.extended = extended
+        # an empty shard still needs a valid matrix: keep one zero row
+        a = a_local if self.m_local else np.zeros((1, self.n))
+        self.dm = DeviceMatrix(a, device)
+        t = lambda v: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64)).to(self.dev)
+        self.b = t(b_local if self.m_local else np.zeros(1))
+        self.z = self.b.clone() if extended else None
+        self.x = torch.zeros(self.n, dtype=torch.float64, device=self.dev)
+        self.xs = None if x_star is None else t(x_star)
+        self.dx = torch.empty(self.n, dtype=torch.float64, device=self.dev)
+        self.err_buf = torch.empty(1, dtype=torch.float64, device=self.dev)
+        self.rows_cache: dict = {}
+
+    def _stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def colstep(self, c_lo: int, c_hi: int):
+        u = self.torch.empty(c_hi - c_lo, dtype=self.torch.float64, device=self.dev)
+        if self.m_local:
+            _lib.check(self.lib.rebk_shard_colstep(self.dm.handle, c_lo, c_hi, ctypes.c_void_p(self.z.data_ptr()),
+                                                   ctypes.c_void_p(u.data_ptr()), self._stream()), "colstep")
+        else:
+            u.zero_()
+        return u
+
+    def zupdate(self, c_lo: int, c_hi: int, scale: float, u):
+        if self.m_local:
+            _lib.check(self.lib.rebk_shard_zupdate(self.dm.handle, c_lo, c_hi, scale, ctypes.c_void_p(u.data_ptr()),
+                                                   ctypes.c_void_p(self.z.data_ptr()), self._stream()), "zupdate")
+
+    def rowstep(self, lo: int, hi: int):
+        key = (lo, hi)
+        rows = self.rows_cache.get(key)
+        if rows is None:
+            rows = self.torch.arange(lo, hi, dtype=self.torch.int64, device=self.dev)
+            self.rows_cache[key] = rows
+        zp = ctypes.c_void_p(self.z.data_ptr()) if self.extended else None
+        _lib.check(self.lib.rebk_shard_rowstep(self.dm.handle, ctypes.c_void_p(rows.data_ptr()), hi - lo,
+                                               ctypes.c_void_p(self.x.data_ptr()), ctypes.c_void_p(self.b.data_ptr()),
+                                               zp, ctypes.c_void_p(self.dx.data_ptr()), self._stream()), "rowstep")
+        return self.dx
+
+    def xupdate(self, scale: float, dx):
+        _lib.check(self.lib.rebk_shard_xupdate(self.n, scale, ctypes.c_void_p(dx.data_ptr()),
+                                               ctypes.c_void_p(self.x.data_ptr()), self._stream()), "xupdate")
+
+    def err(self) -> float:
+        _lib.check(self.lib.rebk_shard_err2(self.n, ctypes.c_void_p(self.x.data_ptr()),
+                                            ctypes.c_void_p(self.xs.data_ptr()), ctypes.c_void_p(self.err_buf.data_ptr()),
+                                            self._stream()), "err2")
+        return float(np.sqrt(self.err_buf.item()))
+
+    def state(self):
+        z = None if self.z is None else self.z.cpu().numpy()[: self.m_local]
+        return self.x.cpu().numpy(), z
+
+
+def run_sharded(backend, plan: ShardPlan, ranges: np.ndarray, max_iters: int, tol: float, stride: int = 1,
+                mode: str = "oracle_error", allreduce=None) -> dict:
+    """The run() loop (solvers.py:425-474) on one rank; `allreduce(t)` sums a
+    vector over all ranks in place (identity for a single rank)."""
+    allreduce = allreduce or (lambda t: None)
+    checking = mode == "oracle_error"
+    final, converged, iters = None, False, 0
+    if checking:
+        final = backend.err()
+        converged = final <= tol
+    if not converged:
+        for k in range(1, max_iters + 1):
+            j, i = int(plan.picks[k - 1, 0]), int(plan.picks[k - 1, 1])
+            if backend.extended:
+                c_lo, c_hi = int(plan.col_ptr[j]), int(plan.col_ptr[j + 1])
+                u = backend.colstep(c_lo, c_hi)
+                allreduce(u)
+                backend.zupdate(c_lo, c_hi, float(plan.col_scale[j]), u)
+            lo, hi = int(ranges[i, 0]), int(ranges[i, 1])
+            dx = backend.rowstep(lo, hi)
+            allreduce(dx)
+            backend.xupdate(float(plan.row_scale[i]), dx)
+            if checking and k % stride == 0:
+                final = backend.err()
+                if final <= tol:
+                    converged, iters = True, k
+                    break
+        else:
+            iters = max_iters
+            if checking and max_iters % stride != 0:
+                final = backend.err()
+                converged = final <= tol
+    x, z = backend.state()
+    return dict(iters=iters, converged=converged, final_error=final, x=x, z_local=z)
+
+
+def run_virtual_ranks(backends: list, plan: ShardPlan, ranges: list, max_iters: int, tol: float,
+                      stride: int = 1) -> dict:
+    """The sharded iteration for several ranks driven in lockstep by one
+    process (one GPU can host them; the "allreduce" is a sum of the ranks'
+    device vectors in rank order).  Used to exercise the multi-rank kernels
+    where only one GPU is available."""
+    first = backends[0]
+    checking = True
+    final = first.err()
+    converged, iters = final <= tol, 0
+    if not converged:
+        for k in range(1, max_iters + 1):
+            j, i = int(plan.picks[k - 1, 0]), int(plan.picks[k - 1, 1])
+            if first.extended:
+                c_lo, c_hi = int(plan.col_ptr[j]), int(plan.col_ptr[j + 1])
+                us = [be.colstep(c_lo, c_hi) for be in backends]
+                u = us[0].clone()
+                for v in us[1:]:
+                    u += v
+                for be in backends:
+                    be.zupdate(c_lo, c_hi, float(plan.col_scale[j]), u)
+            dxs = [be.rowstep(int(r[i, 0]), int(r[i, 1])).clone() for be, r in zip(backends, ranges)]
+            dx = dxs[0]
+            for v in dxs[1:]:
+                dx += v
+            for be in backends:
+                be.xupdate(float(plan.row_scale[i]), dx)
+            if checking and k % stride == 0:
+                final = first.err()
+                if final <= tol:
+                    converged, iters = True, k
+                    break
+        else:
+            iters = max_iters
+    return dict(iters=iters, converged=converged, final_error=final,
+                states=[be.state() for be in backends])

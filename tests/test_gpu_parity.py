@@ -396,3 +396,25 @@ def test_multi_rhs_fp32_matches_reference_columns():
     if tr.iters == int(g["K"]):
         for c in range(2):
             assert rel(tr.X[:, c], g["x_K"][:, c]) <= 1e-4
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 4])
+def test_sharded_kernels_c1(ranks):
+    """Config-3 layout (interleaved row shards, u and dx allreduced) on the
+    C1 instance: one real rank, or 2/4 virtual ranks in lockstep on one GPU.
+    Same ITER as the reference and iterates within 1e-10."""
+    from paper_2001_04179_b200.sharded import CudaShardBackend, owned_rows, plan_from_context, run_virtual_ranks
+
+    g, a, prob, cfg = c1_instance()
+    ctx = P.prepare(prob, cfg)
+    plan = plan_from_context(ctx, 2000)
+    owns = [owned_rows(ctx._row_ptr, ranks, r) for r in range(ranks)]
+    bes = [CudaShardBackend(a[rows], prob.b[rows], g["x_star"], True) for rows, _ in owns]
+    res = run_virtual_ranks(bes, plan, [rg for _, rg in owns], 2000, float(g["tol"]))
+    k = int(g["iters"])
+    assert res["converged"] and res["iters"] == k
+    z = np.zeros(2000)
+    for (rows, _), (x, zl) in zip(owns, res["states"]):
+        assert rel(x, g[f"x_{k}"]) <= RTOL
+        z[rows] = zl
+    assert rel(z, g[f"z_{k}"]) <= RTOL
