@@ -262,6 +262,44 @@ FastGeometry fast_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, bool extend
   return f;
 }
 
+// Split path geometry: clusters [0, ncc) sweep columns (z rows split over
+// ncc*CS CTAs), the rest sweep rows (x columns split over the remaining CTAs).
+FastGeometry split_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int NC, int CS, int ncc) {
+  FastGeometry f;
+  f.CS = CS;
+  f.NC = NC;
+  f.G = NC * CS;
+  const int Gc = ncc * CS, Gr = (NC - ncc) * CS;
+  for (int q = 0; q < Gc; ++q)
+    f.nR_max = std::max(f.nR_max, split_rows(ctx->m, Gc, q + 1) - split_rows(ctx->m, Gc, q));
+  for (int q = 0; q < Gr; ++q)
+    f.nC_max = std::max(f.nC_max, split_even(ctx->n, Gr, q + 1) - split_even(ctx->n, Gr, q));
+  f.nI_max = max_block(cfg->n_row_blocks, cfg->row_ptr);
+  f.nJ_max = max_block(cfg->n_col_blocks, cfg->col_ptr);
+  f.ct_box_w = std::max(2, round_even(f.nJ_max));
+  f.ct_box_h = std::max(1, f.nR_max);
+  f.rt_box_w = std::max(2, round_even(f.nC_max));
+  if (f.rt_box_w % 4 == 0) f.rt_box_w += 2;
+  f.rt_box_h = f.nI_max;
+  if (f.ct_box_w > 256 || f.ct_box_h > 256 || f.rt_box_w > 256 || f.rt_box_h > 256) return f;
+  const int ne_max = std::max(f.nJ_max, f.nI_max) + 1;
+  const int sl = (ne_max + CS - 1) / CS;
+  f.pad_nC = round_even(f.nC_max + 1);
+  f.pad_nR = round_even(f.nR_max + 1);
+  f.pad_ne = round_even(ne_max + 1);
+  f.pad_in = round_even(CS * sl);
+  f.pad_cin = round_even(std::max(ncc, NC - ncc) * sl);
+  auto al16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
+  const size_t tile = std::max((size_t)f.ct_box_w * f.ct_box_h, (size_t)f.rt_box_w * f.rt_box_h);
+  f.ct_off = f.rt_off = 0;
+  f.vec_off = (int)al16(tile);
+  const size_t off = f.vec_off + 2 * (size_t)f.pad_nC + f.pad_nR + 3 * (size_t)f.pad_ne + f.pad_in + f.pad_cin +
+                     2 * 512;  // colsum2<512> row-group scratch
+  f.smem_bytes = off * sizeof(double);
+  f.ok = f.smem_bytes <= (size_t)kSmemBudget;
+  return f;
+}
+
 int env_int(const char* name, int dflt) {
   const char* s = getenv(name);
   return s ? atoi(s) : dflt;
@@ -628,6 +666,30 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
       }
     }
   }
+  // split path: column and row sweeps on two concurrent CTA groups
+  // (rebk_dense_split.cu); needs a column sweep and oracle/no stopping
+  bool use_split = false;
+  int split_ncc = 0;
+  if (use_fast && extended && env_int("REBK_SPLIT", 1) != 0 && fg.NC >= 2) {
+    const int NC = fg.NC, CS = fg.CS;
+    const double colb = (double)ctx->m * max_block(cfg->n_col_blocks, cfg->col_ptr);
+    const double rowb = (double)ctx->n * max_block(cfg->n_row_blocks, cfg->row_ptr);
+    int ncc = (int)(NC * colb / (colb + rowb) + 0.5);
+    ncc = env_int("REBK_SPLIT_NCC", ncc);
+    ncc = std::max(1, std::min(NC - 1, ncc));
+    FastGeometry sg = split_geometry(ctx, cfg, NC, CS, ncc);
+    int maxc = 0;
+    if (sg.ok && split_max_clusters(CS, sg.smem_bytes, &maxc) == cudaSuccess && maxc >= NC &&
+        encode_box(&tm_ct, ctx, sg.ct_box_w, sg.ct_box_h) && encode_box(&tm_rt, ctx, sg.rt_box_w, sg.rt_box_h)) {
+      fg = sg;
+      use_split = true;
+      split_ncc = ncc;
+    } else {
+      cudaGetLastError();
+      // restore the fused path's tensor maps
+      use_fast = encode_box(&tm_ct, ctx, fg.ct_box_w, fg.ct_box_h) && encode_box(&tm_rt, ctx, fg.rt_box_w, fg.rt_box_h);
+    }
+  }
   const int G = use_fast ? fg.G : geo.G;
 
   DevArena arena;
@@ -666,6 +728,17 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   CUDA_TRY(arena.alloc(&d_u, std::max(geo.nJ_max, 1)));
   CUDA_TRY(arena.alloc(&d_r, std::max(geo.nI_max, 1)));
   CUDA_TRY(arena.alloc(&d_errpart, G));
+  LLWord* d_zring = nullptr;
+  double* d_zhist = nullptr;
+  SplitShared* d_sh = nullptr;
+  const int split_D = std::max(2, env_int("REBK_SPLIT_RING", 16)), split_H = split_D + 4;
+  if (use_split) {
+    CUDA_TRY(arena.alloc(&d_zring, (size_t)split_D * fg.nI_max));
+    CUDA_TRY(cudaMemsetAsync(d_zring, 0, (size_t)split_D * fg.nI_max * sizeof(LLWord), stream));
+    CUDA_TRY(arena.alloc(&d_zhist, (size_t)split_H * ctx->m));
+    CUDA_TRY(arena.alloc(&d_sh, 1));
+    CUDA_TRY(cudaMemsetAsync(d_sh, 0, sizeof(SplitShared), stream));
+  }
   LLWord *d_cpu = nullptr, *d_cpr = nullptr;
   if (use_fast) {
     CUDA_TRY(arena.alloc(&d_cpu, (size_t)fg.NC * (fg.nJ_max + 1)));
@@ -778,7 +851,24 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     p.k_begin = k;
     p.k_end = k + count - 1;
     if (err == cudaSuccess) {
-      if (use_fast) {
+      if (use_split) {
+        fpar.d = p;
+        SplitParams spar{};
+        spar.f = fpar;
+        spar.ncc = split_ncc;
+        spar.ring = split_D;
+        spar.hist = split_H;
+        spar.zr_stride = fg.nI_max;
+        spar.zring = d_zring;
+        spar.zhist = d_zhist;
+        spar.sh = d_sh;
+        err = launch_dense_split(spar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
+        if (err != cudaSuccess && fast_coop) {
+          cudaGetLastError();
+          fast_coop = false;
+          err = launch_dense_split(spar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
+        }
+      } else if (use_fast) {
         fpar.d = p;
         err = launch_dense_fast(fpar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
         if (err != cudaSuccess && fast_coop) {
@@ -820,7 +910,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     int khz = 0;
     cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx->device);
     const double it = (double)std::max<int64_t>(1, ctl.iters);
-    fprintf(stderr, "[rebk prof] path=%s ", use_fast ? (fast_coop ? "fast(coop)" : "fast") : "v1");
+    fprintf(stderr, "[rebk prof] path=%s ncc=%d ", use_split ? "split" : (use_fast ? (fast_coop ? "fast(coop)" : "fast") : "v1"), split_ncc);
     fprintf(stderr, "[rebk prof] G=%d iters=%lld loop=%.3f ms (%.3f us/iter); per-iteration us: mark mean max\n", G,
             (long long)ctl.iters, ms, 1e3 * ms / it);
     for (int i = 0; i < 16; ++i) {
@@ -841,7 +931,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     trace->loop_ms = ms;
     trace->n_checks = ctl.n_checks;
     trace->grid_ctas = G;
-    trace->kernel_path = use_fast ? (fast_coop ? 2 : 1) : 0;
+    trace->kernel_path = use_split ? 6 : (use_fast ? (fast_coop ? 2 : 1) : 0);
   }
   return REBK_OK;
 }

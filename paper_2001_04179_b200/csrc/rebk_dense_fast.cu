@@ -32,16 +32,6 @@ namespace cg = cooperative_groups;
 
 namespace rebk {
 
-// Cluster barrier with release/acquire at cluster scope only.  (cg's
-// cluster.sync() also emits a GPU-scope MEMBAR, which is not needed for DSMEM
-// traffic and costs a full drain of outstanding global stores.)
-__device__ __forceinline__ void cluster_sync_rel_acq() {
-#ifdef REBK_CG_CLUSTER_SYNC
-  cg::this_cluster().sync();
-#else
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-#endif
-}
 
 __global__ void __launch_bounds__(kThreads, 1)
     rebk_dense_fast_kernel(const __grid_constant__ FastParams fp, const __grid_constant__ CUtensorMap tm_ct,

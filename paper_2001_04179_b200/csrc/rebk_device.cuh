@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cooperative_groups.h>
+
 #include "rebk_internal.h"
 
 namespace rebk {
@@ -165,6 +167,7 @@ __device__ __forceinline__ double warp_sum_cg(const double* part, int G) {
 }
 
 // block-wide fixed-order sum (all threads must call)
+template <int NT = kThreads>
 __device__ __forceinline__ double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -172,7 +175,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   if (lane == 0) red[warp] = v;
   __syncthreads();
   double s = 0.0;
-  for (int w = 0; w < kWarps; ++w) s += red[w];
+  for (int w = 0; w < (NT / 32); ++w) s += red[w];
   __syncthreads();
   return s;
 }
@@ -184,6 +187,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
           smem_u32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+// pull a 2D box into L2 ahead of its TMA load (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
+               : "memory");
 }
 __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -221,13 +229,13 @@ __device__ __forceinline__ double poll_ll(const LLWord* w, unsigned long long se
 // out[c] = Σ_{r<R} T[r*ld + c] · v[r] for c < C, T in shared memory (ld even,
 // rows 16-byte aligned).  Threads own column pairs; RG row groups, four
 // independent chains per thread; row-group partials summed in fixed order.
-template <typename Epi>
+template <int NT = kThreads, typename Epi>
 __device__ __forceinline__ void colsum2(const double* __restrict__ T, int ld, int R, int C,
                                         const double* __restrict__ v, double* red, Epi epi) {
   const int tid = threadIdx.x;
   if (C <= 0) return;
   const int CP = (C + 1) >> 1;
-  int RG = kThreads / CP;
+  int RG = NT / CP;
   if (RG > R) RG = R > 0 ? R : 1;
   const int cp = tid % CP, rg = tid / CP;
   double2 a0 = make_double2(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
@@ -272,7 +280,7 @@ __device__ __forceinline__ void colsum2(const double* __restrict__ T, int ld, in
     red[rg * 2 * CP + 2 * cp + 1] = sy;
   }
   __syncthreads();
-  for (int c = tid; c < C; c += kThreads) {
+  for (int c = tid; c < C; c += NT) {
     double s = 0.0;
     for (int q = 0; q < RG; ++q) s += red[q * 2 * CP + c];
     epi(c, s);
@@ -283,17 +291,17 @@ __device__ __forceinline__ void colsum2(const double* __restrict__ T, int ld, in
 // out[r] = Σ_{c<C} T[r*ld + c] · v[c] for r < R.  L lanes per row read
 // 16-byte pairs; xor butterfly inside the lane group.  An odd trailing column
 // is handled by one lane so v needs no padding.
-template <typename Epi>
+template <int NT = kThreads, typename Epi>
 __device__ __forceinline__ void rowdot2(const double* __restrict__ T, int ld, int R, int C,
                                         const double* __restrict__ v, Epi epi) {
   if (R <= 0) return;
   const int tid = threadIdx.x;
   const int CPf = C >> 1;  // full pairs
-  int L = pow2floor(kThreads / R);
+  int L = pow2floor(NT / R);
   const int lmax = CPf >= 1 ? pow2floor(CPf) : 1;
   L = L > 32 ? 32 : L;
   L = L > lmax ? lmax : L;
-  const int sub = tid % L, rsub = tid / L, rpp = kThreads / L;
+  const int sub = tid % L, rsub = tid / L, rpp = NT / L;
   const double2* v2 = reinterpret_cast<const double2*>(v);
   for (int r0 = 0; r0 < R; r0 += rpp) {
     const int r = r0 + rsub;
@@ -320,6 +328,17 @@ __device__ __forceinline__ void rowdot2(const double* __restrict__ T, int ld, in
     for (int off = L / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if (sub == 0 && r < R) epi(r, acc);
   }
+}
+
+// Cluster barrier with release/acquire at cluster scope only.  (cg's
+// cluster.sync() also emits a GPU-scope MEMBAR, which is not needed for DSMEM
+// traffic and costs a full drain of outstanding global stores.)
+__device__ __forceinline__ void cluster_sync_rel_acq() {
+#ifdef REBK_CG_CLUSTER_SYNC
+  cooperative_groups::this_cluster().sync();
+#else
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+#endif
 }
 
 }  // namespace rebk

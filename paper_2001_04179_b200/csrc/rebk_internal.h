@@ -33,6 +33,13 @@ struct Control {
   int32_t has_error;
   int32_t fault;  // launch-shape mismatch detected on the device
   unsigned long long xseq;  // exchanges completed (fast path), carried across chunk launches
+  unsigned long long xseq_row;  // split path: row-group exchanges
+};
+
+// Split path: column-sweep group feeding the row-sweep group (rebk_dense_split.cu)
+struct SplitShared {
+  unsigned long long row_progress;  // last iteration whose z_I the row group has consumed
+  unsigned long long stop;          // 0 running; K+1 = the run stopped with state K
 };
 
 // 16-byte {value, sequence} word of the fast path's cross-cluster exchange
@@ -87,6 +94,17 @@ struct FastParams {
   int32_t rt_box_w, rt_box_h;
   int32_t pad_nC, pad_nR, pad_ne, pad_in, pad_cin;  // smem vector sizes (doubles, even)
   int32_t cluster_size;  // expected cluster size (checked on the device)
+};
+
+struct SplitParams {
+  FastParams f;
+  int32_t ncc;       // clusters [0, ncc) sweep columns (z), the rest sweep rows (x)
+  int32_t ring;      // depth D of the z_I ring (column group may run D iterations ahead)
+  int32_t hist;      // depth H of the z history (exact stop state), H >= D + 2
+  int32_t zr_stride; // entries per ring slot (>= nI_max)
+  LLWord* zring;     // [D][zr_stride] {z_{k,i}, seq = k}
+  double* zhist;     // [H][m]
+  SplitShared* sh;
 };
 
 // Sparse (CSR + CSC twin) persistent kernel (rebk_csr.cu).
@@ -169,6 +187,9 @@ cudaError_t dense_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
 cudaError_t launch_dense_fast(const FastParams& fp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
                               int cluster_size, size_t smem_bytes, cudaStream_t stream, bool cooperative);
 cudaError_t fast_max_clusters(int cluster_size, size_t smem_bytes, int* clusters);
+cudaError_t split_max_clusters(int cluster_size, size_t smem_bytes, int* clusters);
+cudaError_t launch_dense_split(const SplitParams& sp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
+                               int cluster_size, size_t smem_bytes, cudaStream_t stream, bool cooperative);
 cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream);
 cudaError_t csr_kernel_occupancy(int* blocks_per_sm);
 struct MrhsRun {
