@@ -97,6 +97,16 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
   uint32_t xpar[2] = {0u, 0u};
   cluster_sync_rel_acq();
 
+  long long prof_acc[16];
+  for (int i = 0; i < 16; ++i) prof_acc[i] = 0;
+  long long prof_last = clock64();
+#define PROF(i)                      \
+  if (p.prof) {                      \
+    const long long _t = clock64();  \
+    prof_acc[i] += _t - prof_last;   \
+    prof_last = _t;                  \
+  }
+  const int xb = colgrp ? 8 : 12;  // exchange-internal profile marks of my group
   // ---- group exchange (same protocol as the fast path, group-local)
   unsigned long long xseq = colgrp ? *((volatile unsigned long long*)&ctl->xseq)
                                    : *((volatile unsigned long long*)&ctl->xseq_row);
@@ -118,17 +128,20 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
     if (tid == 0) mbar_wait(&xbar[0], xpar[0]);
     xpar[0] ^= 1u;
     __syncthreads();
+    PROF(xb + 0);
     for (int e = tid; e < nmy; e += kSplitThreads) {
       double acc = 0.0;
       for (int q = 0; q < CS; ++q) acc += s_in[q * sl + e];
       st_ll(cpart_g + (size_t)lcid * stride_g + e0 + e, acc, seq);
     }
+    PROF(xb + 1);
     for (int t = tid; t < NCg * nmy; t += kSplitThreads) {
       const int q = t / nmy, e = t - q * nmy;
       s_cin[t] = poll_ll(cpart_g + (size_t)q * stride_g + e0 + e, seq);
     }
     if (tid == 0) mbar_arrive_expect_tx(&xbar[1], (uint32_t)(ne * 8));
     __syncthreads();
+    PROF(xb + 2);
     const uint32_t out_base = smem_u32(s_out), bar1 = smem_u32(&xbar[1]);
     for (int e = tid; e < nmy; e += kSplitThreads) {
       double acc = 0.0;
@@ -140,6 +153,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
     if (tid == 0) mbar_wait(&xbar[1], xpar[1]);
     xpar[1] ^= 1u;
     __syncthreads();
+    PROF(xb + 3);
   };
   auto ident = [](int, double s) { return s; };
 
@@ -167,15 +181,6 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
     tile_pending = true;
   };
 
-  long long prof_acc[8];
-  for (int i = 0; i < 8; ++i) prof_acc[i] = 0;
-  long long prof_last = clock64();
-#define PROF(i)                      \
-  if (p.prof) {                      \
-    const long long _t = clock64();  \
-    prof_acc[i] += _t - prof_last;   \
-    prof_last = _t;                  \
-  }
 
   if (colgrp) {
     // ================================ column sweep ================================
@@ -199,9 +204,9 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
       // same iteration (a CTA that left alone would strand the others in it)
       if (tid == 0) s_part[nJ] = ld_acquire_u64(&sh->stop) != 0 ? 1.0 : 0.0;
       __syncthreads();
+      PROF(1);
       exchange(nJ + 1, s_u, ident);
       if (s_u[nJ] != 0.0) break;
-      PROF(1);
       const double cs = pl.c_scale;
       double* hist = spp.zhist + (size_t)(k % H) * p.m;
       rowdot2<kSplitThreads>(s_tile, fp.ct_box_w, nR, nJ, s_u, [&](int r, double acc) {
@@ -324,6 +329,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
       rowdot2<kSplitThreads>(s_tile, fp.rt_box_w, nI, nC, s_x, [&](int r, double acc) { s_part[r] = acc; });
       if (pending && tid == 0) s_part[nI] = s_errp;
       __syncthreads();
+      PROF(5);
       const int rl = pl.r_lo;
       const LLWord* slot = spp.zring + (size_t)(k % D) * spp.zr_stride;
       // r = ((Σ_g rpart) - b_I) + z_{k,I}; z_{k,I} arrives from the column group
@@ -333,7 +339,6 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
         if (p.extended) rv += poll_ll(slot + e, (unsigned long long)k);
         return rv;
       });
-      PROF(5);
       if (pending) {
         pending = false;
         if (decide(s_r[nI], pending_k)) {  // sets sh->stop before any progress past k-1 is visible
@@ -372,7 +377,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
     if (leader) ctl->xseq_row = xseq;
   }
   if (p.prof && tid == 0)
-    for (int i = 0; i < 8; ++i) p.prof[g * 16 + i] = prof_acc[i];
+    for (int i = 0; i < 16; ++i) p.prof[g * 16 + i] = prof_acc[i];
 #undef PROF
   wait_tile();
   __syncthreads();
