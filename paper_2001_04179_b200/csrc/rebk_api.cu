@@ -25,10 +25,12 @@ using namespace rebk;
 struct CsrSegPlan {
   std::vector<int64_t> row_ptr, col_ptr;  // the partition (cache key) and the grid size
   int G = 0;
-  int64_t *cseg_off = nullptr, *cseg_lo = nullptr, *cseg_hi = nullptr, *cseg_cta = nullptr;
-  int32_t* cseg_row = nullptr;
-  int64_t *rseg_off = nullptr, *rseg_lo = nullptr, *rseg_hi = nullptr, *rseg_cta = nullptr;
-  int32_t* rseg_col = nullptr;
+  int64_t *cseg_off = nullptr, *cseg_ptr = nullptr, *cseg_cta = nullptr;
+  int32_t *cseg_row = nullptr, *ccol = nullptr;
+  double* cval = nullptr;
+  int64_t *rseg_off = nullptr, *rseg_ptr = nullptr, *rseg_cta = nullptr;
+  int32_t *rseg_col = nullptr, *rrow = nullptr;
+  double* rval = nullptr;
 };
 
 struct rebk_ctx {
@@ -45,6 +47,7 @@ struct rebk_ctx {
   double *csr_val = nullptr, *csc_val = nullptr;
   std::vector<int64_t> h_csr_ptr, h_csc_ptr;
   std::vector<int32_t> h_csr_col, h_csc_row;
+  std::vector<double> h_csr_val, h_csc_val;
   std::vector<CsrSegPlan*> seg_cache;
   float* A32 = nullptr;  // dense fp32 A (multi-RHS contexts, kind 2)
   double* shard_scratch = nullptr;  // rebk_shard_* partials (not reentrant per ctx)
@@ -221,6 +224,8 @@ struct FastGeometry {
   int ct_box_w = 0, ct_box_h = 0, rt_box_w = 0, rt_box_h = 0;
   int pad_nC = 0, pad_nR = 0, pad_ne = 0, pad_in = 0, pad_cin = 0;
   int ct_off = 0, rt_off = 0, vec_off = 0;
+  int vec_off_c = 0, vec_off_r = 0;  // split path: per-group vector bases
+  int pieces = 1;                    // split path: TMA boxes per tile
   size_t smem_bytes = 0;
 };
 
@@ -264,7 +269,7 @@ FastGeometry fast_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, bool extend
 
 // Split path geometry: clusters [0, ncc) sweep columns (z rows split over
 // ncc*CS CTAs), the rest sweep rows (x columns split over the remaining CTAs).
-FastGeometry split_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int NC, int CS, int ncc) {
+FastGeometry split_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int NC, int CS, int ncc, int xmode, int pieces) {
   FastGeometry f;
   f.CS = CS;
   f.NC = NC;
@@ -277,10 +282,14 @@ FastGeometry split_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int NC, in
   f.nI_max = max_block(cfg->n_row_blocks, cfg->row_ptr);
   f.nJ_max = max_block(cfg->n_col_blocks, cfg->col_ptr);
   f.ct_box_w = std::max(2, round_even(f.nJ_max));
-  f.ct_box_h = std::max(1, f.nR_max);
+  // pieces == 2: each tile arrives as two half-height boxes (rows [0, h) and
+  // [h, 2h)) on two mbarriers, so the next tile's first half loads while the
+  // second half is still being consumed; pieces == 1: one box per tile
+  f.pieces = pieces;
+  f.ct_box_h = std::max(1, (f.nR_max + pieces - 1) / pieces);
   f.rt_box_w = std::max(2, round_even(f.nC_max));
   if (f.rt_box_w % 4 == 0) f.rt_box_w += 2;
-  f.rt_box_h = f.nI_max;
+  f.rt_box_h = std::max(1, (f.nI_max + pieces - 1) / pieces);
   if (f.ct_box_w > 256 || f.ct_box_h > 256 || f.rt_box_w > 256 || f.rt_box_h > 256) return f;
   const int ne_max = std::max(f.nJ_max, f.nI_max) + 1;
   const int sl = (ne_max + CS - 1) / CS;
@@ -288,16 +297,47 @@ FastGeometry split_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int NC, in
   f.pad_nR = round_even(f.nR_max + 1);
   f.pad_ne = round_even(ne_max + 1);
   f.pad_in = round_even(CS * sl);
-  f.pad_cin = round_even(std::max(ncc, NC - ncc) * sl);
+  f.pad_cin = round_even(std::max(ncc, NC - ncc) * ne_max);  // all entries from every cluster
   auto al16 = [](size_t v) { return (v + 15) & ~(size_t)15; };
-  const size_t tile = std::max((size_t)f.ct_box_w * f.ct_box_h, (size_t)f.rt_box_w * f.rt_box_h);
+  // per-group layouts after the group's own tile:
+  //   column group: [tile][z][u r part][in][red][cin over ncc clusters]
+  //   row group:    [tile][x xs][u r part][in][red][cin over NC-ncc clusters]
   f.ct_off = f.rt_off = 0;
-  f.vec_off = (int)al16(tile);
-  const size_t off = f.vec_off + 2 * (size_t)f.pad_nC + f.pad_nR + 3 * (size_t)f.pad_ne + f.pad_in + f.pad_cin +
-                     2 * 512;  // colsum2<512> row-group scratch
-  f.smem_bytes = off * sizeof(double);
+  f.vec_off_c = (int)(pieces * al16((size_t)f.ct_box_w * f.ct_box_h));
+  f.vec_off_r = (int)(pieces * al16((size_t)f.rt_box_w * f.rt_box_h));
+  f.vec_off = f.vec_off_c;
+  const size_t common = 3 * (size_t)f.pad_ne + f.pad_in + 2 * 512;  // 2*512: colsum2<512> scratch
+  // s_cin: a gather-all exchange keeps every cluster's partials of every
+  // entry, a broadcast exchange only those of the CTA's slice
+  const int gather_c = xmode & 1, gather_r = (xmode >> 1) & 1;
+  const size_t cin_c = (size_t)ncc * (gather_c ? ne_max : sl), cin_r = (size_t)(NC - ncc) * (gather_r ? ne_max : sl);
+  const size_t need_c = f.vec_off_c + (size_t)f.pad_nR + common + cin_c;
+  const size_t need_r = f.vec_off_r + 2 * (size_t)f.pad_nC + common + cin_r;
+  f.pad_cin = round_even((int)std::max(cin_c, cin_r));
+  f.smem_bytes = std::max(need_c, need_r) * sizeof(double);
   f.ok = f.smem_bytes <= (size_t)kSmemBudget;
   return f;
+}
+
+// REBK_PROF tables: per-iteration microseconds per mark, mean and max over
+// CTAs; CTAs [0, gsplit) and [gsplit, G) get separate tables (split path).
+void print_prof(const std::vector<long long>& h, int G, int gsplit, int khz, double it) {
+  for (int grp = 0; grp < (gsplit < G ? 2 : 1); ++grp) {
+    const int q0 = grp ? gsplit : 0, q1 = grp ? G : gsplit;
+    if (gsplit < G) fprintf(stderr, "[rebk prof] %s group, %d CTAs\n", grp ? "row" : "column", q1 - q0);
+    double tot = 0;
+    for (int i = 0; i < 16; ++i) {
+      double mean = 0, mx = 0;
+      for (int q = q0; q < q1; ++q) {
+        const double v = (double)h[(size_t)q * 16 + i] / (khz * 1e-3) / it;
+        mean += v / (q1 - q0);
+        mx = std::max(mx, v);
+      }
+      tot += mean;
+      if (mx > 0) fprintf(stderr, "[rebk prof] %2d %8.3f %8.3f\n", i, mean, mx);
+    }
+    fprintf(stderr, "[rebk prof] sum %8.3f\n", tot);
+  }
 }
 
 int env_int(const char* name, int dflt) {
@@ -322,8 +362,10 @@ cudaError_t upload_vec(T** dst, const std::vector<T>& v) {
 
 void free_seg_plan(CsrSegPlan* sp) {
   if (!sp) return;
-  cudaFree(sp->cseg_off); cudaFree(sp->cseg_lo); cudaFree(sp->cseg_hi); cudaFree(sp->cseg_cta); cudaFree(sp->cseg_row);
-  cudaFree(sp->rseg_off); cudaFree(sp->rseg_lo); cudaFree(sp->rseg_hi); cudaFree(sp->rseg_cta); cudaFree(sp->rseg_col);
+  cudaFree(sp->cseg_off); cudaFree(sp->cseg_ptr); cudaFree(sp->cseg_cta); cudaFree(sp->cseg_row);
+  cudaFree(sp->ccol); cudaFree(sp->cval);
+  cudaFree(sp->rseg_off); cudaFree(sp->rseg_ptr); cudaFree(sp->rseg_cta); cudaFree(sp->rseg_col);
+  cudaFree(sp->rrow); cudaFree(sp->rval);
   delete sp;
 }
 
@@ -346,8 +388,9 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
   sp->row_ptr.assign(cfg->row_ptr, cfg->row_ptr + s + 1);
   if (extended) sp->col_ptr.assign(cfg->col_ptr, cfg->col_ptr + t + 1);
   // column blocks -> row segments into CSR
-  std::vector<int64_t> coff(t + 1, 0), clo, chi, ccta;
-  std::vector<int32_t> crow;
+  std::vector<int64_t> coff(t + 1, 0), clo, chi, ccta, cptr(1, 0);
+  std::vector<int32_t> crow, ccolv;
+  std::vector<double> cval;
   if (extended) {
     std::vector<int32_t> blk_of_col(n);
     for (int64_t b = 0; b < t; ++b)
@@ -379,6 +422,19 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
         prev = b;
       }
     }
+    // compact copies of each column block's entries, segment by segment
+    cptr.resize(ns + 1);
+    cptr[0] = 0;
+    for (int64_t q = 0; q < ns; ++q) cptr[q + 1] = cptr[q] + (chi[q] - clo[q]);
+    cval.resize(cptr[ns]);
+    ccolv.resize(cptr[ns]);
+    for (int64_t b = 0; b < t; ++b)
+      for (int64_t q = coff[b]; q < coff[b + 1]; ++q)
+        for (int64_t e = clo[q]; e < chi[q]; ++e) {
+          const int64_t o = cptr[q] + (e - clo[q]);
+          cval[o] = ctx->h_csr_val[e];
+          ccolv[o] = ctx->h_csr_col[e] - (int32_t)cfg->col_ptr[b];
+        }
     ccta.resize(t * (G + 1));
     for (int64_t b = 0; b < t; ++b)
       for (int q = 0; q <= G; ++q) {
@@ -388,8 +444,9 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
       }
   }
   // row blocks -> column segments into CSC
-  std::vector<int64_t> roff(s + 1, 0), rlo, rhi, rcta;
-  std::vector<int32_t> rcol;
+  std::vector<int64_t> roff(s + 1, 0), rlo, rhi, rcta, rptr(1, 0);
+  std::vector<int32_t> rcol, rrowv;
+  std::vector<double> rval;
   {
     std::vector<int32_t> blk_of_row(m);
     for (int64_t b = 0; b < s; ++b)
@@ -421,6 +478,18 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
         prev = b;
       }
     }
+    rptr.resize(ns + 1);
+    rptr[0] = 0;
+    for (int64_t q = 0; q < ns; ++q) rptr[q + 1] = rptr[q] + (rhi[q] - rlo[q]);
+    rval.resize(rptr[ns]);
+    rrowv.resize(rptr[ns]);
+    for (int64_t b = 0; b < s; ++b)
+      for (int64_t q = roff[b]; q < roff[b + 1]; ++q)
+        for (int64_t e = rlo[q]; e < rhi[q]; ++e) {
+          const int64_t o = rptr[q] + (e - rlo[q]);
+          rval[o] = ctx->h_csc_val[e];
+          rrowv[o] = ctx->h_csc_row[e] - (int32_t)cfg->row_ptr[b];
+        }
     rcta.resize(s * (G + 1));
     for (int64_t b = 0; b < s; ++b)
       for (int q = 0; q <= G; ++q) {
@@ -431,13 +500,15 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
   }
   cudaError_t e = cudaSuccess;
   if (!e) e = upload_vec(&sp->cseg_off, coff);
-  if (!e) e = upload_vec(&sp->cseg_lo, clo);
-  if (!e) e = upload_vec(&sp->cseg_hi, chi);
+  if (!e) e = upload_vec(&sp->cseg_ptr, cptr);
+  if (!e) e = upload_vec(&sp->cval, cval);
+  if (!e) e = upload_vec(&sp->ccol, ccolv);
   if (!e) e = upload_vec(&sp->cseg_row, crow);
   if (!e) e = upload_vec(&sp->cseg_cta, ccta);
   if (!e) e = upload_vec(&sp->rseg_off, roff);
-  if (!e) e = upload_vec(&sp->rseg_lo, rlo);
-  if (!e) e = upload_vec(&sp->rseg_hi, rhi);
+  if (!e) e = upload_vec(&sp->rseg_ptr, rptr);
+  if (!e) e = upload_vec(&sp->rval, rval);
+  if (!e) e = upload_vec(&sp->rrow, rrowv);
   if (!e) e = upload_vec(&sp->rseg_col, rcol);
   if (!e) e = upload_vec(&sp->rseg_cta, rcta);
   if (e) {
@@ -502,6 +573,11 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
   if (errs_cap > 0) CUDA_TRY(arena.alloc(&d_errs, errs_cap));
   CUDA_TRY(arena.alloc(&d_ctl, 1));
   CUDA_TRY(cudaMemsetAsync(d_ctl, 0, sizeof(Control), stream));
+  long long* d_prof = nullptr;
+  if (env_int("REBK_PROF", 0) == 1) {
+    CUDA_TRY(arena.alloc(&d_prof, (size_t)G * 16));
+    CUDA_TRY(cudaMemsetAsync(d_prof, 0, (size_t)G * 16 * 8, stream));
+  }
 
   SampleParams smp{};
   smp.key0 = cfg->philox_key[0];
@@ -531,13 +607,15 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
   p.csc_val = ctx->csc_val;
   p.cseg_off = sp->cseg_off;
   p.cseg_row = sp->cseg_row;
-  p.cseg_lo = sp->cseg_lo;
-  p.cseg_hi = sp->cseg_hi;
+  p.cseg_ptr = sp->cseg_ptr;
+  p.cval = sp->cval;
+  p.ccol = sp->ccol;
   p.cseg_cta = sp->cseg_cta;
   p.rseg_off = sp->rseg_off;
   p.rseg_col = sp->rseg_col;
-  p.rseg_lo = sp->rseg_lo;
-  p.rseg_hi = sp->rseg_hi;
+  p.rseg_ptr = sp->rseg_ptr;
+  p.rval = sp->rval;
+  p.rrow = sp->rrow;
   p.rseg_cta = sp->rseg_cta;
   p.b = b_dev;
   p.xs = xs_dev;
@@ -558,6 +636,7 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
   p.max_iters = cfg->max_iters;
   p.res_scale = cfg->residual_scale > 0.0 ? cfg->residual_scale : 1.0;
   p.record = errs_cap > 0;
+  p.prof = d_prof;
 
   cudaEvent_t ev0, ev1;
   CUDA_TRY(cudaEventCreate(&ev0));
@@ -590,6 +669,16 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   if (err != cudaSuccess) return fail(REBK_ECUDA, "sparse REBK run failed: %s", cudaGetErrorString(err));
+  if (d_prof) {
+    std::vector<long long> h((size_t)G * 16);
+    cudaMemcpy(h.data(), d_prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx->device);
+    const double it = (double)std::max<int64_t>(1, ctl.iters);
+    fprintf(stderr, "[rebk prof] path=csr G=%d iters=%lld loop=%.3f ms (%.3f us/iter); mark mean max\n", G,
+            (long long)ctl.iters, ms, 1e3 * ms / it);
+    print_prof(h, G, G, khz, it);
+  }
   if (trace) {
     trace->iters = ctl.iters;
     trace->converged = ctl.converged;
@@ -670,6 +759,8 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   // (rebk_dense_split.cu); needs a column sweep and oracle/no stopping
   bool use_split = false;
   int split_ncc = 0;
+  const int split_xmode = env_int("REBK_SPLIT_XMODE", 0);  // bit 0/1: column/row group exchanges gather all
+  const int split_pieces = std::max(1, std::min(2, env_int("REBK_SPLIT_PIECES", 2)));
   if (use_fast && extended && env_int("REBK_SPLIT", 1) != 0 && fg.NC >= 2) {
     const int NC = fg.NC, CS = fg.CS;
     const double colb = (double)ctx->m * max_block(cfg->n_col_blocks, cfg->col_ptr);
@@ -677,7 +768,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     int ncc = (int)(NC * colb / (colb + rowb) + 0.5);
     ncc = env_int("REBK_SPLIT_NCC", ncc);
     ncc = std::max(1, std::min(NC - 1, ncc));
-    FastGeometry sg = split_geometry(ctx, cfg, NC, CS, ncc);
+    FastGeometry sg = split_geometry(ctx, cfg, NC, CS, ncc, split_xmode, split_pieces);
     int maxc = 0;
     if (sg.ok && split_max_clusters(CS, sg.smem_bytes, &maxc) == cudaSuccess && maxc >= NC &&
         encode_box(&tm_ct, ctx, sg.ct_box_w, sg.ct_box_h) && encode_box(&tm_rt, ctx, sg.rt_box_w, sg.rt_box_h)) {
@@ -741,15 +832,25 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   }
   LLWord *d_cpu = nullptr, *d_cpr = nullptr;
   if (use_fast) {
-    CUDA_TRY(arena.alloc(&d_cpu, (size_t)fg.NC * (fg.nJ_max + 1)));
-    CUDA_TRY(arena.alloc(&d_cpr, (size_t)fg.NC * (2 * fg.nI_max + 1)));
-    CUDA_TRY(cudaMemsetAsync(d_cpu, 0, (size_t)fg.NC * (fg.nJ_max + 1) * sizeof(LLWord), stream));
-    CUDA_TRY(cudaMemsetAsync(d_cpr, 0, (size_t)fg.NC * (2 * fg.nI_max + 1) * sizeof(LLWord), stream));
+    // two slots each (exchange sequence parity)
+    CUDA_TRY(arena.alloc(&d_cpu, 2 * (size_t)fg.NC * (fg.nJ_max + 1)));
+    CUDA_TRY(arena.alloc(&d_cpr, 2 * (size_t)fg.NC * (2 * fg.nI_max + 1)));
+    CUDA_TRY(cudaMemsetAsync(d_cpu, 0, 2 * (size_t)fg.NC * (fg.nJ_max + 1) * sizeof(LLWord), stream));
+    CUDA_TRY(cudaMemsetAsync(d_cpr, 0, 2 * (size_t)fg.NC * (2 * fg.nI_max + 1) * sizeof(LLWord), stream));
   }
   if (cfg->stop_mode == REBK_STOP_RESIDUAL_PROXY) CUDA_TRY(arena.alloc(&d_res, ctx->m));
   const int64_t errs_cap = (cfg->record_errors && trace && trace->errors) ? trace->errors_cap : 0;
   if (errs_cap > 0) CUDA_TRY(arena.alloc(&d_errs, errs_cap));
   CUDA_TRY(arena.alloc(&d_ctl, 1));
+  // REBK_TRACE=n: globaltimer stamps of the split exchanges for iterations
+  // [REBK_TRACE_K0, +n), written raw to REBK_TRACE_FILE (tools/trace_split.py)
+  const int trace_n = env_int("REBK_TRACE", 0);
+  const int64_t trace_k0 = env_int("REBK_TRACE_K0", 2000);
+  unsigned long long* d_trace = nullptr;
+  if (trace_n > 0 && use_split) {
+    CUDA_TRY(arena.alloc(&d_trace, (size_t)trace_n * G * 8));
+    CUDA_TRY(cudaMemsetAsync(d_trace, 0, (size_t)trace_n * G * 8 * 8, stream));
+  }
   const char* prof_env = getenv("REBK_PROF");
   long long* d_prof = nullptr;
   if (prof_env && prof_env[0] == '1') {
@@ -862,6 +963,13 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
         spar.zring = d_zring;
         spar.zhist = d_zhist;
         spar.sh = d_sh;
+        spar.vec_off_c = fg.vec_off_c;
+        spar.vec_off_r = fg.vec_off_r;
+        spar.xmode = split_xmode;
+        spar.pieces = fg.pieces;
+        spar.trace = d_trace;
+        spar.trace_k0 = trace_k0;
+        spar.trace_n = trace_n;
         err = launch_dense_split(spar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
         if (err != cudaSuccess && fast_coop) {
           cudaGetLastError();
@@ -904,6 +1012,18 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   cudaEventDestroy(ev1);
   if (err != cudaSuccess) return fail(REBK_ECUDA, "REBK run failed: %s", cudaGetErrorString(err));
   if (ctl.fault) return fail(REBK_ECUDA, "clustered kernel launched without its %d-CTA clusters", fg.CS);
+  if (d_trace) {
+    std::vector<unsigned long long> h((size_t)trace_n * G * 8);
+    cudaMemcpy(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    const char* fn = getenv("REBK_TRACE_FILE");
+    FILE* f = fopen(fn ? fn : "rebk_trace.bin", "wb");
+    if (f) {
+      const int32_t hdr[4] = {trace_n, G, split_ncc * fg.CS, fg.CS};
+      fwrite(hdr, sizeof hdr, 1, f);
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   if (d_prof) {
     std::vector<long long> h((size_t)G * 16);
     cudaMemcpy(h.data(), d_prof, h.size() * 8, cudaMemcpyDeviceToHost);
@@ -913,15 +1033,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     fprintf(stderr, "[rebk prof] path=%s ncc=%d ", use_split ? "split" : (use_fast ? (fast_coop ? "fast(coop)" : "fast") : "v1"), split_ncc);
     fprintf(stderr, "[rebk prof] G=%d iters=%lld loop=%.3f ms (%.3f us/iter); per-iteration us: mark mean max\n", G,
             (long long)ctl.iters, ms, 1e3 * ms / it);
-    for (int i = 0; i < 16; ++i) {
-      double mean = 0, mx = 0;
-      for (int q = 0; q < G; ++q) {
-        const double v = (double)h[(size_t)q * 16 + i] / (khz * 1e-3) / it;
-        mean += v / G;
-        mx = std::max(mx, v);
-      }
-      if (mx > 0) fprintf(stderr, "[rebk prof] %2d %8.3f %8.3f\n", i, mean, mx);
-    }
+    print_prof(h, G, use_split ? split_ncc * fg.CS : G, khz, it);
   }
   if (trace) {
     trace->iters = ctl.iters;
@@ -1065,13 +1177,14 @@ int rebk_ctx_create_csr(const int64_t* indptr, const int32_t* indices, const dou
         csc_val[q] = data[e];
       }
   }
-  std::vector<double> csr_val(data, data + nnz);
+  c->h_csr_val.assign(data, data + nnz);
+  c->h_csc_val = std::move(csc_val);
   cudaError_t e = upload_vec(&c->csr_ptr, c->h_csr_ptr);
   if (!e) e = upload_vec(&c->csr_col, c->h_csr_col);
-  if (!e) e = upload_vec(&c->csr_val, csr_val);
+  if (!e) e = upload_vec(&c->csr_val, c->h_csr_val);
   if (!e) e = upload_vec(&c->csc_ptr, c->h_csc_ptr);
   if (!e) e = upload_vec(&c->csc_row, c->h_csc_row);
-  if (!e) e = upload_vec(&c->csc_val, csc_val);
+  if (!e) e = upload_vec(&c->csc_val, c->h_csc_val);
   if (e) {
     rebk_ctx_destroy(c);
     return fail(REBK_ENOMEM, "CSR upload failed: %s", cudaGetErrorString(e));

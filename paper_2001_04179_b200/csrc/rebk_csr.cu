@@ -68,6 +68,21 @@ __device__ __forceinline__ double warp_ordered_dot(const double* __restrict__ va
                                                    const double* vec, int off, int64_t lo, int64_t hi) {
   const int lane = threadIdx.x & 31;
   double sum = 0.0;
+  constexpr int kPf = 8;  // chunks whose gathers are all in flight before the ordered adds
+  if (hi - lo <= 32 * kPf) {
+    double prod[kPf];
+#pragma unroll
+    for (int c = 0; c < kPf; ++c) {
+      const int64_t e = lo + 32 * c + lane;
+      prod[c] = e < hi ? __dmul_rn(val[e], __ldcg(vec + (idx[e] - off))) : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < kPf; ++c) {
+      const int64_t base = lo + 32 * c;
+      if (base < hi) sum = ordered_lane_sum(sum, prod[c], (int)((hi - base) < 32 ? (hi - base) : 32));
+    }
+    return sum;
+  }
   for (int64_t base = lo; base < hi; base += 32) {
     const int64_t e = base + lane;
     double prod = 0.0;
@@ -154,7 +169,8 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
   };
   // u_j = Σ_i A_ij z_i over CSC column j, for the column block of `pl`
   // (one warp per column; products gathered in parallel, summed in order)
-  const int64_t gwarp = (int64_t)g * kCsrWarps + warp, gwarps = (int64_t)G * kCsrWarps;
+  // items (columns of J, rows of I) go round-robin over CTAs first, then warps
+  const int64_t gwarp = (int64_t)warp * G + g, gwarps = (int64_t)G * kCsrWarps;
   auto compute_u = [&](const Plan& pl) {
     for (int64_t j = pl.c_lo + gwarp; j < pl.c_hi; j += gwarps) {
       const double acc = warp_ordered_dot(p.csc_val, p.csc_row, p.z, 0, p.csc_ptr[j], p.csc_ptr[j + 1]);
@@ -162,6 +178,15 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     }
   };
 
+  long long prof_acc[8];
+  for (int i = 0; i < 8; ++i) prof_acc[i] = 0;
+  long long prof_last = clock64();
+#define PROF(i)                      \
+  if (p.prof) {                      \
+    const long long _t = clock64();  \
+    prof_acc[i] += _t - prof_last;   \
+    prof_last = _t;                  \
+  }
   bool finished = false;
   if (p.k_begin == 1 && checking) {
     if (oracle) {
@@ -192,6 +217,7 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
       }
     }
     const double cs = pl.c_scale, rs = pl.r_scale;
+    PROF(0);
     if (p.extended) {
       const int64_t s0 = p.cseg_cta[(int64_t)pl.cb * (G + 1) + g];
       const int64_t s1 = p.cseg_cta[(int64_t)pl.cb * (G + 1) + g + 1];
@@ -199,28 +225,43 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
         const int i = p.cseg_row[sg];
         if (i >= pl.r_lo && i < pl.r_hi) continue;  // done by the row-sweep threads below
         double acc = 0.0;
-        for (int64_t e = p.cseg_lo[sg]; e < p.cseg_hi[sg]; ++e)
-          acc = madd(acc, p.csr_val[e], __ldcg(p.u + (p.csr_col[e] - pl.c_lo)));
+        const int64_t e1 = p.cseg_ptr[sg + 1];
+        for (int64_t e = p.cseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.cval[e], __ldcg(p.u + p.ccol[e]));
         __stcg(p.z + i, __dsub_rn(__ldcg(p.z + i), __dmul_rn(cs, acc)));
       }
     }
+    PROF(1);
     // rows of I: one warp per row; r_i and the row's own z update
     for (int64_t i = pl.r_lo + gwarp; i < pl.r_hi; i += gwarps) {
       double ax = 0.0, au = 0.0;
       const int64_t lo = p.csr_ptr[i], hi = p.csr_ptr[i + 1];
-      for (int64_t base = lo; base < hi; base += 32) {
-        const int64_t e = base + lane;
-        double px = 0.0, pu = 0.0;
-        if (e < hi) {
-          const int c = p.csr_col[e];
-          const double a = p.csr_val[e];
-          px = __dmul_rn(a, __ldcg(p.x + c));
-          if (p.extended && c >= pl.c_lo && c < pl.c_hi) pu = __dmul_rn(a, __ldcg(p.u + (c - pl.c_lo)));
+      constexpr int kPf = 4;  // a row's gathers all in flight, then the ordered adds
+      int64_t base = lo;
+      while (base < hi) {
+        double px[kPf], pu[kPf];
+#pragma unroll
+        for (int c = 0; c < kPf; ++c) {
+          const int64_t e = base + 32 * c + lane;
+          px[c] = 0.0;
+          pu[c] = 0.0;
+          if (e < hi) {
+            const int col = p.csr_col[e];
+            const double a = p.csr_val[e];
+            px[c] = __dmul_rn(a, __ldcg(p.x + col));
+            if (p.extended && col >= pl.c_lo && col < pl.c_hi) pu[c] = __dmul_rn(a, __ldcg(p.u + (col - pl.c_lo)));
+          }
         }
-        const int cnt = (int)((hi - base) < 32 ? (hi - base) : 32);
-        ax = ordered_lane_sum(ax, px, cnt);
-        // entries outside J contribute +0.0, an exact no-op on the running sum
-        if (p.extended) au = ordered_lane_sum(au, pu, cnt);
+#pragma unroll
+        for (int c = 0; c < kPf; ++c) {
+          const int64_t b0 = base + 32 * c;
+          if (b0 < hi) {
+            const int cnt = (int)((hi - b0) < 32 ? (hi - b0) : 32);
+            ax = ordered_lane_sum(ax, px[c], cnt);
+            // entries outside J contribute +0.0, an exact no-op on the running sum
+            if (p.extended) au = ordered_lane_sum(au, pu[c], cnt);
+          }
+        }
+        base += 32 * kPf;
       }
       if (lane == 0) {
         double rv = __dsub_rn(ax, __ldg(p.b + i));
@@ -232,7 +273,9 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
         __stcg(p.r + (i - pl.r_lo), rv);
       }
     }
+    PROF(2);
     gsync();
+    PROF(3);
     // ---- Q(k)
     {
       const int64_t s0 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g];
@@ -240,12 +283,13 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
       for (int64_t sg = s0 + tid; sg < s1; sg += kCsrThreads) {
         const int j = p.rseg_col[sg];
         double acc = 0.0;
-        for (int64_t e = p.rseg_lo[sg]; e < p.rseg_hi[sg]; ++e)
-          acc = madd(acc, p.csc_val[e], __ldcg(p.r + (p.csc_row[e] - pl.r_lo)));
+        const int64_t e1 = p.rseg_ptr[sg + 1];
+        for (int64_t e = p.rseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.rval[e], __ldcg(p.r + p.rrow[e]));
         __stcg(p.x + j, __dsub_rn(__ldcg(p.x + j), __dmul_rn(rs, acc)));
       }
     }
     __syncthreads();
+    PROF(4);
     if (check_k) {
       if (oracle) {
         oracle_partial();
@@ -261,8 +305,11 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
         }
       }
     }
+    PROF(5);
     if (p.extended && k < p.k_end) compute_u(p.plan[k + 1 - p.k_begin]);
+    PROF(6);
     gsync();
+    PROF(7);
   }
 
   if (!finished) {
@@ -286,6 +333,9 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
       }
     }
   }
+  if (p.prof && tid == 0)
+    for (int i = 0; i < 8; ++i) p.prof[g * 16 + i] = prof_acc[i];
+#undef PROF
 }
 
 cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream) {

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int e0 = crank * sl;
     const int e1 = (e0 + sl < ne) ? e0 + sl : ne;
     const int nmy = e1 > e0 ? e1 - e0 : 0;
+    cpart += (seq & 1ull) * (size_t)NC * stride;  // two LL slots by sequence parity
     if (tid == 0) mbar_arrive_expect_tx(&xbar[0], (uint32_t)(CS * nmy * 8));
     const uint32_t in_base = smem_u32(s_in), bar0 = smem_u32(&xbar[0]);
     for (int e = tid; e < ne; e += kThreads) {

@@ -105,6 +105,12 @@ struct SplitParams {
   LLWord* zring;     // [D][zr_stride] {z_{k,i}, seq = k}
   double* zhist;     // [H][m]
   SplitShared* sh;
+  int32_t vec_off_c, vec_off_r;  // vector area base (doubles) of the column / row group
+  int32_t xmode;                 // bit 0 / bit 1: column / row group exchanges gather all entries (no broadcast)
+  int32_t pieces;                // TMA boxes per tile (1, or 2 row halves on separate mbarriers)
+  unsigned long long* trace;     // REBK_TRACE: [trace_n][G][4] globaltimer stamps of the exchange stages
+  int64_t trace_k0;
+  int32_t trace_n;
 };
 
 // Sparse (CSR + CSC twin) persistent kernel (rebk_csr.cu).
@@ -116,17 +122,21 @@ struct CsrParams {
   const int64_t* csc_ptr;  // [n+1]
   const int32_t* csc_row;
   const double* csc_val;
-  // per column block J: segments (row, [lo, hi) into the CSR arrays) sorted by row
+  // per column block J: the block's rows with nonzeros (sorted), each with a
+  // [ptr, ptr+1) range into compact copies of its entries (column order)
   const int64_t* cseg_off;  // [t+1]
   const int32_t* cseg_row;
-  const int64_t* cseg_lo;
-  const int64_t* cseg_hi;
+  const int64_t* cseg_ptr;  // [nseg+1] into cval / ccol
+  const double* cval;
+  const int32_t* ccol;      // column - c_lo
   const int64_t* cseg_cta;  // [t][G+1] first segment of each CTA's z-row slice
-  // per row block I: segments (col, [lo, hi) into the CSC arrays) sorted by column
+  // per row block I: the block's columns with nonzeros (sorted), each with a
+  // range into compact copies of its entries (row order)
   const int64_t* rseg_off;  // [s+1]
   const int32_t* rseg_col;
-  const int64_t* rseg_lo;
-  const int64_t* rseg_hi;
+  const int64_t* rseg_ptr;
+  const double* rval;
+  const int32_t* rrow;      // row - r_lo
   const int64_t* rseg_cta;  // [s][G+1] first segment of each CTA's x-column slice
   const double* b;
   const double* xs;
@@ -149,6 +159,7 @@ struct CsrParams {
   double res_scale;
   int32_t record;
   int32_t pad;
+  long long* prof;  // optional per-CTA phase cycle counters [G][16] (REBK_PROF=1)
 };
 
 struct SampleParams {
