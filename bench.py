@@ -339,13 +339,15 @@ def run_ours(args):
                        "kernel_path": ["rebk_dense_kernel", "rebk_dense_fast_kernel (cluster)",
                                        "rebk_dense_fast_kernel (cluster, cooperative)",
                                        "rebk_csr_kernel", "", "",
-                                       "rebk_dense_split_kernel (column/row groups)"][int(tr.kernel_path)]},
+                                       "rebk_dense_split_kernel (column/row groups)",
+                                       "rebk_dense_stream_kernel (TMA ring)"][int(tr.kernel_path)]},
             "time_to_tol_s": ms_max / args.steps / 1e3,
             "achieved_gbps": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": ["rebk_dense_kernel", "rebk_dense_fast_kernel", "rebk_dense_fast_kernel",
-                                    "rebk_csr_kernel", "", "", "rebk_dense_split_kernel"][int(tr.kernel_path)],
+                                    "rebk_csr_kernel", "", "", "rebk_dense_split_kernel",
+                                    "rebk_dense_stream_kernel"][int(tr.kernel_path)],
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_iter": bytes_per_iter,
                          "iters_per_launch": per_solve_iters, "kernel_ms_per_launch": kernel_ms},

@@ -111,6 +111,8 @@ int max_block(int64_t nb, const int64_t* ptr) {
   return (int)mx;
 }
 
+int env_int(const char* name, int dflt);
+
 bool blocks_even(int64_t nb, const int64_t* ptr) {
   for (int64_t b = 0; b < nb; ++b)
     if (ptr[b] & 1) return false;
@@ -315,6 +317,62 @@ FastGeometry split_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int NC, in
   const size_t need_r = f.vec_off_r + 2 * (size_t)f.pad_nC + common + cin_r;
   f.pad_cin = round_even((int)std::max(cin_c, cin_r));
   f.smem_bytes = std::max(need_c, need_r) * sizeof(double);
+  f.ok = f.smem_bytes <= (size_t)kSmemBudget;
+  return f;
+}
+
+// Streaming path geometry (rebk_dense_stream.cu): G CTAs, one per SM; the
+// vectors go after a ring of NS stages that takes the rest of the budget.
+struct StreamGeometry {
+  bool ok = false;
+  int G = 0, NS = 0, SD = 0, cw = 0, ch = 0, rw = 0, rh = 0, lc = 0, lr = 0;
+  int nR_max = 0, nC_max = 0, nJ_max = 0, nI_max = 0;
+  int pad_nC = 0, pad_nR = 0, pad_nJ = 0, pad_nI = 0;
+  size_t smem_bytes = 0;
+};
+
+int pow2floor_host(int v) {
+  int p = 1;
+  while (p * 2 <= v) p *= 2;
+  return p;
+}
+
+StreamGeometry stream_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int G, bool extended) {
+  StreamGeometry f;
+  f.G = G;
+  for (int q = 0; q < G; ++q) {
+    f.nR_max = std::max(f.nR_max, split_rows(ctx->m, G, q + 1) - split_rows(ctx->m, G, q));
+    f.nC_max = std::max(f.nC_max, split_even(ctx->n, G, q + 1) - split_even(ctx->n, G, q));
+  }
+  f.nI_max = max_block(cfg->n_row_blocks, cfg->row_ptr);
+  f.nJ_max = extended ? max_block(cfg->n_col_blocks, cfg->col_ptr) : 0;
+  f.pad_nC = round_even(f.nC_max + 1);
+  f.pad_nR = extended ? round_even(f.nR_max + 1) : 0;
+  f.pad_nJ = round_even(f.nJ_max + 2);  // + a leading column for odd block starts
+  f.pad_nI = round_even(f.nI_max + 1);
+  const size_t vec = 2 * (size_t)f.pad_nC + f.pad_nR + f.pad_nJ + f.pad_nI + 2 * 512;
+  const size_t budget = (size_t)kSmemBudget / 8;
+  if (vec + 4 * 1024 > budget) return f;  // z slice too large for the on-chip vectors
+  // two large stages measured best on C3 (profiles/r01_c3_stream.txt): HBM
+  // runs at its copy peak on the column passes with ~95 KB boxes
+  f.NS = std::max(2, std::min(kStreamMaxStages, env_int("REBK_STREAM_NS", 2)));
+  f.SD = (int)(((budget - vec) / f.NS) & ~(size_t)15);
+  const int hcap = std::max(1, std::min(256, env_int("REBK_STREAM_HCAP", 256)));
+  // boxes: widths <= 256 elements, even; heights so a box fills a stage and
+  // each row gets at least 8 lanes in the row dots (bank-conflict free)
+  auto width = [](int len) {
+    const int nsub = std::max(1, (len + 255) / 256);
+    return std::max(2, round_even((len + nsub - 1) / nsub));
+  };
+  if (extended) {
+    f.cw = width(f.nJ_max + (blocks_even(cfg->n_col_blocks, cfg->col_ptr) ? 0 : 1));
+    f.ch = std::max(1, std::min({f.SD / f.cw, hcap, std::max(1, f.nR_max)}));
+    f.lc = std::min(32, pow2floor_host(512 / f.ch));
+  }
+  f.rw = width(std::max(f.nC_max, 2));
+  f.rh = std::max(1, std::min({f.SD / f.rw, hcap, std::max(1, f.nI_max)}));
+  f.lr = std::min(32, pow2floor_host(512 / f.rh));
+  f.smem_bytes = ((size_t)f.NS * f.SD + vec) * sizeof(double);
   f.ok = f.smem_bytes <= (size_t)kSmemBudget;
   return f;
 }
@@ -734,7 +792,10 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   {
     const int CS = env_int("REBK_CLUSTER", 8);
     const bool aligned = (ctx->lda % 2 == 0) && ((uintptr_t)ctx->A % 16 == 0);
-    if (env_int("REBK_NO_FAST", 0) == 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY && aligned && CS >= 1 &&
+    // TMA boxes start on 16-byte aligned columns: the clustered kernels need
+    // even column-block starts (the streaming kernel handles odd ones)
+    const bool even_cols = !extended || blocks_even(cfg->n_col_blocks, cfg->col_ptr);
+    if (env_int("REBK_NO_FAST", 0) == 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY && aligned && even_cols && CS >= 1 &&
         G0 >= CS && encode_fn() != nullptr) {
       int NC = std::max(1, G0 / CS);
       for (int attempt = 0; attempt < 3 && NC >= 1; ++attempt) {
@@ -781,7 +842,25 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
       use_fast = encode_box(&tm_ct, ctx, fg.ct_box_w, fg.ct_box_h) && encode_box(&tm_rt, ctx, fg.rt_box_w, fg.rt_box_h);
     }
   }
-  const int G = use_fast ? fg.G : geo.G;
+  // streaming path: blocks whose per-CTA slices the general kernel cannot
+  // stage in shared memory (C3) stream through a TMA ring instead
+  bool use_stream = false;
+  StreamGeometry stg;
+  CUtensorMap tm_sc, tm_sr;
+  const int stream_env = env_int("REBK_STREAM", 1);  // 0 off, 1 when the general kernel cannot stage, 2 always
+  if (!use_fast && stream_env != 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY &&
+      (ctx->lda % 2 == 0) && ((uintptr_t)ctx->A % 16 == 0) && encode_fn() != nullptr &&
+      (stream_env == 2 || !geo.stage_rt || (extended && !geo.stage_ct))) {
+    stg = stream_geometry(ctx, cfg, std::min(G0, ctx->sm_count), extended);
+    int occs = 0;
+    if (stg.ok && stream_kernel_occupancy(stg.smem_bytes, &occs) == cudaSuccess && occs >= 1 &&
+        (!extended || encode_box(&tm_sc, ctx, stg.cw, stg.ch)) && encode_box(&tm_sr, ctx, stg.rw, stg.rh)) {
+      use_stream = true;
+      if (!extended) tm_sc = tm_sr;
+    }
+    cudaGetLastError();
+  }
+  const int G = use_fast ? fg.G : (use_stream ? stg.G : geo.G);
 
   DevArena arena;
   arena.stream = stream;
@@ -986,6 +1065,22 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
           fast_coop = false;
           err = launch_dense_fast(fpar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
         }
+      } else if (use_stream) {
+        StreamParams spar{};
+        spar.d = p;
+        spar.stages = stg.NS;
+        spar.stage_doubles = stg.SD;
+        spar.cw = stg.cw;
+        spar.ch = stg.ch;
+        spar.rw = stg.rw;
+        spar.rh = stg.rh;
+        spar.lc = stg.lc;
+        spar.lr = stg.lr;
+        spar.pad_nC = stg.pad_nC;
+        spar.pad_nR = stg.pad_nR;
+        spar.pad_nJ = stg.pad_nJ;
+        spar.pad_nI = stg.pad_nI;
+        err = launch_dense_stream(spar, tm_sc, tm_sr, G, stg.smem_bytes, stream);
       } else {
         err = launch_dense(p, G, geo.smem_bytes, stream);
       }
@@ -1030,7 +1125,9 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     int khz = 0;
     cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx->device);
     const double it = (double)std::max<int64_t>(1, ctl.iters);
-    fprintf(stderr, "[rebk prof] path=%s ncc=%d ", use_split ? "split" : (use_fast ? (fast_coop ? "fast(coop)" : "fast") : "v1"), split_ncc);
+    fprintf(stderr, "[rebk prof] path=%s ncc=%d ",
+            use_split ? "split" : (use_fast ? (fast_coop ? "fast(coop)" : "fast") : (use_stream ? "stream" : "v1")),
+            split_ncc);
     fprintf(stderr, "[rebk prof] G=%d iters=%lld loop=%.3f ms (%.3f us/iter); per-iteration us: mark mean max\n", G,
             (long long)ctl.iters, ms, 1e3 * ms / it);
     print_prof(h, G, use_split ? split_ncc * fg.CS : G, khz, it);
@@ -1043,7 +1140,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     trace->loop_ms = ms;
     trace->n_checks = ctl.n_checks;
     trace->grid_ctas = G;
-    trace->kernel_path = use_split ? 6 : (use_fast ? (fast_coop ? 2 : 1) : 0);
+    trace->kernel_path = use_split ? 6 : (use_fast ? (fast_coop ? 2 : 1) : (use_stream ? 7 : 0));
   }
   return REBK_OK;
 }

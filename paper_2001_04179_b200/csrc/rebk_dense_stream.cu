@@ -1,0 +1,448 @@
+// rebk_dense_stream.cu — REBK for dense fp64 problems whose per-CTA block
+// slices do not fit in shared memory (C3: 200000 x 10000, |J| = 500, |I| = 1000:
+// a CTA's slice of the column block is ~1350 rows x 500 = 5.4 MB).
+//
+// Same iteration, ownership and reductions as rebk_dense.cu (step_rebk,
+// solvers.py:324-337; P1..P5 with 4 grid barriers; partial sums stored
+// transposed and summed in fixed order, so runs replay bit for bit).  What
+// changes is the data movement: every pass over a block is a stream of TMA
+// boxes through a ring of NS shared-memory stages, each on its own mbarrier.
+// The chunk sequence of a whole run is known in advance (the block plan), so
+// thread 0 keeps NS boxes in flight across phases and grid barriers: while a
+// CTA waits at a barrier, the first boxes of the next pass are already
+// landing.  Per iteration each CTA streams
+//   C1  its rows of A[:, J]  (u partials, column sums)          HBM
+//   C2  the same rows again  (z -= s_J A_J u, row dots)          HBM (800 MB does not stay in L2)
+//   R1  A[I, its columns]    (r partials, row dots)              HBM
+//   R2  the same again       (x -= s_I A_Iᵀ r, column sums)      L2  (80 MB, just read by R1)
+// so the column block is read twice: the HBM floor is ~1.68 GB per C3
+// iteration, 0.52 of the "blocks read once" algorithmic figure.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rebk_device.cuh"
+#include "rebk_internal.h"
+
+namespace rebk {
+
+constexpr int kStreamThreads = 512;
+constexpr int kStreamWarps = kStreamThreads / 32;
+
+// position in the run's box sequence: iteration k, phase (0 C1, 1 C2, 2 R1,
+// 3 R2), box index i within the phase
+struct Cursor {
+  int64_t k;
+  int ph;
+  int i;
+};
+
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    rebk_dense_stream_kernel(const __grid_constant__ StreamParams sp, const __grid_constant__ CUtensorMap tm_c,
+                             const __grid_constant__ CUtensorMap tm_r) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t sbar[kStreamMaxStages];
+  __shared__ double s_bcast[2];
+
+  const DenseParams& p = sp.d;
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  Control* ctl = p.ctl;
+  if (*((volatile int32_t*)&ctl->done)) return;
+
+  const int zr0 = split_rows(p.m, G, g), zr1 = split_rows(p.m, G, g + 1);
+  const int xq0 = split_even(p.n, G, g), xq1 = split_even(p.n, G, g + 1);
+  const int nR = zr1 - zr0, nC = xq1 - xq0;
+  const int NS = sp.stages, SD = sp.stage_doubles;
+  const int cw = sp.cw, ch = sp.ch, rw = sp.rw, rh = sp.rh;
+
+  double* s_x = sm + (size_t)NS * SD;
+  double* s_xs = s_x + sp.pad_nC;
+  double* s_z = s_xs + sp.pad_nC;
+  double* s_u = s_z + sp.pad_nR;
+  double* s_r = s_u + sp.pad_nJ;
+  double* s_red = s_r + sp.pad_nI;  // 2 * kStreamThreads
+
+  for (int c = tid; c < nC; c += kStreamThreads) {
+    s_x[c] = __ldcg(p.x + xq0 + c);
+    s_xs[c] = p.xs ? __ldg(p.xs + xq0 + c) : 0.0;
+  }
+  if (p.extended)
+    for (int r = tid; r < nR; r += kStreamThreads) s_z[r] = __ldcg(p.z + zr0 + r);
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&sbar[s], 1);
+    fence_mbar_init();
+    prefetch_tensormap(&tm_c);
+    prefetch_tensormap(&tm_r);
+  }
+  __syncthreads();
+
+  unsigned long long bar_target = 0;
+  auto gsync = [&]() {
+    bar_target += (unsigned long long)G;
+    grid_barrier(&ctl->bar, bar_target);
+  };
+
+  // ---- the box sequence (identical walk on the producer and consumer side)
+  auto plan_of = [&](int64_t k) -> const Plan& { return p.plan[k - p.k_begin]; };
+  auto cdiv = [](int a, int b) { return (a + b - 1) / b; };
+  // TMA box columns start 16-byte aligned: a column block that starts on an
+  // odd column is loaded from the even column before it (span = nJ + 1, the
+  // extra leading column is weighted by zero / dropped)
+  auto span_c = [](const Plan& pl) { return pl.c_hi - pl.c_lo + (pl.c_lo & 1); };
+  auto boxes = [&](int64_t k, int ph) -> int {
+    const Plan& pl = plan_of(k);
+    if (ph < 2) {
+      if (!p.extended || nR <= 0) return 0;
+      return cdiv(span_c(pl), cw) * cdiv(nR, ch);
+    }
+    if (nC <= 0) return 0;
+    return cdiv(pl.r_hi - pl.r_lo, rh) * cdiv(nC, rw);
+  };
+  // skip empty phases; k > k_end means the walk is over
+  auto settle = [&](Cursor& c) {
+    while (c.k <= p.k_end && c.i >= boxes(c.k, c.ph)) {
+      c.i = 0;
+      if (++c.ph == 4) {
+        c.ph = 0;
+        ++c.k;
+      }
+    }
+  };
+  auto issue = [&](const Cursor& c, int stage) {  // thread 0
+    const Plan& pl = plan_of(c.k);
+    fence_proxy_async();
+    double* dst = sm + (size_t)stage * SD;
+    if (c.ph < 2) {
+      const int nsc = cdiv(span_c(pl), cw), nrc = cdiv(nR, ch);
+      // C1 walks subtile-major (column sums accumulate down the rows),
+      // C2 row-chunk-major (row dots accumulate across the subtiles)
+      const int s = c.ph == 0 ? c.i / nrc : c.i % nsc;
+      const int rc = c.ph == 0 ? c.i % nrc : c.i / nsc;
+      mbar_arrive_expect_tx(&sbar[stage], (uint32_t)(cw * ch * 8));
+      tma_load_2d(dst, &tm_c, (pl.c_lo & ~1) + s * cw, zr0 + rc * ch, &sbar[stage]);
+    } else {
+      const int nsr = cdiv(nC, rw), nrr = cdiv(pl.r_hi - pl.r_lo, rh);
+      // R1 row-chunk-major (row dots), R2 subtile-major (column sums)
+      const int s = c.ph == 2 ? c.i % nsr : c.i / nrr;
+      const int rr = c.ph == 2 ? c.i / nsr : c.i % nrr;
+      mbar_arrive_expect_tx(&sbar[stage], (uint32_t)(rw * rh * 8));
+      tma_load_2d(dst, &tm_r, xq0 + s * rw, pl.r_lo + rr * rh, &sbar[stage]);
+    }
+  };
+  Cursor prod{p.k_begin, 0, 0};
+  int64_t produced = 0, consumed = 0;
+  auto refill = [&]() {  // thread 0: keep NS boxes in flight
+    if (tid != 0) return;
+    settle(prod);
+    while (prod.k <= p.k_end && produced < consumed + NS) {
+      issue(prod, (int)(produced % NS));
+      ++produced;
+      ++prod.i;
+      settle(prod);
+    }
+  };
+  // consumer: wait for the next box, hand it to f, release its stage
+  auto take = [&](auto f) {
+    const int stage = (int)(consumed % NS);
+    mbar_wait(&sbar[stage], (uint32_t)((consumed / NS) & 1));
+    f(sm + (size_t)stage * SD);
+    __syncthreads();  // every reader of this stage is done
+    ++consumed;
+    refill();
+  };
+
+  const bool checking = p.stop_mode != 2;
+  auto oracle_partial = [&]() {
+    double acc = 0.0;
+    for (int c = tid; c < nC; c += kStreamThreads) {
+      const double d = s_x[c] - s_xs[c];
+      acc = fma(d, d, acc);
+    }
+    const double s = block_sum<kStreamThreads>(acc, s_red);
+    if (tid == 0) __stcg(p.errpart + g, s);
+  };
+  auto decide = [&](int64_t k) -> bool {
+    if (warp == 0) {
+      const double s = warp_sum_cg(p.errpart, G);
+      if (lane == 0) s_bcast[0] = s;
+    }
+    __syncthreads();
+    const double err = sqrt(s_bcast[0]);
+    const bool conv = err <= p.tol;
+    if (g == 0 && tid == 0) {
+      const int64_t nc = ctl->n_checks;
+      if (p.record && nc < p.errs_cap) p.errs[nc] = err;
+      ctl->n_checks = nc + 1;
+      ctl->final_error = err;
+      ctl->has_error = 1;
+      if (conv) {
+        ctl->converged = 1;
+        ctl->iters = k;
+        ctl->done = 1;
+      }
+    }
+    __syncthreads();
+    return conv;
+  };
+
+  // Column sums of a box stream, subtile by subtile: out(c, Σ_r T[r][c] v[r])
+  // for the C columns of subtile s; box rc holds rows [rc*bh, rc*bh + bh).
+  // Threads own column pairs (cp) and a row residue (rg); the RG partials are
+  // summed in fixed order through s_red.
+  auto colsum_stream = [&](int C, int R, int bw, int bh, const double* v, auto out) {
+    const int nsub = cdiv(C, bw), nrc = cdiv(R, bh);
+    for (int s = 0; s < nsub; ++s) {
+      const int Cs = min(bw, C - s * bw);
+      const int CP = (Cs + 1) >> 1;
+      int RG = kStreamThreads / CP;
+      if (RG > bh) RG = bh;
+      const int cp = tid % CP, rg = tid / CP;
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+      for (int rc = 0; rc < nrc; ++rc) {
+        const int Rb = min(bh, R - rc * bh);
+        const double* vb = v + rc * bh;
+        take([&](const double* T) {
+          if (rg < RG) {
+            const double* col = T + 2 * cp;
+            int r = rg;
+            for (; r + RG < Rb; r += 2 * RG) {
+              const double2 t0 = *reinterpret_cast<const double2*>(col + (size_t)r * bw);
+              const double2 t1 = *reinterpret_cast<const double2*>(col + (size_t)(r + RG) * bw);
+              const double v0 = vb[r], v1 = vb[r + RG];
+              a0.x = fma(t0.x, v0, a0.x);
+              a0.y = fma(t0.y, v0, a0.y);
+              a1.x = fma(t1.x, v1, a1.x);
+              a1.y = fma(t1.y, v1, a1.y);
+            }
+            if (r < Rb) {
+              const double2 t0 = *reinterpret_cast<const double2*>(col + (size_t)r * bw);
+              const double v0 = vb[r];
+              a0.x = fma(t0.x, v0, a0.x);
+              a0.y = fma(t0.y, v0, a0.y);
+            }
+          }
+        });
+      }
+      if (rg < RG) {
+        s_red[rg * 2 * CP + 2 * cp] = a0.x + a1.x;
+        s_red[rg * 2 * CP + 2 * cp + 1] = a0.y + a1.y;
+      }
+      __syncthreads();
+      for (int c = tid; c < Cs; c += kStreamThreads) {
+        double acc = 0.0;
+        for (int q = 0; q < RG; ++q) acc += s_red[q * 2 * CP + c];
+        out(s * bw + c, acc);
+      }
+      __syncthreads();
+    }
+  };
+  // Row dots of a box stream, row chunk by row chunk: out(r, Σ_c T[r][c] v[c])
+  // over all subtiles of the row; L lanes per row (bh * L <= threads), the
+  // accumulators carry across the subtiles of a row chunk.
+  auto rowdot_stream = [&](int C, int R, int bw, int bh, int L, const double* v, auto out) {
+    const int nsub = cdiv(C, bw), nrc = cdiv(R, bh);
+    const int sub = tid % L, rsub = tid / L;
+    for (int rc = 0; rc < nrc; ++rc) {
+      const int Rb = min(bh, R - rc * bh);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (int s = 0; s < nsub; ++s) {
+        const int Cs = min(bw, C - s * bw);
+        const int CPf = Cs >> 1;
+        const double* vs = v + s * bw;
+        take([&](const double* T) {
+          if (rsub < Rb) {
+            const double2* row = reinterpret_cast<const double2*>(T + (size_t)rsub * bw);
+            const double2* v2 = reinterpret_cast<const double2*>(vs);
+            int q = sub;
+            for (; q + L < CPf; q += 2 * L) {
+              const double2 t0 = row[q], t1 = row[q + L];
+              const double2 w0 = v2[q], w1 = v2[q + L];
+              a0 = fma(t0.x, w0.x, a0);
+              a1 = fma(t0.y, w0.y, a1);
+              a2 = fma(t1.x, w1.x, a2);
+              a3 = fma(t1.y, w1.y, a3);
+            }
+            if (q < CPf) {
+              const double2 t0 = row[q], w0 = v2[q];
+              a0 = fma(t0.x, w0.x, a0);
+              a1 = fma(t0.y, w0.y, a1);
+            }
+            if ((Cs & 1) && sub == (CPf % L)) a2 = fma(T[(size_t)rsub * bw + Cs - 1], vs[Cs - 1], a2);
+          }
+        });
+      }
+      double acc = (a0 + a1) + (a2 + a3);
+      for (int off = L / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (sub == 0 && rsub < Rb) out(rc * bh + rsub, acc);
+      // out() writes are ordered before later readers by the next take()'s barrier
+    }
+  };
+
+  long long prof_acc[16];
+  for (int i = 0; i < 16; ++i) prof_acc[i] = 0;
+  long long prof_last = clock64();
+#define PROF(i)                          \
+  if (p.prof) {                          \
+    const long long _t = clock64();      \
+    prof_acc[i] += _t - prof_last;       \
+    prof_last = _t;                      \
+  }
+  bool finished = false;
+  if (p.k_begin == 1 && checking) {
+    oracle_partial();
+    gsync();
+    if (decide(0)) finished = true;
+  }
+  if (!finished) refill();
+
+  bool pending = false;
+  int64_t pending_k = 0;
+  int64_t k = p.k_begin;
+  for (; !finished && k <= p.k_end; ++k) {
+    const Plan pl = plan_of(k);
+    const int nJ = pl.c_hi - pl.c_lo, nI = pl.r_hi - pl.r_lo;
+    const int co = pl.c_lo & 1, W = nJ + co;  // column span of the boxes
+    const int rl = pl.r_lo;
+    const bool check_k = checking && (k % p.stride == 0);
+    PROF(0);
+    if (p.extended) {
+      // C1: partial u over owned rows -> upart[e * G + g]
+      if (nR > 0)
+        colsum_stream(W, nR, cw, ch, s_z, [&](int c, double val) {
+          if (c >= co) __stcg(p.upart + (int64_t)(c - co) * G + g, val);
+        });
+      else
+        for (int c = tid; c < nJ; c += kStreamThreads) __stcg(p.upart + (int64_t)c * G + g, 0.0);
+      PROF(1);
+      gsync();
+      PROF(2);
+      if (pending) {
+        pending = false;
+        if (decide(pending_k)) {
+          finished = true;
+          break;
+        }
+      }
+      for (int e = g * kStreamWarps + warp; e < nJ; e += G * kStreamWarps) {
+        const double s = warp_sum_cg(p.upart + (int64_t)e * G, G);
+        if (lane == 0) __stcg(p.u + e, s);
+      }
+      PROF(3);
+      gsync();
+      PROF(4);
+      // C2: z[zr] -= s_J · A[zr, J] u
+      for (int c = tid; c < W; c += kStreamThreads) s_u[c] = c < co ? 0.0 : __ldcg(p.u + c - co);
+      __syncthreads();
+      const double cs = pl.c_scale;
+      if (nR > 0)
+        rowdot_stream(W, nR, cw, ch, sp.lc, s_u, [&](int r, double acc) {
+          const double zn = s_z[r] - cs * acc;
+          s_z[r] = zn;
+          __stcg(p.z + zr0 + r, zn);
+        });
+      PROF(5);
+    }
+    // R1: partial r over owned columns -> rpart[e * G + g]
+    if (nC > 0)
+      rowdot_stream(nC, nI, rw, rh, sp.lr, s_x, [&](int r, double acc) { __stcg(p.rpart + (int64_t)r * G + g, acc); });
+    else
+      for (int r = tid; r < nI; r += kStreamThreads) __stcg(p.rpart + (int64_t)r * G + g, 0.0);
+    PROF(6);
+    gsync();
+    PROF(7);
+    if (!p.extended && pending) {
+      pending = false;
+      if (decide(pending_k)) {
+        finished = true;
+        break;
+      }
+    }
+    for (int e = g * kStreamWarps + warp; e < nI; e += G * kStreamWarps) {
+      const double s = warp_sum_cg(p.rpart + (int64_t)e * G, G);
+      if (lane == 0) {
+        double rv = s - __ldg(p.b + rl + e);
+        if (p.extended) rv += __ldcg(p.z + rl + e);
+        __stcg(p.r + e, rv);
+      }
+    }
+    PROF(8);
+    gsync();
+    PROF(9);
+    // R2: x[xq] -= s_I · A[I, xq]ᵀ r
+    for (int c = tid; c < nI; c += kStreamThreads) s_r[c] = __ldcg(p.r + c);
+    __syncthreads();
+    const double rs = pl.r_scale;
+    if (nC > 0) colsum_stream(nC, nI, rw, rh, s_r, [&](int c, double acc) { s_x[c] = s_x[c] - rs * acc; });
+    __syncthreads();
+    PROF(10);
+    if (check_k) {
+      oracle_partial();
+      pending = true;
+      pending_k = k;
+    }
+  }
+  if (!finished) {
+    if (pending) {
+      gsync();
+      if (decide(pending_k)) finished = true;
+    }
+    if (!finished && p.k_end == p.max_iters) {
+      if (checking && (p.max_iters % p.stride) != 0) {
+        oracle_partial();
+        gsync();
+        decide(p.max_iters);
+      }
+      if (g == 0 && tid == 0) {
+        if (!ctl->converged) ctl->iters = p.max_iters;
+        ctl->done = 1;
+      }
+    }
+  }
+  if (p.prof && tid == 0)
+    for (int i = 0; i < 16; ++i) p.prof[g * 16 + i] = prof_acc[i];
+#undef PROF
+  for (int c = tid; c < nC; c += kStreamThreads) __stcg(p.x + xq0 + c, s_x[c]);
+  if (p.extended)
+    for (int r = tid; r < nR; r += kStreamThreads) __stcg(p.z + zr0 + r, s_z[r]);
+  // boxes issued for iterations past a stop are still landing: drain them
+  while (consumed < produced) {
+    mbar_wait(&sbar[consumed % NS], (uint32_t)((consumed / NS) & 1));
+    ++consumed;
+  }
+  __syncthreads();
+}
+
+static cudaError_t set_stream_attrs() {
+  static int configured_device = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (configured_device == dev) return cudaSuccess;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(rebk_dense_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+  if (e == cudaSuccess) configured_device = dev;
+  return e;
+}
+
+cudaError_t stream_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm) {
+  cudaError_t e = set_stream_attrs();
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, rebk_dense_stream_kernel, kStreamThreads,
+                                                       smem_bytes);
+}
+
+cudaError_t launch_dense_stream(const StreamParams& sp, const CUtensorMap& tm_c, const CUtensorMap& tm_r, int G,
+                                size_t smem_bytes, cudaStream_t stream) {
+  cudaError_t e = set_stream_attrs();
+  if (e != cudaSuccess) return e;
+  StreamParams spc = sp;
+  CUtensorMap a = tm_c, b = tm_r;
+  void* args[] = {&spc, &a, &b};
+  return cudaLaunchCooperativeKernel((const void*)rebk_dense_stream_kernel, dim3(G), dim3(kStreamThreads), args,
+                                     smem_bytes, stream);
+}
+
+}  // namespace rebk

@@ -113,6 +113,18 @@ struct SplitParams {
   int32_t trace_n;
 };
 
+// Streaming path for blocks too large for shared memory (rebk_dense_stream.cu):
+// every pass streams TMA boxes through a ring of `stages` shared-memory stages.
+constexpr int kStreamMaxStages = 8;
+struct StreamParams {
+  DenseParams d;
+  int32_t stages, stage_doubles;  // ring geometry (stage_doubles % 16 == 0)
+  int32_t cw, ch;                 // column-block box: cw columns x ch rows
+  int32_t rw, rh;                 // row-block box: rw columns x rh rows
+  int32_t lc, lr;                 // lanes per row in the row dots (ch * lc, rh * lr <= 512)
+  int32_t pad_nC, pad_nR, pad_nJ, pad_nI;  // vector areas after the ring (doubles, even)
+};
+
 // Sparse (CSR + CSC twin) persistent kernel (rebk_csr.cu).
 struct CsrParams {
   int32_t m, n;
@@ -201,6 +213,9 @@ cudaError_t fast_max_clusters(int cluster_size, size_t smem_bytes, int* clusters
 cudaError_t split_max_clusters(int cluster_size, size_t smem_bytes, int* clusters);
 cudaError_t launch_dense_split(const SplitParams& sp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
                                int cluster_size, size_t smem_bytes, cudaStream_t stream, bool cooperative);
+cudaError_t launch_dense_stream(const StreamParams& sp, const CUtensorMap& tm_c, const CUtensorMap& tm_r, int G,
+                                size_t smem_bytes, cudaStream_t stream);
+cudaError_t stream_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
 cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream);
 cudaError_t csr_kernel_occupancy(int* blocks_per_sm);
 struct MrhsRun {

@@ -449,3 +449,70 @@ def test_split_path_small_ring_and_chunk_edges(monkeypatch):
                           stop=P.StoppingRule(mode="max_iters_only"), beta_max=cfg.beta_max)
     t2 = P.run(prob, cfg2)
     assert t2.iters == 100 and rel(t2.x, g["x_100"]) <= RTOL and rel(t2.z, g["z_100"]) <= RTOL
+
+
+@pytest.mark.parametrize("grid", ["0", "7"])
+def test_stream_path_matches_reference_c1(monkeypatch, grid):
+    """The streaming kernel (TMA ring, used when block slices exceed shared
+    memory, e.g. C3) forced onto C1: ITER, x, z as the reference, bitwise
+    replay; with 7 CTAs each column slice is ~286 rows = 13 ring boxes."""
+    monkeypatch.setenv("REBK_NO_FAST", "1")
+    monkeypatch.setenv("REBK_STREAM", "2")
+    if grid != "0":
+        monkeypatch.setenv("REBK_GRID", grid)
+    g, a, prob, cfg = c1_instance()
+    t1 = P.run(prob, cfg)
+    t2 = P.run(prob, cfg)
+    assert t1.kernel_path == 7
+    k = int(g["iters"])
+    assert t1.converged and t1.iters == k
+    assert rel(t1.x, g[f"x_{k}"]) <= RTOL and rel(t1.z, g[f"z_{k}"]) <= RTOL
+    assert np.array_equal(t1.x, t2.x) and np.array_equal(t1.z, t2.z)
+
+
+@pytest.mark.parametrize("algorithm", ["rebk", "rabk", "rk", "rek"])
+def test_stream_path_ragged_blocks_and_algorithms(monkeypatch, algorithm):
+    """Ragged partitions (odd block widths, a short last block), an odd n,
+    stride 3 and max_iters cut-off on the streaming kernel vs the oracle."""
+    monkeypatch.setenv("REBK_NO_FAST", "1")
+    monkeypatch.setenv("REBK_STREAM", "2")
+    rs = np.random.default_rng(5)
+    m, n = 701, 333
+    a = rs.standard_normal((m, n))
+    xs = rs.standard_normal(n)
+    b = a @ xs + 0.01 * rs.standard_normal(m)
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=b, x_star=np.linalg.lstsq(a, b, rcond=None)[0],
+                             b_perp=None, meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    single = algorithm in ("rek", "rk")
+    rp = P.contiguous_partition(m, 1 if single else 97, "row")
+    cp = P.contiguous_partition(n, 1 if single else 61, "col")
+    cfg = P.SolverConfig(algorithm=algorithm, alpha=1.0 if single else 0.7, seed=3, max_iters=400,
+                         row_partition=rp, col_partition=cp, stop=P.StoppingRule(tol=1e-9, check_stride=3),
+                         beta_max=1.0)
+    t = P.run(prob, cfg)
+    assert t.kernel_path == 7
+    rp_ptr = np.arange(m + 1) if single else np.array(list(range(0, m, 97)) + [m])
+    cp_ptr = np.arange(n + 1) if single else np.array(list(range(0, n, 61)) + [n])
+    orc = OracleSolver(a, b, rp_ptr, cp_ptr, cfg.alpha, algorithm=algorithm)
+    res = orc.run(3, 400, 1e-9, prob.x_star, stride=3)
+    assert res["iters"] == t.iters and res["converged"] == t.converged
+    assert rel(t.x, res["x"]) <= 1e-10
+    if algorithm in ("rebk", "rek"):
+        assert rel(t.z, res["z"]) <= 1e-10
+
+
+def test_odd_column_block_starts_take_a_safe_path():
+    """Column blocks of 99 (odd starts): the clustered kernels need 16-byte
+    aligned TMA starts and must not be chosen; the result still matches the
+    oracle."""
+    g, a, prob, _ = c1_instance()
+    rp, cp = P.contiguous_partition(2000, 100, "row"), P.contiguous_partition(500, 99, "col")
+    cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=int(g["seed"]), max_iters=300,
+                         row_partition=rp, col_partition=cp, stop=P.StoppingRule(mode="max_iters_only"),
+                         beta_max=float(g["beta"]))
+    t = P.run(prob, cfg)
+    assert t.kernel_path in (0, 7)
+    orc = OracleSolver(a, g["b"], np.arange(0, 2001, 100), np.array(list(range(0, 500, 99)) + [500]),
+                       float(g["alpha"]))
+    res = orc.run(int(g["seed"]), 300, 0.0, None, mode="max_iters_only")
+    assert rel(t.x, res["x"]) <= RTOL and rel(t.z, res["z"]) <= RTOL
