@@ -211,3 +211,94 @@ def build(name: str, **kw) -> Workload:
         return Workload("c4", prob, rp, cp, kw.pop("alpha_factor", 1.0) / beta, beta, kw.pop("rel_tol", 1e-6),
                         kw.pop("seed", 17))
     raise KeyError(f"unknown workload {name!r}")
+
+
+@dataclass
+class DeviceWorkload:
+    """A dense instance that lives in device memory only (C3: 16 GB).  The
+    block weights, cumulative sums and scales are computed on the device and
+    handed to the C-ABI in the reference's layout (SolverContext fields)."""
+
+    name: str
+    a: "object"  # torch.Tensor (m, n) float64, row-major
+    b: "object"
+    x_star: "object"
+    row_ptr: np.ndarray
+    col_ptr: np.ndarray
+    row_w: np.ndarray
+    col_w: np.ndarray
+    alpha: float
+    beta_max: float
+    rel_tol: float = 1e-6
+    seed: int = 17
+
+    @property
+    def shape(self):
+        return tuple(self.a.shape)
+
+    @property
+    def algorithmic_bytes_per_iter(self) -> float:
+        m, n = self.shape
+        return 8.0 * (m * int(np.diff(self.col_ptr).max()) + int(np.diff(self.row_ptr).max()) * n)
+
+    def cfg(self, stop_mode: str, tol: float, max_iters: int):
+        """rebk_cfg with the same fields SolverContext.make_cfg fills."""
+        from . import _lib
+
+        c = _lib.RebkCfg()
+        c.algorithm = _lib.ALGO_CODES["rebk"]
+        c.stop_mode = _lib.STOP_CODES[stop_mode]
+        c.tol = float(tol)
+        c.check_stride = 1
+        c.max_iters = int(max_iters)
+        k = _lib.philox_key(self.seed)
+        c.philox_key[0], c.philox_key[1] = int(k[0]), int(k[1])
+        self._keep = [np.ascontiguousarray(v) for v in (self.row_ptr, np.cumsum(self.row_w), self.alpha / self.row_w,
+                                                        self.col_ptr, np.cumsum(self.col_w), self.alpha / self.col_w)]
+        rp, rc, rs, cp, cc, cs = self._keep
+        c.n_row_blocks = len(rp) - 1
+        c.row_ptr, c.row_cum, c.row_total, c.row_scale = _lib.i64ptr(rp), _lib.dptr(rc), float(rc[-1]), _lib.dptr(rs)
+        c.n_col_blocks = len(cp) - 1
+        c.col_ptr, c.col_cum, c.col_total, c.col_scale = _lib.i64ptr(cp), _lib.dptr(cc), float(cc[-1]), _lib.dptr(cs)
+        return c
+
+
+def c3_device(m: int = 200000, n: int = 10000, tau_row: int = 1000, tau_col: int = 500, seed: int = 0,
+              device: int = 0) -> DeviceWorkload:
+    """BASELINE config 3 built on the GPU with torch (16 GB does not round-trip
+    through the host): A = randn(m, n), x* = randn(n), r = (I - A A†) randn(m)
+    scaled to 0.1 ||A x*||, b = A x* + r, x* = A†b by Cholesky of AᵀA.
+    Seeded torch Philox stands in for the reference's numpy stream (SURVEY
+    §8(d.1) C3 gives the same shapes and distributions; ITER differs from its
+    576 by the instance).  beta_max from block Gram eigenvalues on device."""
+    import torch
+
+    from .matrix import DeviceMatrix
+
+    dev = torch.device("cuda", device)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    a = torch.randn(m, n, dtype=torch.float64, device=dev, generator=g)
+    xs = torch.randn(n, dtype=torch.float64, device=dev, generator=g)
+    w = torch.randn(m, dtype=torch.float64, device=dev, generator=g)
+    chol = torch.linalg.cholesky(a.T @ a)
+    ax = a @ xs
+    r = w - a @ torch.cholesky_solve((a.T @ w)[:, None], chol)[:, 0]
+    r *= 0.1 * ax.norm() / r.norm()
+    b = ax + r
+    x_star = torch.cholesky_solve((a.T @ b)[:, None], chol)[:, 0]
+    del chol, ax, r, w
+    row_ptr = np.array(list(range(0, m, tau_row)) + [m], dtype=np.int64)
+    col_ptr = np.array(list(range(0, n, tau_col)) + [n], dtype=np.int64)
+    dm = DeviceMatrix.from_device_pointer(a.data_ptr(), m, n, n, device)
+    row_w = dm.block_frobenius_sq(0, row_ptr)
+    col_w = dm.block_frobenius_sq(1, col_ptr)
+    dm.close()
+    beta = 0.0
+    for lo, hi, wt in zip(row_ptr[:-1], row_ptr[1:], row_w):
+        blk = a[lo:hi]
+        beta = max(beta, float(torch.linalg.eigvalsh(blk @ blk.T)[-1]) / wt)
+    for lo, hi, wt in zip(col_ptr[:-1], col_ptr[1:], col_w):
+        blk = a[:, lo:hi]
+        beta = max(beta, float(torch.linalg.eigvalsh(blk.T @ blk)[-1]) / wt)
+    torch.cuda.synchronize(dev)
+    return DeviceWorkload("c3", a, b, x_star, row_ptr, col_ptr, row_w, col_w, 1.0 / beta, beta)

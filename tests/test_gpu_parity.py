@@ -516,3 +516,33 @@ def test_odd_column_block_starts_take_a_safe_path():
                        float(g["alpha"]))
     res = orc.run(int(g["seed"]), 300, 0.0, None, mode="max_iters_only")
     assert rel(t.x, res["x"]) <= RTOL and rel(t.z, res["z"]) <= RTOL
+
+
+@pytest.mark.slow
+def test_c3_full_size_matches_oracle():
+    """BASELINE config 3 at full size (200000 x 10000, 16 GB, built on the
+    device): the streaming kernel's run to ||x - x*|| <= 1e-6 ||x*|| against
+    the oracle on the same instance: ITER equal, x and z within 1e-10."""
+    import torch
+
+    from oracle.rebk_oracle import NumpyRng
+    from paper_2001_04179_b200.matrix import DeviceMatrix
+    from paper_2001_04179_b200.workloads import c3_device
+
+    wl = c3_device()
+    m, n = wl.shape
+    dm = DeviceMatrix.from_device_pointer(wl.a.data_ptr(), m, n, n, 0)
+    tol = wl.rel_tol * float(wl.x_star.norm())
+    c = wl.cfg("oracle_error", tol, 2000)
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    z = wl.b.clone()
+    tr = _lib.RebkTrace()
+    _lib.check(_lib.load().rebk_run_device(dm.handle, ctypes.byref(c), ctypes.c_void_p(wl.b.data_ptr()),
+                                           ctypes.c_void_p(wl.x_star.data_ptr()), ctypes.c_void_p(x.data_ptr()),
+                                           ctypes.c_void_p(z.data_ptr()), None, ctypes.byref(tr)), "run")
+    assert tr.kernel_path == 7 and tr.converged
+    a_h = wl.a.cpu().numpy()
+    orc = OracleSolver(a_h, wl.b.cpu().numpy(), wl.row_ptr, wl.col_ptr, wl.alpha, "rebk")
+    res = orc.run(wl.seed, 2000, tol, wl.x_star.cpu().numpy(), rng=NumpyRng(wl.seed))
+    assert res["iters"] == tr.iters
+    assert rel(x.cpu().numpy(), res["x"]) <= RTOL and rel(z.cpu().numpy(), res["z"]) <= RTOL
