@@ -102,7 +102,7 @@ typedef struct rebk_trace {
   int64_t errors_cap;
   int64_t n_checks;
   int32_t grid_ctas;        /* CTAs the persistent kernel used */
-  int32_t kernel_path;      /* 0 dense general, 1 dense clustered, 2 same (cooperative), 3 sparse, 4/5 multi-RHS (5: BF16x9 tensor cores), 6 dense split column/row groups, 7 dense streaming (blocks larger than shared memory) */
+  int32_t kernel_path;      /* 0 dense general, 1 dense clustered, 2 same (cooperative), 3 sparse, 4/5 multi-RHS (5: BF16x9 tensor cores), 6 dense split column/row groups, 7 dense streaming (blocks larger than shared memory), 8 multi-RHS on hand-written tcgen05 3xTF32 kernels */
 } rebk_trace;
 
 /* ---- library / device ---------------------------------------------------- */

@@ -50,6 +50,8 @@ struct rebk_ctx {
   std::vector<double> h_csr_val, h_csc_val;
   std::vector<CsrSegPlan*> seg_cache;
   float* A32 = nullptr;  // dense fp32 A (multi-RHS contexts, kind 2)
+  float* A32t = nullptr;  // its transpose (n x ldat), built at the first tensor-core run
+  int64_t ldat = 0;
   double* shard_scratch = nullptr;  // rebk_shard_* partials (not reentrant per ctx)
   size_t shard_scratch_len = 0;
 };
@@ -1391,7 +1393,23 @@ int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float*
       sp.col_cum = d_col_cum;
       sp.col_total = cfg->col_total;
       sp.col_scale = d_col_scale;
-      MrhsRun w{ctx->A32, m, n, ctx->lda, (int)R, dB, dX, dZ, dXs, cfg, tols, extended};
+      // the tensor-core path reads column blocks as rows of Aᵀ (kind::tf32
+      // operands must be K-major): one transposed copy per context
+      const char* mm = getenv("REBK_MRHS_MATH");
+      if (!ctx->A32t && (!mm || !strcmp(mm, "tc")) && m % 4 == 0 && n % 4 == 0) {
+        const int64_t ldat = m;
+        if (cudaMalloc(&ctx->A32t, sizeof(float) * n * ldat) == cudaSuccess) {
+          ctx->ldat = ldat;
+          if (mrhs_transpose_a(ctx->A32, m, n, ctx->lda, ctx->A32t, ldat, stream) != cudaSuccess) {
+            cudaFree(ctx->A32t);
+            ctx->A32t = nullptr;
+          }
+        } else {
+          cudaGetLastError();
+          ctx->A32t = nullptr;
+        }
+      }
+      MrhsRun w{ctx->A32, m, n, ctx->lda, ctx->A32t, ctx->ldat, (int)R, dB, dX, dZ, dXs, cfg, tols, extended};
       double ms = 0.0;
       int64_t K = 0;
       int math = 0;
@@ -1424,7 +1442,7 @@ int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float*
           trace->loop_ms = ms;
           trace->n_checks = 0;
           trace->grid_ctas = 0;
-          trace->kernel_path = math == 4 ? 5 : 4;
+          trace->kernel_path = math == 6 ? 8 : (math == 4 ? 5 : 4);
         }
       }
     }
@@ -1499,6 +1517,7 @@ int rebk_ctx_destroy(rebk_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaFree(ctx->shard_scratch);
   }
+  if (ctx->A32t) cudaFree(ctx->A32t);
   if (ctx->A32) {
     cudaSetDevice(ctx->device);
     cudaFree(ctx->A32);

@@ -221,6 +221,8 @@ cudaError_t csr_kernel_occupancy(int* blocks_per_sm);
 struct MrhsRun {
   const float* A;
   int64_t m, n, lda;
+  const float* At;  // transposed copy (n x ldat) for the tensor-core path, or null
+  int64_t ldat;
   int R;
   float *B, *X, *Z, *Xs;  // device, row-major (rows x R)
   const struct rebk_cfg* cfg;
@@ -230,6 +232,12 @@ struct MrhsRun {
 int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SampleParams* unused, int64_t* iters_out,
              double* errs_out, double* loop_ms, int64_t* k_final, char* errbuf, size_t errlen, cudaStream_t stream,
              int* math_used);
+// tensor-core (tcgen05, 3xTF32) multi-RHS path (rebk_mrhs_tc.cu)
+bool mrhs_tc_supported(int64_t m, int64_t n, int R, int nJmax, int nImax);
+cudaError_t mrhs_transpose_a(const float* A, int64_t m, int64_t n, int64_t lda, float* At, int64_t ldat,
+                             cudaStream_t st);
+int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iters_out, double* errs_out,
+                double* loop_ms, int64_t* k_final, char* errbuf, size_t errlen, cudaStream_t stream);
 // row-sharded multi-GPU pieces (rebk_shard.cu)
 cudaError_t shard_colstep(const double* A, int64_t lda, int64_t m, int64_t c_lo, int nJ, const double* z, double* u,
                           double* scratch, cudaStream_t st);

@@ -164,7 +164,7 @@ __global__ void mrhs_check_final(const double* __restrict__ part, int nchunks, i
 static int mrhs_math_mode() {
   const char* s = getenv("REBK_MRHS_MATH");
   if (s && !strcmp(s, "bf16x9")) return CUBLAS_FP32_EMULATED_BF16X9_MATH;
-  if (s && !strcmp(s, "default")) return CUBLAS_DEFAULT_MATH;
+  if (s && !strcmp(s, "default")) return CUBLAS_DEFAULT_MATH;  // "pedantic" (or anything else): FP32
   return CUBLAS_PEDANTIC_MATH;
 }
 
@@ -172,6 +172,24 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
              double* errs_out, double* loop_ms, int64_t* k_final, char* errbuf, size_t errlen, cudaStream_t stream,
              int* math_used) {
   (void)unused;
+  // default: the hand-written tcgen05 3xTF32 kernels (rebk_mrhs_tc.cu);
+  // REBK_MRHS_MATH=pedantic|default|bf16x9 selects the cuBLAS path
+  const char* mm = getenv("REBK_MRHS_MATH");
+  if (w.At && (!mm || !strcmp(mm, "tc"))) {
+    int nJm = 1, nIm = 1;
+    for (int64_t b = 0; b < w.cfg->n_row_blocks; ++b)
+      nIm = std::max<int>(nIm, (int)(w.cfg->row_ptr[b + 1] - w.cfg->row_ptr[b]));
+    if (w.extended)
+      for (int64_t b = 0; b < w.cfg->n_col_blocks; ++b)
+        nJm = std::max<int>(nJm, (int)(w.cfg->col_ptr[b + 1] - w.cfg->col_ptr[b]));
+    if (mrhs_tc_supported(w.m, w.n, w.R, nJm, nIm)) {
+      const int r = run_mrhs_tc(w, sp_template, iters_out, errs_out, loop_ms, k_final, errbuf, errlen, stream);
+      if (r != -3) {  // -3: partition not supported by the tensor-core path
+        *math_used = 6;
+        return r;
+      }
+    }
+  }
   CublasApi& cb = cublas();
   if (!cb.ok) {
     snprintf(errbuf, errlen, "cuBLAS could not be loaded (dlopen libcublas.so.12)");

@@ -1,0 +1,628 @@
+// rebk_mrhs_tc.cu — multi-RHS fp32 REBK (BASELINE config 5) on the 5th-gen
+// tensor cores: hand-written tcgen05 kind::tf32 GEMMs with 3xTF32 operand
+// splitting (fp32 accuracy), accumulators in TMEM.
+//
+// kind::tf32 takes K-major operands only, so everything is arranged for K to
+// be the contiguous dimension in HBM:
+//   * A (m x n, row-major) and a transposed copy At (n x m, built once per
+//     context) — the column sweep reads At rows, the row sweep A rows;
+//   * the iterates live transposed, Zt (R x m) and Xt (R x n), and so do the
+//     small per-iteration vectors Ut (R x |J|) and Rt (R x |I|).
+// The four products of step_rebk (solvers.py:283-295) are then
+//   U  = A_Jᵀ Z    : D[j][c] = Σ_r At[c_lo+j][r] · Zt[c][r]     (split over r)
+//   Z -= s A_J U   : D[r][c] = Σ_j A[r][c_lo+j] · Ut[c][j]     (tiles of 128 r)
+//   Rr = A_I X..   : D[i][c] = Σ_k A[r_lo+i][k] · Xt[c][k]     (split over k)
+//   X -= s A_Iᵀ Rr : D[k][c] = Σ_i At[k][r_lo+i] · Rt[c][i]    (tiles of 128 k)
+// with c the right-hand side.  Every operand tile is one 2D TMA box of 32
+// fp32 along K (128 bytes) x rows with the 128-byte swizzle, i.e. exactly the
+// K-major SWIZZLE_128B UMMA layout (umma.cuh).  (A no-swizzle layout needs
+// 16-byte-wide boxes, which TMA moves far too slowly.)  3xTF32:
+// D += hi·hi + hi·lo + lo·hi; the raw fp32 tile serves as "hi" (the tensor
+// core truncates to TF32, measured bit-identical to an explicit split) and
+// the CTA computes the lo tiles in shared memory.  Partial sums of the split
+// products are reduced in a fixed order, so runs replay bit for bit.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/rebk.h"
+#include "rebk_device.cuh"
+#include "rebk_internal.h"
+#include "umma.cuh"
+
+namespace rebk {
+
+namespace tc {
+
+constexpr int BK = 32;           // K per pipeline stage: one 128-byte swizzle atom (4 tf32 MMA k-steps)
+constexpr int NSTAGE = 4;
+constexpr int TM = 128;          // MMA M (rows per tile)
+constexpr int RHS = 64;          // MMA N = number of right-hand sides
+
+// shared memory of one stage (floats): A raw, A lo, B raw, B lo
+constexpr int STAGE_FLOATS = 2 * TM * BK + 2 * RHS * BK;
+constexpr size_t SMEM_BYTES = (size_t)NSTAGE * STAGE_FLOATS * 4 + 1024;  // + alignment slack
+
+__device__ __forceinline__ float* aligned_smem(float* p) {
+  return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~(uintptr_t)1023);
+}
+
+// ---- warp-specialized persistent GEMM -----------------------------------------
+// 12 warps: warp 0 = TMA producer, warp 1 = MMA issuer (one lane each),
+// warps 2-7 = converters (lo = x - trunc_tf32(x) into the stage's lo tiles),
+// warps 8-11 = epilogue (TMEM lanes 32*(warp%4)..).  Ring of NSTAGE stages
+// (raw A, lo A, raw B, lo B); two TMEM accumulators (D_hh | D_hl, 128
+// columns each) so the epilogue of one tile overlaps the next tile's MMAs.
+// Work list: tile j of this CTA = (row0, k-block range); MODE 0 writes split-K
+// partials, MODE 1 applies Yt[c][row] -= s * D[row][c].
+constexpr int NTW = 384;
+constexpr int CONV0 = 2, NCONV = 6, EPI0 = 8;
+
+struct Pipe {
+  uint64_t full[NSTAGE], conv[NSTAGE], empty[NSTAGE];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem;
+};
+
+struct TileJob {
+  int row0;   // first operand row of the tile
+  int kb0, kb1;
+  int slot;   // output index: partial slice (MODE 0) / unused
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(NTW, 1)
+    k_gemm(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, int a_k0, int row_lo,
+           int nrows, int nkb, int nslices, float s, float* __restrict__ out, int64_t ldy, int dbg) {
+  extern __shared__ float smem_raw[];
+  float* smem = aligned_smem(smem_raw);
+  __shared__ Pipe P;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) umma::tmem_alloc<256>(&P.tmem);
+  if (tid == 32) {
+    for (int q = 0; q < NSTAGE; ++q) {
+      mbar_init(&P.full[q], 1);
+      mbar_init(&P.conv[q], NCONV);
+      mbar_init(&P.empty[q], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&P.tfull[b], 1);
+      mbar_init(&P.tempty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = P.tmem;
+
+  // this CTA's tiles: MODE 0 -> one (row tile, K slice); MODE 1 -> row tiles
+  // blockIdx.x, +gridDim.x, ... with the whole K range
+  const int ntiles_total = (nrows + TM - 1) / TM;
+  const int ntiles_part = (nrows + TM - 1) / TM;  // MODE 0: row tiles, all for this CTA's K slice
+  auto job = [&](int j, TileJob& J) -> bool {
+    if (MODE == 0) {
+      if (j >= ntiles_part) return false;
+      const int t = j, q = blockIdx.x;
+      J.row0 = row_lo + t * TM;
+      J.kb0 = (int)((int64_t)nkb * q / nslices);
+      J.kb1 = (int)((int64_t)nkb * (q + 1) / nslices);
+      J.slot = q;
+      return true;
+    }
+    const int tau = blockIdx.x + j * gridDim.x;
+    if (tau >= ntiles_total) return false;
+    J.row0 = tau * TM;
+    J.kb0 = 0;
+    J.kb1 = nkb;
+    J.slot = tau;
+    return true;
+  };
+  auto a_raw = [&](int q) { return smem + (size_t)q * STAGE_FLOATS; };
+  auto a_lo = [&](int q) { return smem + (size_t)q * STAGE_FLOATS + TM * BK; };
+  auto b_raw = [&](int q) { return smem + (size_t)q * STAGE_FLOATS + 2 * TM * BK; };
+  auto b_lo = [&](int q) { return smem + (size_t)q * STAGE_FLOATS + 2 * TM * BK + RHS * BK; };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      uint32_t ph = 0;
+      int it = 0;
+      TileJob J;
+      // pull every block of this CTA into L2 first: the DRAM then sees whole
+      // row segments at once, and the ring's TMA loads hit L2
+      if (dbg & 4)
+        for (int j = 0; job(j, J); ++j)
+          for (int kb = J.kb0; kb < J.kb1; ++kb) {
+            tma_prefetch_l2_2d(&ma, a_k0 + kb * BK, J.row0);
+            if (j == 0) tma_prefetch_l2_2d(&mb, kb * BK, 0);
+          }
+      for (int j = 0; job(j, J); ++j)
+        for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
+          const int q = it % NSTAGE;
+          if (it >= NSTAGE) {
+            mbar_wait(&P.empty[q], (ph >> q) & 1u);
+            ph ^= 1u << q;
+          }
+          mbar_arrive_expect_tx(&P.full[q], (TM + RHS) * BK * 4);
+          tma_load_2d(a_raw(q), &ma, a_k0 + kb * BK, J.row0, &P.full[q]);
+          tma_load_2d(b_raw(q), &mb, kb * BK, 0, &P.full[q]);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      const uint32_t idesc = umma::idesc_tf32(TM, RHS);
+      uint32_t phc = 0, pht = 0;
+      int it = 0;
+      TileJob J;
+      for (int j = 0; job(j, J); ++j) {
+        const int b = j & 1;
+        if (j >= 2) {  // accumulator b is free once the epilogue of tile j-2 has read it
+          mbar_wait(&P.tempty[b], (pht >> b) & 1u);
+          pht ^= 1u << b;
+        }
+        const uint32_t dh = tmem + b * 128, dl = dh + RHS;
+        for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
+          const int q = it % NSTAGE;
+          mbar_wait(&P.conv[q], (phc >> q) & 1u);
+          phc ^= 1u << q;
+          umma::fence_after_sync();
+          for (int ks = 0; ks < ((dbg & 2) ? 0 : BK / 8); ++ks) {
+            const uint64_t ah = umma::make_desc_sw128(smem_u32(a_raw(q)) + 32 * ks);
+            const uint64_t al = umma::make_desc_sw128(smem_u32(a_lo(q)) + 32 * ks);
+            const uint64_t bh = umma::make_desc_sw128(smem_u32(b_raw(q)) + 32 * ks);
+            const uint64_t bl = umma::make_desc_sw128(smem_u32(b_lo(q)) + 32 * ks);
+            const bool acc = kb > J.kb0 || ks > 0;
+            umma::mma_tf32(dh, ah, bh, idesc, acc);
+            umma::mma_tf32(dl, ah, bl, idesc, acc);
+            umma::mma_tf32(dh, al, bh, idesc, true);
+          }
+          umma::commit(&P.empty[q]);
+        }
+        umma::commit(&P.tfull[b]);  // (an empty K range leaves D untouched; see the epilogue)
+      }
+    }
+  } else if (warp < EPI0) {  // ---- converters
+    const int ct = tid - CONV0 * 32;
+    uint32_t phf = 0;
+    int it = 0;
+    TileJob J;
+    for (int j = 0; job(j, J); ++j)
+      for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
+        const int q = it % NSTAGE;
+        mbar_wait(&P.full[q], (phf >> q) & 1u);
+        phf ^= 1u << q;
+        constexpr int A4 = TM * BK / 4, B4 = RHS * BK / 4;
+        for (int e = ct; e < ((dbg & 1) ? 0 : A4 + B4); e += NCONV * 32) {
+          const float4* src = e < A4 ? reinterpret_cast<const float4*>(a_raw(q)) + e
+                                     : reinterpret_cast<const float4*>(b_raw(q)) + (e - A4);
+          float4* dst = e < A4 ? reinterpret_cast<float4*>(a_lo(q)) + e : reinterpret_cast<float4*>(b_lo(q)) + (e - A4);
+          const float4 v = *src;
+          float4 l;
+          float h;
+          umma::split_tf32(v.x, h, l.x);
+          umma::split_tf32(v.y, h, l.y);
+          umma::split_tf32(v.z, h, l.z);
+          umma::split_tf32(v.w, h, l.w);
+          *dst = l;
+        }
+        fence_proxy_async();  // this thread's generic smem writes -> async proxy
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&P.conv[q]);
+      }
+  } else {  // ---- epilogue
+    uint32_t pht = 0;
+    TileJob J;
+    const int rlane = (warp & 3) * 32;
+    for (int j = 0; job(j, J); ++j) {
+      const int b = j & 1;
+      mbar_wait(&P.tfull[b], (pht >> b) & 1u);
+      pht ^= 1u << b;
+      umma::fence_after_sync();
+      const uint32_t base = tmem + ((uint32_t)rlane << 16) + b * 128;
+      const int row = rlane + lane;
+      const bool any = J.kb1 > J.kb0;
+      for (int c0 = 0; c0 < RHS; c0 += 16) {
+        float h[16], l[16];
+        umma::tmem_ld16(base + c0, h);
+        umma::tmem_ld16(base + RHS + c0, l);
+        if (MODE == 0) {
+          const int jrow = J.row0 - row_lo + row;
+          if (jrow < nrows) {
+            float4* dst = reinterpret_cast<float4*>(out + ((size_t)J.slot * 256 + jrow) * RHS + c0);
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+              dst[w] = any ? make_float4(h[4 * w] + l[4 * w], h[4 * w + 1] + l[4 * w + 1], h[4 * w + 2] + l[4 * w + 2],
+                                         h[4 * w + 3] + l[4 * w + 3])
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        } else {
+          const int r = J.row0 + row;
+          if (r < nrows && any) {
+            float y[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) y[q] = __ldcg(out + (size_t)(c0 + q) * ldy + r);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) __stcg(out + (size_t)(c0 + q) * ldy + r, y[q] - s * (h[q] + l[q]));
+          }
+        }
+      }
+      umma::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&P.tempty[b]);
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc<256>(tmem);
+}
+
+// Split-K sums, fixed order: block (row j of 256, 32 columns c) with 8 warps;
+// warp g sums partials q = g, g + 8, ... for its lane's column, then lane
+// c of warp 0 adds the 8 group sums in order.
+__device__ __forceinline__ float sum_parts(const float* __restrict__ part, int nparts, int j, int c) {
+  __shared__ float grp[8][32];
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float acc = 0.f;
+  for (int q = g; q < nparts; q += 8) acc += part[((size_t)q * 256 + j) * RHS + c];
+  grp[g][lane] = acc;
+  __syncthreads();
+  float s = 0.f;
+  if (g == 0)
+    for (int w = 0; w < 8; ++w) s += grp[w][lane];
+  return s;
+}
+// Ut[c][j] = Σ_q part[q][j][c] for j < nJ, zero for nJ <= j < 256 (K padding)
+__global__ void __launch_bounds__(256) k_reduce_u(const float* __restrict__ part, int nparts, int nJ, int ldu,
+                                                  float* __restrict__ Ut) {
+  const int j = blockIdx.x, c = blockIdx.y * 32 + (threadIdx.x & 31);
+  const float s = j < nJ ? sum_parts(part, nparts, j, c) : 0.f;
+  if (threadIdx.x < 32) Ut[(size_t)c * ldu + j] = s;
+}
+// Rt[c][i] = ((Σ_q part[q][i][c]) - Bt[c][r_lo+i]) + Zt[c][r_lo+i]  (solvers.py:291-293 order)
+__global__ void __launch_bounds__(256) k_reduce_r(const float* __restrict__ part, int nparts, int nI, int ldr,
+                                                  const float* __restrict__ Bt, const float* __restrict__ Zt,
+                                                  int64_t ldm, int r_lo, float* __restrict__ Rt) {
+  const int i = blockIdx.x, c = blockIdx.y * 32 + (threadIdx.x & 31);
+  float v = 0.f;
+  if (i < nI) {
+    v = sum_parts(part, nparts, i, c);
+    if (threadIdx.x < 32) {
+      v = v - Bt[(size_t)c * ldm + r_lo + i];
+      if (Zt) v += Zt[(size_t)c * ldm + r_lo + i];
+    }
+  }
+  if (threadIdx.x < 32) Rt[(size_t)c * ldr + i] = v;
+}
+
+// out[c][r] = in[r][c] for the R columns of a row-major (rows x R) array
+// (columns R..63 of the transposed array stay zero), and the inverse
+__global__ void k_to_t(const float* __restrict__ in, int64_t rows, int R, float* __restrict__ out, int64_t ldo) {
+  __shared__ float t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + y;
+    const int c = c0 + threadIdx.x;
+    t[y][threadIdx.x] = (r < rows && c < R) ? in[r * R + c] : 0.f;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x;
+    if (r < rows) out[(size_t)(c0 + y) * ldo + r] = t[threadIdx.x][y];
+  }
+}
+__global__ void k_from_t(const float* __restrict__ in, int64_t ldi, int64_t rows, int R, float* __restrict__ out) {
+  __shared__ float t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x;
+    t[y][threadIdx.x] = r < rows ? in[(size_t)(c0 + y) * ldi + r] : 0.f;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + y;
+    const int c = c0 + threadIdx.x;
+    if (r < rows && c < R) out[r * R + c] = t[threadIdx.x][y];
+  }
+}
+__global__ void k_transpose(const float* __restrict__ A, int64_t m, int64_t n, int64_t lda, float* __restrict__ At,
+                            int64_t ldat) {
+  __shared__ float t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + y, c = c0 + threadIdx.x;
+    t[y][threadIdx.x] = (r < m && c < n) ? A[r * lda + c] : 0.f;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + y, r = r0 + threadIdx.x;
+    if (c < n && r < m) At[c * ldat + r] = t[threadIdx.x][y];
+  }
+}
+
+// per-RHS ||Xt[c] - Xst[c]||^2: chunk partials (fixed order) + crossing logic
+constexpr int kChk = 1024;
+__global__ void k_check_part(const float* __restrict__ Xt, const float* __restrict__ Xst, int64_t n,
+                             double* __restrict__ part) {
+  __shared__ double red[8];
+  const int c = blockIdx.y;
+  const int64_t k0 = (int64_t)blockIdx.x * kChk;
+  double acc = 0.0;
+  for (int64_t k = k0 + threadIdx.x; k < k0 + kChk && k < n; k += blockDim.x) {
+    const double d = (double)Xt[(size_t)c * n + k] - (double)Xst[(size_t)c * n + k];
+    acc = fma(d, d, acc);
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    part[(size_t)c * gridDim.x + blockIdx.x] = s;
+  }
+}
+__global__ void k_check_final(const double* __restrict__ part, int nchunks, int R, const double* __restrict__ tol,
+                              int64_t k, int64_t* iters, double* errs_at, int32_t* n_done) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= R) return;
+  double s = 0.0;
+  for (int q = 0; q < nchunks; ++q) s += part[(size_t)c * nchunks + q];
+  const double e = sqrt(s);
+  if (iters[c] < 0 && e <= tol[c]) {
+    iters[c] = k;
+    errs_at[c] = e;
+    atomicAdd(n_done, 1);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encoder() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+// K-major operand view of a row-major fp32 matrix (rows x kdim, leading dim
+// ld): box of 32 along K x box_rows with the 128-byte swizzle
+static bool encode_kmajor(CUtensorMap* map, const float* base, int64_t rows, int64_t kdim, int64_t ld, int box_rows) {
+  EncodeTiledFn fn = encoder();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace tc
+
+cudaError_t mrhs_transpose_a(const float* A, int64_t m, int64_t n, int64_t lda, float* At, int64_t ldat,
+                             cudaStream_t st) {
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((m + 31) / 32)), block(32, 8);
+  tc::k_transpose<<<grid, block, 0, st>>>(A, m, n, lda, At, ldat);
+  return cudaGetLastError();
+}
+
+bool mrhs_tc_supported(int64_t m, int64_t n, int R, int nJmax, int nImax) {
+  return R >= 1 && R <= tc::RHS && m % 4 == 0 && n % 4 == 0 && nJmax <= 256 && nImax <= 256 && tc::encoder() != nullptr;
+}
+
+#define TC_TRY(expr)                                                     \
+  do {                                                                   \
+    cudaError_t _e = (expr);                                             \
+    if (_e != cudaSuccess) {                                             \
+      snprintf(errbuf, errlen, "%s: %s", #expr, cudaGetErrorString(_e)); \
+      return -2;                                                         \
+    }                                                                    \
+  } while (0)
+
+// Same contract as run_mrhs (rebk_mrhs.cu): per-column stopping on the
+// device, chunks of 64 iterations captured as CUDA graphs, exact stop state
+// by checkpoint + replay.  w.B/X/Z/Xs are row-major (rows x 64) on entry and
+// exit; inside they are kept transposed.
+int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iters_out, double* errs_out,
+                double* loop_ms, int64_t* k_final, char* errbuf, size_t errlen, cudaStream_t stream) {
+  using namespace tc;
+  const rebk_cfg* cfg = w.cfg;
+  const int R = w.R;
+  const int64_t m = w.m, n = w.n;
+  const bool checking = cfg->stop_mode == 0;
+  int nJmax = 1, nImax = 1;
+  for (int64_t b = 0; b < cfg->n_row_blocks; ++b) nImax = std::max<int>(nImax, (int)(cfg->row_ptr[b + 1] - cfg->row_ptr[b]));
+  if (w.extended)
+    for (int64_t b = 0; b < cfg->n_col_blocks; ++b)
+      nJmax = std::max<int>(nJmax, (int)(cfg->col_ptr[b + 1] - cfg->col_ptr[b]));
+  for (int64_t b = 0; b < cfg->n_row_blocks; ++b)
+    if (cfg->row_ptr[b] % 4) {
+      snprintf(errbuf, errlen, "tensor-core multi-RHS path needs row blocks starting at multiples of 4");
+      return -3;
+    }
+  if (w.extended)
+    for (int64_t b = 0; b < cfg->n_col_blocks; ++b)
+      if (cfg->col_ptr[b] % 4) {
+        snprintf(errbuf, errlen, "tensor-core multi-RHS path needs column blocks starting at multiples of 4");
+        return -3;
+      }
+  const int ldu = 256, ldr = 256;  // Ut / Rt padded to whole K-blocks (zeros)
+  float *Zt = nullptr, *Xt, *Bt, *Xst = nullptr, *Ut, *Rt, *part, *Xsnap, *Zsnap = nullptr;
+  double *d_tol, *d_errs_at, *d_cpart;
+  int64_t* d_iters;
+  int32_t* d_ndone;
+  Plan* d_plan;
+  const int G1 = 148, G3 = 40;  // CTAs (K slices) of the two split-K products; each does every row tile
+  const int nchk = (int)((n + kChk - 1) / kChk);
+  // the transposed arrays always have 64 rows (the MMA N); rows R..63 are zero
+  TC_TRY(cudaMallocAsync((void**)&Xt, sizeof(float) * RHS * n, stream));
+  TC_TRY(cudaMallocAsync((void**)&Bt, sizeof(float) * RHS * m, stream));
+  if (w.extended) TC_TRY(cudaMallocAsync((void**)&Zt, sizeof(float) * RHS * m, stream));
+  if (w.Xs) TC_TRY(cudaMallocAsync((void**)&Xst, sizeof(float) * RHS * n, stream));
+  TC_TRY(cudaMallocAsync((void**)&Ut, sizeof(float) * RHS * ldu, stream));
+  TC_TRY(cudaMallocAsync((void**)&Rt, sizeof(float) * RHS * ldr, stream));
+  TC_TRY(cudaMallocAsync((void**)&part, sizeof(float) * (size_t)std::max(G1, G3) * 256 * RHS, stream));
+  TC_TRY(cudaMemsetAsync(part, 0, sizeof(float) * (size_t)std::max(G1, G3) * 256 * RHS, stream));
+  TC_TRY(cudaMallocAsync((void**)&Xsnap, sizeof(float) * RHS * n, stream));
+  if (w.extended) TC_TRY(cudaMallocAsync((void**)&Zsnap, sizeof(float) * RHS * m, stream));
+  TC_TRY(cudaMallocAsync((void**)&d_tol, sizeof(double) * R, stream));
+  TC_TRY(cudaMallocAsync((void**)&d_errs_at, sizeof(double) * R, stream));
+  TC_TRY(cudaMallocAsync((void**)&d_cpart, sizeof(double) * R * nchk, stream));
+  TC_TRY(cudaMallocAsync((void**)&d_iters, sizeof(int64_t) * R, stream));
+  TC_TRY(cudaMallocAsync((void**)&d_ndone, sizeof(int32_t), stream));
+  const int64_t CH = 64;
+  TC_TRY(cudaMallocAsync((void**)&d_plan, sizeof(Plan) * CH, stream));
+  dim3 tb(32, 8);
+  k_to_t<<<dim3((unsigned)((n + 31) / 32), RHS / 32), tb, 0, stream>>>(w.X, n, R, Xt, n);
+  k_to_t<<<dim3((unsigned)((m + 31) / 32), RHS / 32), tb, 0, stream>>>(w.B, m, R, Bt, m);
+  if (w.extended) k_to_t<<<dim3((unsigned)((m + 31) / 32), RHS / 32), tb, 0, stream>>>(w.Z, m, R, Zt, m);
+  if (Xst) k_to_t<<<dim3((unsigned)((n + 31) / 32), RHS / 32), tb, 0, stream>>>(w.Xs, n, R, Xst, n);
+  TC_TRY(cudaGetLastError());
+  std::vector<double> tol(R);
+  for (int c = 0; c < R; ++c) tol[c] = w.tols ? w.tols[c] : cfg->tol;
+  TC_TRY(cudaMemcpyAsync(d_tol, tol.data(), sizeof(double) * R, cudaMemcpyHostToDevice, stream));
+  TC_TRY(cudaMemsetAsync(d_iters, 0xff, sizeof(int64_t) * R, stream));
+  TC_TRY(cudaMemsetAsync(d_ndone, 0, sizeof(int32_t), stream));
+  TC_TRY(cudaMemsetAsync(d_errs_at, 0, sizeof(double) * R, stream));
+
+  // tensor maps: A and At views (128-row boxes), iterate views (64-row boxes)
+  CUtensorMap mA, mAt, mZt, mXt, mUt, mRt;
+  bool ok = encode_kmajor(&mA, w.A, m, n, w.lda, TM) && encode_kmajor(&mXt, Xt, RHS, n, n, RHS) &&
+            encode_kmajor(&mUt, Ut, RHS, ldu, ldu, RHS) && encode_kmajor(&mRt, Rt, RHS, ldr, ldr, RHS);
+  if (w.extended) ok = ok && encode_kmajor(&mAt, w.At, n, m, w.ldat, TM) && encode_kmajor(&mZt, Zt, RHS, m, m, RHS);
+  else ok = ok && encode_kmajor(&mAt, w.At, n, m, w.ldat, TM);
+  if (!ok) {
+    snprintf(errbuf, errlen, "tensor map encoding failed");
+    return -2;
+  }
+  TC_TRY(cudaFuncSetAttribute(k_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+  TC_TRY(cudaFuncSetAttribute(k_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+
+  auto launch_check = [&](int64_t k) -> cudaError_t {
+    k_check_part<<<dim3(nchk, R), 256, 0, stream>>>(Xt, Xst, n, d_cpart);
+    k_check_final<<<(R + 63) / 64, 64, 0, stream>>>(d_cpart, nchk, R, d_tol, k, d_iters, d_errs_at, d_ndone);
+    return cudaGetLastError();
+  };
+  const int nkb_m = (int)((m + BK - 1) / BK), nkb_n = (int)((n + BK - 1) / BK);
+  const char* dbg_env = getenv("REBK_TC_DBG");  // experiments: 1 skip lo split, 2 skip MMAs, 4 L2 prefetch
+  const int dbg = dbg_env ? atoi(dbg_env) : 0;
+  if (TM * 2 > 256 || RHS % 32) return -3;
+  auto enqueue_iter = [&](const Plan& pl, int64_t k, bool do_check) -> cudaError_t {
+    const int nJ = pl.c_hi - pl.c_lo, nI = pl.r_hi - pl.r_lo;
+    if (w.extended) {
+      const int ns = G1;
+      k_gemm<0><<<ns, NTW, SMEM_BYTES, stream>>>(mAt, mZt, 0, pl.c_lo, nJ, nkb_m, ns, 0.f, part, 0, dbg);
+      k_reduce_u<<<dim3(ldu, RHS / 32), 256, 0, stream>>>(part, ns, nJ, ldu, Ut);
+      k_gemm<1><<<std::min(nsm, (int)((m + TM - 1) / TM)), NTW, SMEM_BYTES, stream>>>(
+          mA, mUt, pl.c_lo, 0, (int)m, (nJ + BK - 1) / BK, 0, (float)pl.c_scale, Zt, m, dbg);
+    }
+    const int ns3 = G3;
+    k_gemm<0><<<ns3, NTW, SMEM_BYTES, stream>>>(mA, mXt, 0, pl.r_lo, nI, nkb_n, ns3, 0.f, part, 0, dbg);
+    k_reduce_r<<<dim3(ldr, RHS / 32), 256, 0, stream>>>(part, ns3, nI, ldr, Bt, Zt, m, pl.r_lo, Rt);
+    k_gemm<1><<<std::min(nsm, (int)((n + TM - 1) / TM)), NTW, SMEM_BYTES, stream>>>(
+        mAt, mRt, pl.r_lo, 0, (int)n, (nI + BK - 1) / BK, 0, (float)pl.r_scale, Xt, n, dbg);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && do_check) e = launch_check(k);
+    return e;
+  };
+
+  cudaEvent_t ev0, ev1;
+  TC_TRY(cudaEventCreate(&ev0));
+  TC_TRY(cudaEventCreate(&ev1));
+  TC_TRY(cudaEventRecord(ev0, stream));
+  int64_t K = cfg->max_iters;
+  bool all_done = false;
+  if (checking) {
+    TC_TRY(launch_check(0));
+    int32_t nd = 0;
+    TC_TRY(cudaMemcpyAsync(&nd, d_ndone, sizeof nd, cudaMemcpyDeviceToHost, stream));
+    TC_TRY(cudaStreamSynchronize(stream));
+    if (nd == R) {
+      all_done = true;
+      K = 0;
+    }
+  }
+  std::vector<Plan> hplan(CH);
+  for (int64_t k0 = 1; !all_done && k0 <= cfg->max_iters; k0 += CH) {
+    const int64_t cnt = std::min(CH, cfg->max_iters - k0 + 1);
+    TC_TRY(launch_sample_plan(sp_template, k0, cnt, d_plan, nullptr, stream));
+    TC_TRY(cudaMemcpyAsync(hplan.data(), d_plan, sizeof(Plan) * cnt, cudaMemcpyDeviceToHost, stream));
+    TC_TRY(cudaStreamSynchronize(stream));
+    if (checking) {
+      TC_TRY(cudaMemcpyAsync(Xsnap, Xt, sizeof(float) * n * RHS, cudaMemcpyDeviceToDevice, stream));
+      if (w.extended) TC_TRY(cudaMemcpyAsync(Zsnap, Zt, sizeof(float) * m * RHS, cudaMemcpyDeviceToDevice, stream));
+    }
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    TC_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t ce = cudaSuccess;
+    for (int64_t q = 0; q < cnt && ce == cudaSuccess; ++q) {
+      const int64_t k = k0 + q;
+      ce = enqueue_iter(hplan[q], k, checking && (k % cfg->check_stride == 0 || k == cfg->max_iters));
+    }
+    cudaError_t ee = cudaStreamEndCapture(stream, &graph);
+    if (ce != cudaSuccess || ee != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      snprintf(errbuf, errlen, "graph capture failed: %s", cudaGetErrorString(ce != cudaSuccess ? ce : ee));
+      return -2;
+    }
+    TC_TRY(cudaGraphInstantiate(&gexec, graph, 0));
+    TC_TRY(cudaGraphLaunch(gexec, stream));
+    TC_TRY(cudaStreamSynchronize(stream));
+    cudaGraphExecDestroy(gexec);
+    cudaGraphDestroy(graph);
+    if (checking) {
+      int32_t nd = 0;
+      TC_TRY(cudaMemcpyAsync(&nd, d_ndone, sizeof nd, cudaMemcpyDeviceToHost, stream));
+      TC_TRY(cudaStreamSynchronize(stream));
+      if (nd == R) {
+        std::vector<int64_t> it(R);
+        TC_TRY(cudaMemcpy(it.data(), d_iters, sizeof(int64_t) * R, cudaMemcpyDeviceToHost));
+        K = *std::max_element(it.begin(), it.end());
+        all_done = true;
+        if (K < k0 + cnt - 1) {  // rewind to the chunk start and replay up to K exactly
+          TC_TRY(cudaMemcpyAsync(Xt, Xsnap, sizeof(float) * n * RHS, cudaMemcpyDeviceToDevice, stream));
+          if (w.extended) TC_TRY(cudaMemcpyAsync(Zt, Zsnap, sizeof(float) * m * RHS, cudaMemcpyDeviceToDevice, stream));
+          for (int64_t k = k0; k <= K; ++k) TC_TRY(enqueue_iter(hplan[k - k0], k, false));
+        }
+      }
+    }
+  }
+  TC_TRY(cudaEventRecord(ev1, stream));
+  TC_TRY(cudaStreamSynchronize(stream));
+  float ms = 0.f;
+  TC_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  *loop_ms = ms;
+  *k_final = K;
+  // results back to the row-major layout of the caller
+  k_from_t<<<dim3((unsigned)((n + 31) / 32), RHS / 32), tb, 0, stream>>>(Xt, n, n, R, w.X);
+  if (w.extended) k_from_t<<<dim3((unsigned)((m + 31) / 32), RHS / 32), tb, 0, stream>>>(Zt, m, m, R, w.Z);
+  TC_TRY(cudaGetLastError());
+  if (iters_out) TC_TRY(cudaMemcpy(iters_out, d_iters, sizeof(int64_t) * R, cudaMemcpyDeviceToHost));
+  if (errs_out) TC_TRY(cudaMemcpy(errs_out, d_errs_at, sizeof(double) * R, cudaMemcpyDeviceToHost));
+  for (void* ptr : {(void*)Xt, (void*)Bt, (void*)Zt, (void*)Xst, (void*)Ut, (void*)Rt, (void*)part, (void*)Xsnap,
+                    (void*)Zsnap, (void*)d_tol, (void*)d_errs_at, (void*)d_cpart, (void*)d_iters, (void*)d_ndone,
+                    (void*)d_plan})
+    if (ptr) cudaFreeAsync(ptr, stream);
+  TC_TRY(cudaStreamSynchronize(stream));
+  return 0;
+}
+
+}  // namespace rebk

@@ -1,0 +1,130 @@
+// umma.cuh — minimal tcgen05 (5th-gen tensor core) helpers for sm_100a:
+// TMEM allocation, shared-memory matrix descriptors for the K-major
+// no-swizzle ("interleave") canonical layout, the kind::tf32 MMA, commit to an
+// mbarrier and TMEM -> register loads.  Used by the multi-RHS (C5) kernels.
+//
+// Operand layout (K-major, SWIZZLE_NONE), in 16-byte chunks: a tile of
+// ROWS x K 32-bit elements is stored as core matrices of 8 rows x 16 bytes
+// (4 tf32) that are 128 contiguous bytes each; element (row, k) lives at
+//   (k / 4) * LBO + (row / 8) * SBO + (row % 8) * 16 + (k % 4) * 4   bytes
+// with SBO = 128 (core matrices of consecutive row groups are adjacent) and
+// LBO = ROWS / 8 * 128 (next 4 columns of K).  One kind::tf32 MMA consumes
+// K = 8 (two K chunks); the next MMA's operand starts 2 * LBO further on.
+#pragma once
+#include <stdint.h>
+
+namespace rebk {
+namespace umma {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// byte offset of element (row, k) in a K-major no-swizzle tile of `rows` rows
+__device__ __forceinline__ uint32_t kmajor_offset(int row, int k, int rows) {
+  return (uint32_t)((k >> 2) * (rows >> 3) * 128 + (row >> 3) * 128 + (row & 7) * 16 + (k & 3) * 4);
+}
+
+// shared-memory matrix descriptor (tcgen05 "matrix descriptor", version 1)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (Blackwell)
+  // base offset 0, lbo mode 0, layout type 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// K-major tile with the 128-byte swizzle (what a TMA box of 32 fp32 along K
+// with CU_TENSOR_MAP_SWIZZLE_128B writes): row r at r * 128 bytes, its eight
+// 16-byte K chunks permuted by chunk ^ (r % 8); tile base 1024-byte aligned.
+// Descriptor: SBO = 1024 (8-row groups), LBO unused, layout type 2; the MMA
+// k-step s (8 tf32) starts s * 32 bytes into the row.
+__device__ __forceinline__ uint32_t kmajor_sw128_offset(int row, int k) {
+  return (uint32_t)(row * 128 + ((((k >> 2) ^ row) & 7) << 4) + (k & 3) * 4);
+}
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                    // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // SBO
+  d |= (uint64_t)1 << 46;                    // version
+  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: D f32, A/B tf32, M x N; a_mn / b_mn select the
+// MN-major operand layout (else K-major)
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn = false, bool b_mn = false) {
+  return (1u << 4)                        // c_format F32
+         | (2u << 7)                      // a_format TF32
+         | (2u << 10)                     // b_format TF32
+         | ((uint32_t)a_mn << 15)         // a_major
+         | ((uint32_t)b_mn << 16)         // b_major
+         | ((uint32_t)(N >> 3) << 17)     // n_dim
+         | ((uint32_t)(M >> 4) << 24);    // m_dim
+}
+
+// MN-major no-swizzle tile of `mn` x K 32-bit elements: core matrices of
+// 8 k x 4 mn (16 bytes per k, 128 contiguous bytes); core matrix (mn/4, k/8)
+// at (k/8) * LBO + (mn/4) * SBO with SBO = 128 and LBO = mn/4 * 128.  One
+// tf32 MMA (K = 8) reads one core-matrix column; the next starts LBO on.
+__device__ __forceinline__ uint32_t mnmajor_offset(int mn, int k, int mn_total) {
+  return (uint32_t)((k >> 3) * (mn_total >> 2) * 128 + (mn >> 2) * 128 + (k & 7) * 16 + (mn & 3) * 4);
+}
+
+// D[tmem] (+)= A[smem] * B[smem]ᵀ (both K-major), issued by one thread
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                        bool accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"((uint32_t)accumulate)
+      : "memory");
+}
+
+// arrive on an mbarrier when all previously issued MMAs of this thread are done
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(mbar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// warp-collective TMEM allocation; the base address lands in *dst (smem)
+template <int NCOLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(dst)),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+
+// 32 lanes x 16 consecutive 32-bit columns: thread t of the warp gets lane
+// (taddr.lane + t), columns [col, col + 16)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 3xTF32 operand split: hi keeps the 10 mantissa bits TF32 uses, lo is the
+// exact fp32 remainder (the MMA truncates it to TF32 again)
+__device__ __forceinline__ void split_tf32(float a, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+  lo = a - hi;
+}
+
+}  // namespace umma
+}  // namespace rebk
