@@ -189,6 +189,18 @@ Geometry plan_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int G, bool ext
   return g;
 }
 
+// The general kernel falls back to unstaged (global-memory) tile reads when a
+// tile is not TMA-able (odd column-block starts, 1-wide blocks) and when it is
+// too large for shared memory.  Only the second case goes to the streaming
+// kernel: small unaligned problems keep the general kernel's summation order,
+// so e.g. REBK with z0 = 0 stays bitwise equal to RABK (test_solvers.py:249-265).
+bool tiles_exceed_smem(const Geometry& g, bool extended) {
+  const size_t vec = (size_t)(2 * g.nC_max + g.nR_max + g.nJ_max + g.nI_max + kThreads);
+  const size_t budget = (size_t)kSmemBudget / 8;
+  if (vec + (size_t)g.nI_max * g.rt_ld > budget) return true;
+  return extended && vec + (size_t)g.nR_max * g.ct_ld > budget;
+}
+
 // ---- fast path (rebk_dense_fast.cu) -------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -852,7 +864,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   const int stream_env = env_int("REBK_STREAM", 1);  // 0 off, 1 when the general kernel cannot stage, 2 always
   if (!use_fast && stream_env != 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY &&
       (ctx->lda % 2 == 0) && ((uintptr_t)ctx->A % 16 == 0) && encode_fn() != nullptr &&
-      (stream_env == 2 || !geo.stage_rt || (extended && !geo.stage_ct))) {
+      (stream_env == 2 || tiles_exceed_smem(geo, extended))) {
     stg = stream_geometry(ctx, cfg, std::min(G0, ctx->sm_count), extended);
     int occs = 0;
     if (stg.ok && stream_kernel_occupancy(stg.smem_bytes, &occs) == cudaSuccess && occs >= 1 &&
