@@ -382,6 +382,511 @@ __global__ void k_check_final(const double* __restrict__ part, int nchunks, int 
   }
 }
 
+// ---- persistent whole-run kernel ------------------------------------------------
+// One cooperative launch runs every iteration of a chunk.  The four products
+// of an iteration and the two split-K reductions are phases separated by
+// grid-wide barriers (a monotonically increasing arrival counter), and the
+// phases are arranged so that independent products share a phase:
+//   A_k: P4(k-1)  X -= s A_Iᵀ R    (the previous iteration's x update)
+//        P1(k)    U partials = A_Jᵀ Z over K slices of m
+//   B_k: U = Σ partials; stop check of iteration k-1 (every CTA decides
+//        redundantly from the per-tile error partials P4 wrote)
+//   C_k: P2(k)    Z -= s A_J U
+//        P3(k)    R partials = A_I X over K slices of n
+//   D_k: R = (Σ partials - B_I) + Z_I
+// (P1(k) needs Z_{k-1} only, P3(k) needs X_{k-1} only.)  Four barriers per
+// iteration instead of six kernels; the run stops inside the kernel with the
+// exact state of the first check at which every column has crossed, so no
+// checkpoint/replay is needed.  Warp roles as in k_gemm; the converter and
+// epilogue warps (320 threads) also do the reductions.
+struct PkArgs {
+  const Plan* plan;
+  int64_t k_begin, k_end;  // iterations of this launch
+  int m, n, nkb_m, nkb_n;
+  int extended, checking, stride;
+  int64_t max_iters;
+  int ns1;           // P1 K slices (CTA pairs 2q, 2q+1 = the two 128-row halves of the column block)
+  int ns3, p3_first; // P3 K slices (CTA pairs from p3_first)
+  int nt2, nt4;      // 128-row tiles of the z and x updates
+  int R;
+  float *Zt, *Xt, *Ut, *Rt, *part1, *part3;
+  const float *Bt, *Xst;
+  double* errpart;        // [nt4][RHS] per-tile Σ (x - x*)^2 of a check iteration
+  const double* tol;      // [R]
+  int64_t* iters;         // [R] first crossing (-1: not yet)
+  double* errs_at;        // [R]
+  int64_t* k_final;       // iteration of the final state
+  int32_t* stopped;       // set when every column has crossed
+  unsigned long long* gbar;
+  unsigned long long* trace;  // REBK_PK_TRACE: globaltimer stamps [iteration][CTA][8]
+  int64_t trace_k0;
+  int trace_n;
+  int prefetch;  // L2 prefetch of the next phase's A boxes
+};
+struct PJob {
+  int kind;  // 1: P1, 2: P2, 3: P3, 4: P4
+  int row0, kc0, kb0, kb1, slot, prow;
+  float s;
+  int check;
+};
+constexpr int NRED = NTW - CONV0 * 32;  // threads of the reduction phases (converter + epilogue warps)
+
+// non-aligned named barrier: callers may arrive from divergent code (e.g.
+// right after one lane polled the grid barrier)
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void gbar_arrive(unsigned long long* g) {
+  __threadfence();
+  asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(g) : "memory");
+}
+__device__ __forceinline__ void gbar_wait(const unsigned long long* g, unsigned long long target) {
+  unsigned long long v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(g) : "memory");
+  } while (v < target);
+}
+// L2 loads of data other CTAs wrote during this launch.  __ldcg is a
+// non-volatile asm without a memory clobber, so the compiler may hoist it
+// above a barrier; these may not move.
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+  float v;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_cg_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void pk_stamp(const PkArgs& a, int64_t k, int i) {
+  if (a.trace && k >= a.trace_k0 && k < a.trace_k0 + a.trace_n) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[((size_t)(k - a.trace_k0) * gridDim.x + blockIdx.x) * 8 + i] = t;
+  }
+}
+__device__ __forceinline__ bool pk_is_check(const PkArgs& a, int64_t k) {
+  return a.checking && k >= 1 && (k % a.stride == 0 || k == a.max_iters);
+}
+// job j of this CTA in phase 0 (A_k) or 1 (C_k) of round k
+__device__ __forceinline__ bool pk_job(const PkArgs& a, int phase, int64_t k, int j, PJob& J) {
+  const int b = blockIdx.x, G = gridDim.x;
+  int idx = 0;
+  if (phase == 0) {
+    if (k - 1 >= a.k_begin && b < a.nt4) {
+      if (idx++ == j) {
+        const Plan& pl = a.plan[k - 1 - a.k_begin];
+        J = PJob{4, b * TM, pl.r_lo, 0, (pl.r_hi - pl.r_lo + BK - 1) / BK, b, 0, (float)pl.r_scale,
+                 pk_is_check(a, k - 1) ? 1 : 0};
+        return true;
+      }
+    }
+    if (a.extended && k <= a.k_end) {
+      const Plan& pl = a.plan[k - a.k_begin];
+      const int q = b >> 1, h = b & 1;
+      if (q < a.ns1 && h * TM < pl.c_hi - pl.c_lo && idx++ == j) {
+        // pairs whose CTAs also run a P4 tile (CTAs < nt4) get kb4 fewer K
+        // blocks of m, so every CTA streams about the same number of stages
+        int kb4 = 0, np4 = 0;
+        if (k - 1 >= a.k_begin) {
+          const Plan& pp = a.plan[k - 1 - a.k_begin];
+          kb4 = (pp.r_hi - pp.r_lo + BK - 1) / BK;
+          np4 = (a.nt4 + 1) / 2;
+        }
+        const int64_t T = (int64_t)a.nkb_m + (int64_t)kb4 * np4;
+        if (T - (int64_t)kb4 * a.ns1 < (int64_t)a.ns1) kb4 = 0;  // degenerate: plain even split
+#ifdef PK_NO_WEIGHT
+        kb4 = 0;
+#endif
+        const int64_t T2 = (int64_t)a.nkb_m + (int64_t)kb4 * np4;
+        auto start = [&](int qq) {
+          return (int)(((int64_t)qq * T2 - (int64_t)kb4 * a.ns1 * (qq < np4 ? qq : np4)) / a.ns1);
+        };
+        J = PJob{1, pl.c_lo + h * TM, 0, start(q), start(q + 1), q, h * TM, 0.f, 0};
+        return true;
+      }
+    }
+    return false;
+  }
+  const Plan& pl = a.plan[k - a.k_begin];
+  int cnt2 = 0;
+  if (a.extended && b < a.nt2) cnt2 = (a.nt2 - b + G - 1) / G;
+  if (j < cnt2) {
+    J = PJob{2, (b + j * G) * TM, pl.c_lo, 0, (pl.c_hi - pl.c_lo + BK - 1) / BK, 0, 0, (float)pl.c_scale, 0};
+    return true;
+  }
+  idx = cnt2;
+  if (b >= a.p3_first) {
+    const int q = (b - a.p3_first) >> 1, h = (b - a.p3_first) & 1;
+    if (q < a.ns3 && h * TM < pl.r_hi - pl.r_lo && idx == j) {
+      J = PJob{3, pl.r_lo + h * TM, 0, (int)((int64_t)a.nkb_n * q / a.ns3), (int)((int64_t)a.nkb_n * (q + 1) / a.ns3), q,
+               h * TM, 0.f, 0};
+      return true;
+    }
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(NTW, 1)
+    k_rebk_mrhs_persistent(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAt,
+                           const __grid_constant__ CUtensorMap mZt, const __grid_constant__ CUtensorMap mXt,
+                           const __grid_constant__ CUtensorMap mUt, const __grid_constant__ CUtensorMap mRt,
+                           const __grid_constant__ PkArgs a) {
+  extern __shared__ float smem_raw[];
+  float* smem = aligned_smem(smem_raw);
+  __shared__ Pipe P;
+  __shared__ int s_crossed[RHS];
+  __shared__ volatile int s_stop;
+  __shared__ double s_err[4][RHS];
+  __shared__ float s_half[NRED];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x;
+  if (warp == 0) umma::tmem_alloc<256>(&P.tmem);
+  if (tid == 32) {
+    for (int q = 0; q < NSTAGE; ++q) {
+      mbar_init(&P.full[q], 1);
+      mbar_init(&P.conv[q], NCONV);
+      mbar_init(&P.empty[q], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&P.tfull[b], 1);
+      mbar_init(&P.tempty[b], 4);
+    }
+    fence_mbar_init();
+    s_stop = 0;
+  }
+  for (int c = tid; c < RHS; c += NTW) s_crossed[c] = (c < a.R) ? (a.iters[c] >= 0) : 1;
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = P.tmem;
+  // end of global phase p = 4 (k - k_begin) + {0 A, 1 B, 2 C, 3 D}
+  auto phase_end = [&](int64_t k, int ph) -> unsigned long long {
+    return (unsigned long long)G * (unsigned long long)(4 * (k - a.k_begin) + ph + 1);
+  };
+  auto a_raw = [&](int q) { return smem + (size_t)q * STAGE_FLOATS; };
+  auto a_lo = [&](int q) { return smem + (size_t)q * STAGE_FLOATS + TM * BK; };
+  auto b_raw = [&](int q) { return smem + (size_t)q * STAGE_FLOATS + 2 * TM * BK; };
+  auto b_lo = [&](int q) { return smem + (size_t)q * STAGE_FLOATS + 2 * TM * BK + RHS * BK; };
+  const int64_t k_last = a.k_end + 1;  // final round: P4(k_end) and its check only
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      uint32_t ph = 0;
+      int it = 0;
+      for (int64_t k = a.k_begin; k <= k_last; ++k) {
+        for (int phase = 0; phase < 2; ++phase) {
+          if (phase == 1) {
+            if (k == k_last) break;
+            gbar_wait(a.gbar, phase_end(k, 1));  // U ready (and the stop verdict)
+            pk_stamp(a, k, 6);
+            if (s_stop) break;
+          } else if (k > a.k_begin) {
+            gbar_wait(a.gbar, phase_end(k - 1, 3));  // R of the previous iteration ready
+            pk_stamp(a, k, 7);
+          }
+          fence_proxy_async_global();
+          PJob J;
+          for (int j = 0; pk_job(a, phase, k, j, J); ++j) {
+            const CUtensorMap* ma = (J.kind == 1 || J.kind == 4) ? &mAt : &mA;
+            const CUtensorMap* mb = J.kind == 1 ? &mZt : (J.kind == 2 ? &mUt : (J.kind == 3 ? &mXt : &mRt));
+            for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
+              const int q = it % NSTAGE;
+              if (it >= NSTAGE) {
+                mbar_wait(&P.empty[q], (ph >> q) & 1u);
+                ph ^= 1u << q;
+              }
+              mbar_arrive_expect_tx(&P.full[q], (TM + RHS) * BK * 4);
+              tma_load_2d(a_raw(q), ma, J.kc0 + kb * BK, J.row0, &P.full[q]);
+              tma_load_2d(b_raw(q), mb, kb * BK, 0, &P.full[q]);
+            }
+          }
+          // A is immutable and the block sequence known: pull the next
+          // phase's A boxes into L2 now, so HBM streams them during the
+          // barriers and reductions in between (B operands are not final yet)
+          if (a.prefetch) {
+            const int nph = phase ^ 1;
+            const int64_t nk = phase == 0 ? k : k + 1;
+            if (nk <= k_last && !(nph == 1 && nk == k_last))
+              for (int j = 0; pk_job(a, nph, nk, j, J); ++j) {
+                const CUtensorMap* ma = (J.kind == 1 || J.kind == 4) ? &mAt : &mA;
+                for (int kb = J.kb0; kb < J.kb1; ++kb) tma_prefetch_l2_2d(ma, J.kc0 + kb * BK, J.row0);
+              }
+          }
+        }
+        if (s_stop) break;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      const uint32_t idesc = umma::idesc_tf32(TM, RHS);
+      uint32_t phc = 0, pht = 0;
+      int it = 0, jt = 0;
+      for (int64_t k = a.k_begin; k <= k_last; ++k) {
+        for (int phase = 0; phase < 2; ++phase) {
+          if (phase == 1) {
+            if (k == k_last) break;
+            gbar_wait(a.gbar, phase_end(k, 1));
+            if (s_stop) break;
+          }
+          PJob J;
+          for (int j = 0; pk_job(a, phase, k, j, J); ++j, ++jt) {
+            const int b = jt & 1;
+            if (jt >= 2) {
+              mbar_wait(&P.tempty[b], (pht >> b) & 1u);
+              pht ^= 1u << b;
+            }
+            const uint32_t dh = tmem + b * 128, dl = dh + RHS;
+            for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
+              const int q = it % NSTAGE;
+              mbar_wait(&P.conv[q], (phc >> q) & 1u);
+              phc ^= 1u << q;
+              umma::fence_after_sync();
+              for (int ks = 0; ks < BK / 8; ++ks) {
+                const uint64_t ah = umma::make_desc_sw128(smem_u32(a_raw(q)) + 32 * ks);
+                const uint64_t al = umma::make_desc_sw128(smem_u32(a_lo(q)) + 32 * ks);
+                const uint64_t bh = umma::make_desc_sw128(smem_u32(b_raw(q)) + 32 * ks);
+                const uint64_t bl = umma::make_desc_sw128(smem_u32(b_lo(q)) + 32 * ks);
+                const bool acc = kb > J.kb0 || ks > 0;
+                umma::mma_tf32(dh, ah, bh, idesc, acc);
+                umma::mma_tf32(dl, ah, bl, idesc, acc);
+                umma::mma_tf32(dh, al, bh, idesc, true);
+              }
+              umma::commit(&P.empty[q]);
+            }
+            umma::commit(&P.tfull[b]);
+          }
+        }
+        if (s_stop) break;
+      }
+    }
+  } else {
+    // ---- converter warps (2-7) and epilogue warps (8-11); all of them run the reductions
+    const bool conv = warp < EPI0;
+    const int tr = tid - CONV0 * 32;  // 0 .. NRED-1
+    uint32_t phf = 0, pht = 0;
+    int it = 0, jt = 0;
+    for (int64_t k = a.k_begin; k <= k_last; ++k) {
+      for (int phase = 0; phase < 2; ++phase) {
+        if (phase == 1 && k == k_last) break;
+        PJob J;
+        if (conv) {
+          const int ct = tid - CONV0 * 32;
+          for (int j = 0; pk_job(a, phase, k, j, J); ++j)
+            for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
+              const int q = it % NSTAGE;
+              mbar_wait(&P.full[q], (phf >> q) & 1u);
+              phf ^= 1u << q;
+              constexpr int A4 = TM * BK / 4, B4 = RHS * BK / 4;
+              for (int e = ct; e < A4 + B4; e += NCONV * 32) {
+                const float4* src = e < A4 ? reinterpret_cast<const float4*>(a_raw(q)) + e
+                                           : reinterpret_cast<const float4*>(b_raw(q)) + (e - A4);
+                float4* dst =
+                    e < A4 ? reinterpret_cast<float4*>(a_lo(q)) + e : reinterpret_cast<float4*>(b_lo(q)) + (e - A4);
+                const float4 v = *src;
+                float4 l;
+                float h;
+                umma::split_tf32(v.x, h, l.x);
+                umma::split_tf32(v.y, h, l.y);
+                umma::split_tf32(v.z, h, l.z);
+                umma::split_tf32(v.w, h, l.w);
+                *dst = l;
+              }
+              fence_proxy_async();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&P.conv[q]);
+            }
+        } else {
+          const int ew = warp & 3, rlane = ew * 32;
+          for (int j = 0; pk_job(a, phase, k, j, J); ++j, ++jt) {
+            const int b = jt & 1;
+            mbar_wait(&P.tfull[b], (pht >> b) & 1u);
+            pht ^= 1u << b;
+            umma::fence_after_sync();
+            const uint32_t base = tmem + ((uint32_t)rlane << 16) + b * 128;
+            const int row = rlane + lane;
+            const bool any = J.kb1 > J.kb0;
+            const bool mode0 = J.kind == 1 || J.kind == 3;
+            float* part = J.kind == 1 ? a.part1 : a.part3;
+            float* Y = J.kind == 2 ? a.Zt : a.Xt;
+            const int64_t ldy = J.kind == 2 ? a.m : a.n;
+            const int r = J.row0 + row;
+            for (int c0 = 0; c0 < RHS; c0 += 16) {
+              float h[16], l[16];
+              umma::tmem_ld16(base + c0, h);
+              umma::tmem_ld16(base + RHS + c0, l);
+              if (mode0) {
+                float4* dst = reinterpret_cast<float4*>(part + ((size_t)J.slot * 256 + J.prow + row) * RHS + c0);
+#pragma unroll
+                for (int w = 0; w < 4; ++w)
+                  dst[w] = any ? make_float4(h[4 * w] + l[4 * w], h[4 * w + 1] + l[4 * w + 1],
+                                             h[4 * w + 2] + l[4 * w + 2], h[4 * w + 3] + l[4 * w + 3])
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+              } else {
+                const bool live = r < ldy;
+                double e2[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) e2[q] = 0.0;
+                if (live) {
+                  float y[16];
+#pragma unroll
+                  for (int q = 0; q < 16; ++q) y[q] = ld_cg_f32(Y + (size_t)(c0 + q) * ldy + r);
+                  if (any) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                      y[q] = y[q] - J.s * (h[q] + l[q]);
+                      __stcg(Y + (size_t)(c0 + q) * ldy + r, y[q]);
+                    }
+                  }
+                  if (J.check) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                      const double d = (double)y[q] - (double)__ldg(a.Xst + (size_t)(c0 + q) * ldy + r);
+                      e2[q] = d * d;
+                    }
+                  }
+                }
+                if (J.check) {
+#pragma unroll
+                  for (int q = 0; q < 16; ++q) {
+                    double v = e2[q];
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                    if (lane == 0) s_err[ew][c0 + q] = v;
+                  }
+                }
+              }
+            }
+            fence_proxy_async_global();
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&P.tempty[b]);
+            if (J.check) {
+              named_bar(1, 128);
+              if (tr - (EPI0 - CONV0) * 32 < RHS) {
+                const int c = tr - (EPI0 - CONV0) * 32;
+                a.errpart[(size_t)J.slot * RHS + c] = ((s_err[0][c] + s_err[1][c]) + s_err[2][c]) + s_err[3][c];
+              }
+              named_bar(1, 128);
+            }
+          }
+          // this CTA's part of the phase is written: arrive
+          named_bar(1, 128);
+          if (tid == EPI0 * 32) {
+            pk_stamp(a, k, phase == 0 ? 0 : 3);
+            // the counter is shared by all phases: a CTA with no jobs in this
+            // phase must not arrive before the previous phase has ended
+            // everywhere, or its arrival would stand in for a late one there
+            if (phase == 1) gbar_wait(a.gbar, phase_end(k, 1));
+            else if (k > a.k_begin) gbar_wait(a.gbar, phase_end(k - 1, 3));
+            gbar_arrive(a.gbar);
+          }
+        }
+        // ---- reduction phase (B after A, D after C): one thread polls
+#ifdef PK_ALLPOLL
+        gbar_wait(a.gbar, phase_end(k, phase == 0 ? 0 : 2));
+#else
+        if (tr == 0) {
+          gbar_wait(a.gbar, phase_end(k, phase == 0 ? 0 : 2));
+          pk_stamp(a, k, phase == 0 ? 1 : 4);
+        }
+#endif
+        __syncwarp();
+        named_bar(2, NRED);
+        const int b = blockIdx.x;
+        if (phase == 0) {
+          // stop check of iteration k-1 (every CTA, same bits)
+          if (k - 1 >= a.k_begin && pk_is_check(a, k - 1)) {
+            if (tr < a.R) {
+              double s = 0.0;
+#pragma unroll 8
+              for (int t = 0; t < a.nt4; ++t) s += ld_cg_f64(a.errpart + (size_t)t * RHS + tr);
+              const double e = sqrt(s);
+              if (!s_crossed[tr] && e <= a.tol[tr]) {
+                s_crossed[tr] = 1;
+                if (b == 0) {
+                  a.iters[tr] = k - 1;
+                  a.errs_at[tr] = e;
+                }
+              }
+            }
+            named_bar(2, NRED);
+            if (tr == 0) {
+              int all = 1;
+              for (int c = 0; c < a.R; ++c) all &= s_crossed[c];
+              if (all) {
+                s_stop = 1;
+                if (b == 0) {
+                  *a.k_final = k - 1;
+                  *a.stopped = 1;
+                }
+              }
+            }
+          }
+          // U = Σ_q part1[q]: 128 chunks of 128 entries, two K halves per entry
+          if (a.extended && k <= a.k_end) {
+            const Plan& pl = a.plan[k - a.k_begin];
+            const int nJ = pl.c_hi - pl.c_lo;
+            const int e_loc = tr & 127, hf = tr >> 7;
+            for (int ch = b; ch < 256 * RHS / 128; ch += G) {
+              const int e = ch * 128 + e_loc, j = e / RHS, c = e % RHS;
+              float s = 0.f;
+              if (hf < 2 && j < nJ) {
+                const int q0 = hf ? a.ns1 / 2 : 0, q1 = hf ? a.ns1 : a.ns1 / 2;
+#pragma unroll 8
+                for (int q = q0; q < q1; ++q) s += ld_cg_f32(a.part1 + ((size_t)q * 256 + j) * RHS + c);
+              }
+              if (hf == 1) s_half[e_loc] = s;
+              named_bar(2, NRED);
+              if (hf == 0) a.Ut[(size_t)c * 256 + j] = s + s_half[e_loc];
+              named_bar(2, NRED);
+            }
+          }
+        } else {
+          // R = ((Σ_q part3[q]) - B_I) + Z_I  (solvers.py:291-293 order), zero past |I|
+          const Plan& pl = a.plan[k - a.k_begin];
+          const int nI = pl.r_hi - pl.r_lo;
+          const int e_loc = tr & 127, hf = tr >> 7;
+          for (int ch = b; ch < 256 * RHS / 128; ch += G) {
+            const int e = ch * 128 + e_loc, i = e / RHS, c = e % RHS;
+            float s = 0.f;
+            if (hf < 2 && i < nI) {
+              const int q0 = hf ? a.ns3 / 2 : 0, q1 = hf ? a.ns3 : a.ns3 / 2;
+#pragma unroll 8
+              for (int q = q0; q < q1; ++q) s += ld_cg_f32(a.part3 + ((size_t)q * 256 + i) * RHS + c);
+            }
+            if (hf == 1) s_half[e_loc] = s;
+            named_bar(2, NRED);
+            if (hf == 0) {
+              float v = 0.f;
+              if (i < nI) {
+                v = (s + s_half[e_loc]) - a.Bt[(size_t)c * a.m + pl.r_lo + i];
+                if (a.extended) v += ld_cg_f32(a.Zt + (size_t)c * a.m + pl.r_lo + i);
+              }
+              a.Rt[(size_t)c * 256 + i] = v;
+            }
+            named_bar(2, NRED);
+          }
+        }
+        fence_proxy_async_global();
+        named_bar(2, NRED);
+        if (tr == 0) {
+          pk_stamp(a, k, phase == 0 ? 2 : 5);
+          gbar_arrive(a.gbar);
+        }
+        if (phase == 0 && (s_stop || k == k_last)) break;
+      }
+      if (s_stop || k == k_last) break;
+    }
+    if (tr == 0 && blockIdx.x == 0 && !s_stop) *a.k_final = a.k_end;
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc<256>(tmem);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -541,6 +1046,19 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
     return e;
   };
 
+  // persistent whole-run kernel (default): one cooperative launch per chunk
+  // of up to 2^20 iterations; REBK_MRHS_PK=0 selects the per-product kernels
+  const char* pk_env = getenv("REBK_MRHS_PK");
+  const int G = nsm & ~1;
+  const int nt2 = (int)((m + TM - 1) / TM), nt4 = (int)((n + TM - 1) / TM);
+  bool use_pk = !(pk_env && pk_env[0] == '0') && G >= 2 && nt4 <= G && !(dbg & 3);
+  if (use_pk) {
+    TC_TRY(cudaFuncSetAttribute(k_rebk_mrhs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    int occ = 0;
+    TC_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rebk_mrhs_persistent, NTW, SMEM_BYTES));
+    use_pk = occ >= 1;
+  }
+
   cudaEvent_t ev0, ev1;
   TC_TRY(cudaEventCreate(&ev0));
   TC_TRY(cudaEventCreate(&ev1));
@@ -556,6 +1074,106 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
       all_done = true;
       K = 0;
     }
+  }
+  if (use_pk && !all_done && cfg->max_iters > 0) {
+    PkArgs pa{};
+    pa.m = (int)m;
+    pa.n = (int)n;
+    pa.nkb_m = nkb_m;
+    pa.nkb_n = nkb_n;
+    pa.extended = w.extended;
+    pa.checking = checking;
+    pa.stride = (int)cfg->check_stride;
+    pa.max_iters = cfg->max_iters;
+    pa.ns1 = std::max(1, std::min(G / 2, nkb_m));
+    pa.p3_first = 0;
+    if (w.extended && nt2 % G != 0) pa.p3_first = std::min(G - 2, ((nt2 % G) + 1) & ~1);
+    pa.ns3 = std::max(1, std::min((G - pa.p3_first) / 2, nkb_n));
+    pa.nt2 = nt2;
+    pa.nt4 = nt4;
+    pa.R = R;
+    pa.Zt = Zt;
+    pa.Xt = Xt;
+    pa.Ut = Ut;
+    pa.Rt = Rt;
+    pa.Bt = Bt;
+    pa.Xst = Xst;
+    pa.tol = d_tol;
+    pa.iters = d_iters;
+    pa.errs_at = d_errs_at;
+    float *p1 = nullptr, *p3 = nullptr;
+    double* ep = nullptr;
+    int64_t* d_kf = nullptr;
+    int32_t* d_stopped = nullptr;
+    unsigned long long* d_gbar = nullptr;
+    Plan* d_plan_all = nullptr;
+    const int64_t CHK = std::min<int64_t>(cfg->max_iters, (int64_t)1 << 20);
+    TC_TRY(cudaMallocAsync((void**)&p1, sizeof(float) * (size_t)pa.ns1 * 256 * RHS, stream));
+    TC_TRY(cudaMallocAsync((void**)&p3, sizeof(float) * (size_t)pa.ns3 * 256 * RHS, stream));
+    TC_TRY(cudaMallocAsync((void**)&ep, sizeof(double) * (size_t)nt4 * RHS, stream));
+    TC_TRY(cudaMallocAsync((void**)&d_kf, sizeof(int64_t), stream));
+    TC_TRY(cudaMallocAsync((void**)&d_stopped, sizeof(int32_t), stream));
+    TC_TRY(cudaMallocAsync((void**)&d_gbar, sizeof(unsigned long long), stream));
+    TC_TRY(cudaMallocAsync((void**)&d_plan_all, sizeof(Plan) * CHK, stream));
+    TC_TRY(cudaMemsetAsync(d_stopped, 0, sizeof(int32_t), stream));
+    pa.part1 = p1;
+    pa.part3 = p3;
+    pa.errpart = ep;
+    pa.k_final = d_kf;
+    pa.stopped = d_stopped;
+    pa.gbar = d_gbar;
+    pa.plan = d_plan_all;
+    const char* pf_env = getenv("REBK_PK_PREFETCH");
+    pa.prefetch = pf_env ? atoi(pf_env) : 1;
+    const char* tr_env = getenv("REBK_PK_TRACE");
+    pa.trace_n = tr_env ? atoi(tr_env) : 0;
+    pa.trace_k0 = 100;
+    unsigned long long* d_tr = nullptr;
+    if (pa.trace_n > 0) {
+      TC_TRY(cudaMallocAsync((void**)&d_tr, sizeof(unsigned long long) * pa.trace_n * G * 8, stream));
+      TC_TRY(cudaMemsetAsync(d_tr, 0, sizeof(unsigned long long) * pa.trace_n * G * 8, stream));
+      pa.trace = d_tr;
+    }
+    for (int64_t k0 = 1; k0 <= cfg->max_iters; k0 += CHK) {
+      const int64_t cnt = std::min(CHK, cfg->max_iters - k0 + 1);
+      TC_TRY(launch_sample_plan(sp_template, k0, cnt, d_plan_all, nullptr, stream));
+      TC_TRY(cudaMemsetAsync(d_gbar, 0, sizeof(unsigned long long), stream));
+      pa.k_begin = k0;
+      pa.k_end = k0 + cnt - 1;
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(G);
+      lc.blockDim = dim3(NTW);
+      lc.dynamicSmemBytes = SMEM_BYTES;
+      lc.stream = stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      TC_TRY(cudaLaunchKernelEx(&lc, k_rebk_mrhs_persistent, mA, mAt, w.extended ? mZt : mXt, mXt,
+                                mUt, mRt, pa));
+      int32_t st = 0;
+      int64_t kf = 0;
+      TC_TRY(cudaMemcpyAsync(&st, d_stopped, sizeof st, cudaMemcpyDeviceToHost, stream));
+      TC_TRY(cudaMemcpyAsync(&kf, d_kf, sizeof kf, cudaMemcpyDeviceToHost, stream));
+      TC_TRY(cudaStreamSynchronize(stream));
+      K = kf;
+      if (st) break;
+    }
+    if (d_tr) {
+      std::vector<unsigned long long> h((size_t)pa.trace_n * G * 8);
+      TC_TRY(cudaMemcpy(h.data(), d_tr, h.size() * 8, cudaMemcpyDeviceToHost));
+      const char* fn = getenv("REBK_PK_TRACE_FILE");
+      FILE* f = fopen(fn ? fn : "pk_trace.bin", "wb");
+      if (f) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+      }
+      cudaFree(d_tr);
+    }
+    all_done = true;  // skip the per-product loop below
+    for (void* ptr : {(void*)p1, (void*)p3, (void*)ep, (void*)d_kf, (void*)d_stopped, (void*)d_gbar, (void*)d_plan_all})
+      cudaFreeAsync(ptr, stream);
   }
   std::vector<Plan> hplan(CH);
   for (int64_t k0 = 1; !all_done && k0 <= cfg->max_iters; k0 += CH) {
