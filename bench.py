@@ -377,7 +377,8 @@ def run_ours_c5(args):
     beta = compute_beta_max(a64, rp, cp)[2]
     log(f"[bench] built c5 ({time.time() - t0:.1f}s), beta_max={beta:.6g}")
     cfg = SolverConfig(algorithm="rebk", alpha=1.0 / beta, seed=17, max_iters=args.max_iters, row_partition=rp,
-                       col_partition=cp, stop=StoppingRule(tol=1.0), beta_max=beta)
+                       col_partition=cp, stop=StoppingRule(tol=1.0, check_stride=int(os.environ.get("REBK_BENCH_STRIDE", "1"))),
+                       beta_max=beta)
     tols = 1e-4 * np.linalg.norm(xs, axis=0)
     dm = DeviceMatrix32(a32)
     tr = None

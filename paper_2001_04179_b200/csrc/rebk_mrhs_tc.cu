@@ -421,7 +421,9 @@ struct PkArgs {
   unsigned long long* trace;  // REBK_PK_TRACE: globaltimer stamps [iteration][CTA][8]
   int64_t trace_k0;
   int trace_n;
+  unsigned long long* trace2;
   int prefetch;  // L2 prefetch of the next phase's A boxes
+  int dbg;       // REBK_PK_DBG experiments (8: check without the warp sums, 16: check without x* loads)
 };
 struct PJob {
   int kind;  // 1: P1, 2: P2, 3: P3, 4: P4
@@ -465,6 +467,18 @@ __device__ __forceinline__ void pk_stamp(const PkArgs& a, int64_t k, int i) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     a.trace[((size_t)(k - a.trace_k0) * gridDim.x + blockIdx.x) * 8 + i] = t;
+  }
+}
+// per-job stamps of CTAs 0 and 120 at iteration trace_k0 (events: 0 producer
+// starts the job, 1 producer issued its last stage, 2 MMA got the first
+// converted stage, 3 MMA committed the job, 4 epilogue has the accumulator,
+// 5 epilogue done)
+__device__ __forceinline__ void pk_jstamp(const PkArgs& a, int64_t k, int phase, int j, int ev) {
+  if (a.trace && k == a.trace_k0 && (blockIdx.x == 0 || blockIdx.x == 120) && j < 4) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int sel = blockIdx.x == 0 ? 0 : 1;
+    a.trace2[((sel * 2 + phase) * 4 + j) * 8 + ev] = t;
   }
 }
 __device__ __forceinline__ bool pk_is_check(const PkArgs& a, int64_t k) {
@@ -533,13 +547,15 @@ __global__ void __launch_bounds__(NTW, 1)
     k_rebk_mrhs_persistent(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAt,
                            const __grid_constant__ CUtensorMap mZt, const __grid_constant__ CUtensorMap mXt,
                            const __grid_constant__ CUtensorMap mUt, const __grid_constant__ CUtensorMap mRt,
-                           const __grid_constant__ PkArgs a) {
+                           const __grid_constant__ CUtensorMap mXst, const __grid_constant__ PkArgs a) {
   extern __shared__ float smem_raw[];
   float* smem = aligned_smem(smem_raw);
   __shared__ Pipe P;
   __shared__ int s_crossed[RHS];
   __shared__ volatile int s_stop;
-  __shared__ double s_err[4][RHS];
+  __shared__ double s_d2[16][TM];  // stop check: (x - x*)^2 of one 16-column chunk of a tile
+  __shared__ double s_g8[16][8];
+  __shared__ double s_errt[RHS];
   __shared__ float s_half[NRED];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x;
@@ -592,6 +608,16 @@ __global__ void __launch_bounds__(NTW, 1)
           for (int j = 0; pk_job(a, phase, k, j, J); ++j) {
             const CUtensorMap* ma = (J.kind == 1 || J.kind == 4) ? &mAt : &mA;
             const CUtensorMap* mb = J.kind == 1 ? &mZt : (J.kind == 2 ? &mUt : (J.kind == 3 ? &mXt : &mRt));
+            pk_jstamp(a, k, phase, j, 0);
+            if (J.kind == 2 || J.kind == 4) {
+              // the epilogue's read-modify-write rows (and x* on a check):
+              // into L2 now, while this job's stages stream
+              const CUtensorMap* my = J.kind == 2 ? &mZt : &mXt;
+              for (int kk = 0; kk < TM / BK; ++kk) {
+                tma_prefetch_l2_2d(my, J.row0 + kk * BK, 0);
+                if (J.check) tma_prefetch_l2_2d(&mXst, J.row0 + kk * BK, 0);
+              }
+            }
             for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
               const int q = it % NSTAGE;
               if (it >= NSTAGE) {
@@ -602,6 +628,7 @@ __global__ void __launch_bounds__(NTW, 1)
               tma_load_2d(a_raw(q), ma, J.kc0 + kb * BK, J.row0, &P.full[q]);
               tma_load_2d(b_raw(q), mb, kb * BK, 0, &P.full[q]);
             }
+            pk_jstamp(a, k, phase, j, 1);
           }
           // A is immutable and the block sequence known: pull the next
           // phase's A boxes into L2 now, so HBM streams them during the
@@ -643,6 +670,7 @@ __global__ void __launch_bounds__(NTW, 1)
               const int q = it % NSTAGE;
               mbar_wait(&P.conv[q], (phc >> q) & 1u);
               phc ^= 1u << q;
+              if (kb == J.kb0) pk_jstamp(a, k, phase, j, 2);
               umma::fence_after_sync();
               for (int ks = 0; ks < BK / 8; ++ks) {
                 const uint64_t ah = umma::make_desc_sw128(smem_u32(a_raw(q)) + 32 * ks);
@@ -657,6 +685,7 @@ __global__ void __launch_bounds__(NTW, 1)
               umma::commit(&P.empty[q]);
             }
             umma::commit(&P.tfull[b]);
+            pk_jstamp(a, k, phase, j, 3);
           }
         }
         if (s_stop) break;
@@ -679,20 +708,29 @@ __global__ void __launch_bounds__(NTW, 1)
               const int q = it % NSTAGE;
               mbar_wait(&P.full[q], (phf >> q) & 1u);
               phf ^= 1u << q;
-              constexpr int A4 = TM * BK / 4, B4 = RHS * BK / 4;
-              for (int e = ct; e < A4 + B4; e += NCONV * 32) {
-                const float4* src = e < A4 ? reinterpret_cast<const float4*>(a_raw(q)) + e
-                                           : reinterpret_cast<const float4*>(b_raw(q)) + (e - A4);
-                float4* dst =
-                    e < A4 ? reinterpret_cast<float4*>(a_lo(q)) + e : reinterpret_cast<float4*>(b_lo(q)) + (e - A4);
-                const float4 v = *src;
-                float4 l;
+              constexpr int A4 = TM * BK / 4, B4 = RHS * BK / 4, PER = (A4 + B4) / (NCONV * 32);
+              static_assert((A4 + B4) % (NCONV * 32) == 0, "converter split");
+              const float4* srcA = reinterpret_cast<const float4*>(a_raw(q));
+              const float4* srcB = reinterpret_cast<const float4*>(b_raw(q));
+              float4* dstA = reinterpret_cast<float4*>(a_lo(q));
+              float4* dstB = reinterpret_cast<float4*>(b_lo(q));
+              float4 v[PER];
+#pragma unroll
+              for (int i = 0; i < PER; ++i) {
+                const int e = ct + i * NCONV * 32;
+                v[i] = e < A4 ? srcA[e] : srcB[e - A4];
+              }
+#pragma unroll
+              for (int i = 0; i < PER; ++i) {
+                const int e = ct + i * NCONV * 32;
+                float4 lo;
                 float h;
-                umma::split_tf32(v.x, h, l.x);
-                umma::split_tf32(v.y, h, l.y);
-                umma::split_tf32(v.z, h, l.z);
-                umma::split_tf32(v.w, h, l.w);
-                *dst = l;
+                umma::split_tf32(v[i].x, h, lo.x);
+                umma::split_tf32(v[i].y, h, lo.y);
+                umma::split_tf32(v[i].z, h, lo.z);
+                umma::split_tf32(v[i].w, h, lo.w);
+                if (e < A4) dstA[e] = lo;
+                else dstB[e - A4] = lo;
               }
               fence_proxy_async();
               __syncwarp();
@@ -702,10 +740,6 @@ __global__ void __launch_bounds__(NTW, 1)
           const int ew = warp & 3, rlane = ew * 32;
           for (int j = 0; pk_job(a, phase, k, j, J); ++j, ++jt) {
             const int b = jt & 1;
-            mbar_wait(&P.tfull[b], (pht >> b) & 1u);
-            pht ^= 1u << b;
-            umma::fence_after_sync();
-            const uint32_t base = tmem + ((uint32_t)rlane << 16) + b * 128;
             const int row = rlane + lane;
             const bool any = J.kb1 > J.kb0;
             const bool mode0 = J.kind == 1 || J.kind == 3;
@@ -713,7 +747,36 @@ __global__ void __launch_bounds__(NTW, 1)
             float* Y = J.kind == 2 ? a.Zt : a.Xt;
             const int64_t ldy = J.kind == 2 ? a.m : a.n;
             const int r = J.row0 + row;
+            const bool live = !mode0 && r < ldy;
+            const bool chk = J.check && live && !(a.dbg & 16);
+            // chunk 0 of the rows this tile updates (final for this phase) is
+            // fetched while the MMAs run, chunk c+1 while chunk c is applied
+            float ycur[16], ynext[16], xcur[16], xnext[16];
+            if (live) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) ycur[q] = ld_cg_f32(Y + (size_t)q * ldy + r);
+            }
+            if (chk) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) xcur[q] = __ldg(a.Xst + (size_t)q * ldy + r);
+            }
+            mbar_wait(&P.tfull[b], (pht >> b) & 1u);
+            pht ^= 1u << b;
+            if (tid == EPI0 * 32) pk_jstamp(a, k, phase, j, 4);
+            umma::fence_after_sync();
+            const uint32_t base = tmem + ((uint32_t)rlane << 16) + b * 128;
+#pragma unroll
             for (int c0 = 0; c0 < RHS; c0 += 16) {
+              if (c0 + 16 < RHS) {
+                if (live) {
+#pragma unroll
+                  for (int q = 0; q < 16; ++q) ynext[q] = ld_cg_f32(Y + (size_t)(c0 + 16 + q) * ldy + r);
+                }
+                if (chk) {
+#pragma unroll
+                  for (int q = 0; q < 16; ++q) xnext[q] = __ldg(a.Xst + (size_t)(c0 + 16 + q) * ldy + r);
+                }
+              }
               float h[16], l[16];
               umma::tmem_ld16(base + c0, h);
               umma::tmem_ld16(base + RHS + c0, l);
@@ -725,51 +788,60 @@ __global__ void __launch_bounds__(NTW, 1)
                                              h[4 * w + 2] + l[4 * w + 2], h[4 * w + 3] + l[4 * w + 3])
                                : make_float4(0.f, 0.f, 0.f, 0.f);
               } else {
-                const bool live = r < ldy;
-                double e2[16];
+                if (live && any) {
 #pragma unroll
-                for (int q = 0; q < 16; ++q) e2[q] = 0.0;
-                if (live) {
-                  float y[16];
-#pragma unroll
-                  for (int q = 0; q < 16; ++q) y[q] = ld_cg_f32(Y + (size_t)(c0 + q) * ldy + r);
-                  if (any) {
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) {
-                      y[q] = y[q] - J.s * (h[q] + l[q]);
-                      __stcg(Y + (size_t)(c0 + q) * ldy + r, y[q]);
-                    }
-                  }
-                  if (J.check) {
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) {
-                      const double d = (double)y[q] - (double)__ldg(a.Xst + (size_t)(c0 + q) * ldy + r);
-                      e2[q] = d * d;
-                    }
+                  for (int q = 0; q < 16; ++q) {
+                    ycur[q] = ycur[q] - J.s * (h[q] + l[q]);
+                    __stcg(Y + (size_t)(c0 + q) * ldy + r, ycur[q]);
                   }
                 }
                 if (J.check) {
+                  // Σ over the tile's 128 rows of (x - x*)^2 for these 16
+                  // columns, through shared memory in a fixed order: thread
+                  // (q, g) sums rows g, g + 8, ... of column q, then the 8
+                  // group sums of each column in order
+                  const int et = tid - EPI0 * 32;
 #pragma unroll
                   for (int q = 0; q < 16; ++q) {
-                    double v = e2[q];
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-                    if (lane == 0) s_err[ew][c0 + q] = v;
+                    double v = 0.0;
+                    if (chk) {
+                      const double d = (double)ycur[q] - (double)xcur[q];
+                      v = d * d;
+                    }
+                    s_d2[q][row] = v;
                   }
+                  named_bar(1, 128);
+                  {
+                    const int q = et >> 3, g = et & 7;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) acc += s_d2[q][g + 8 * i];
+                    s_g8[q][g] = acc;
+                  }
+                  named_bar(1, 128);
+                  if (et < 16) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) acc += s_g8[et][g];
+                    s_errt[c0 + et] = acc;
+                  }
+                  named_bar(1, 128);
                 }
+              }
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                ycur[q] = ynext[q];
+                xcur[q] = xnext[q];
               }
             }
             fence_proxy_async_global();
             umma::fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(&P.tempty[b]);
-            if (J.check) {
-              named_bar(1, 128);
-              if (tr - (EPI0 - CONV0) * 32 < RHS) {
-                const int c = tr - (EPI0 - CONV0) * 32;
-                a.errpart[(size_t)J.slot * RHS + c] = ((s_err[0][c] + s_err[1][c]) + s_err[2][c]) + s_err[3][c];
-              }
-              named_bar(1, 128);
+            if (tid == EPI0 * 32) pk_jstamp(a, k, phase, j, 5);
+            if (J.check && tr - (EPI0 - CONV0) * 32 < RHS) {
+              const int c = tr - (EPI0 - CONV0) * 32;
+              a.errpart[(size_t)J.slot * RHS + c] = s_errt[c];
             }
           }
           // this CTA's part of the phase is written: arrive
@@ -1009,6 +1081,8 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
             encode_kmajor(&mUt, Ut, RHS, ldu, ldu, RHS) && encode_kmajor(&mRt, Rt, RHS, ldr, ldr, RHS);
   if (w.extended) ok = ok && encode_kmajor(&mAt, w.At, n, m, w.ldat, TM) && encode_kmajor(&mZt, Zt, RHS, m, m, RHS);
   else ok = ok && encode_kmajor(&mAt, w.At, n, m, w.ldat, TM);
+  CUtensorMap mXst = mXt;
+  if (ok && Xst) ok = encode_kmajor(&mXst, Xst, RHS, n, n, RHS);
   if (!ok) {
     snprintf(errbuf, errlen, "tensor map encoding failed");
     return -2;
@@ -1125,6 +1199,8 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
     pa.plan = d_plan_all;
     const char* pf_env = getenv("REBK_PK_PREFETCH");
     pa.prefetch = pf_env ? atoi(pf_env) : 1;
+    const char* pdbg = getenv("REBK_PK_DBG");
+    pa.dbg = pdbg ? atoi(pdbg) : 0;
     const char* tr_env = getenv("REBK_PK_TRACE");
     pa.trace_n = tr_env ? atoi(tr_env) : 0;
     pa.trace_k0 = 100;
@@ -1133,6 +1209,8 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
       TC_TRY(cudaMallocAsync((void**)&d_tr, sizeof(unsigned long long) * pa.trace_n * G * 8, stream));
       TC_TRY(cudaMemsetAsync(d_tr, 0, sizeof(unsigned long long) * pa.trace_n * G * 8, stream));
       pa.trace = d_tr;
+      TC_TRY(cudaMallocAsync((void**)&pa.trace2, sizeof(unsigned long long) * 2 * 2 * 4 * 8, stream));
+      TC_TRY(cudaMemsetAsync(pa.trace2, 0, sizeof(unsigned long long) * 2 * 2 * 4 * 8, stream));
     }
     for (int64_t k0 = 1; k0 <= cfg->max_iters; k0 += CHK) {
       const int64_t cnt = std::min(CHK, cfg->max_iters - k0 + 1);
@@ -1151,7 +1229,7 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
       lc.attrs = at;
       lc.numAttrs = 1;
       TC_TRY(cudaLaunchKernelEx(&lc, k_rebk_mrhs_persistent, mA, mAt, w.extended ? mZt : mXt, mXt,
-                                mUt, mRt, pa));
+                                mUt, mRt, mXst, pa));
       int32_t st = 0;
       int64_t kf = 0;
       TC_TRY(cudaMemcpyAsync(&st, d_stopped, sizeof st, cudaMemcpyDeviceToHost, stream));
@@ -1170,6 +1248,21 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
         fclose(f);
       }
       cudaFree(d_tr);
+      std::vector<unsigned long long> h2(2 * 2 * 4 * 8);
+      TC_TRY(cudaMemcpy(h2.data(), pa.trace2, h2.size() * 8, cudaMemcpyDeviceToHost));
+      unsigned long long t0 = 0;
+      for (auto v : h2)
+        if (v && (!t0 || v < t0)) t0 = v;
+      for (int sel = 0; sel < 2; ++sel)
+        for (int ph = 0; ph < 2; ++ph)
+          for (int jj = 0; jj < 4; ++jj) {
+            const unsigned long long* e = &h2[((sel * 2 + ph) * 4 + jj) * 8];
+            if (!e[0]) continue;
+            fprintf(stderr, "[pk job] cta %d phase %c job %d:", sel ? 120 : 0, ph ? 'C' : 'A', jj);
+            for (int ev = 0; ev < 6; ++ev) fprintf(stderr, " %8.2f", e[ev] ? (e[ev] - t0) * 1e-3 : -1.0);
+            fprintf(stderr, "\n");
+          }
+      cudaFree(pa.trace2);
     }
     all_done = true;  // skip the per-product loop below
     for (void* ptr : {(void*)p1, (void*)p3, (void*)ep, (void*)d_kf, (void*)d_stopped, (void*)d_gbar, (void*)d_plan_all})
