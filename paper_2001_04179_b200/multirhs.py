@@ -25,7 +25,8 @@ from .matrix import Matrix
 from .problems import ProblemInstance, ProblemMeta
 from .solvers import SolverConfig, SolverContext
 
-KERNEL_PATHS = {4: "cuBLAS FP32 GEMMs", 5: "cuBLAS FP32 GEMMs emulated on BF16 tensor cores (BF16x9)"}
+KERNEL_PATHS = {4: "cuBLAS FP32 GEMMs", 5: "cuBLAS FP32 GEMMs emulated on BF16 tensor cores (BF16x9)",
+                8: "hand-written tcgen05 kind::tf32 kernels, 3xTF32 (persistent whole-run kernel by default)"}
 
 
 class DeviceMatrix32:

@@ -398,6 +398,67 @@ def test_multi_rhs_fp32_matches_reference_columns():
             assert rel(tr.X[:, c], g["x_K"][:, c]) <= 1e-4
 
 
+def _mini_mrhs(algorithm="rebk", blk=64, m=6000, n=600, R=8, max_iters=40, stride=1, mode="max_iters_only"):
+    from paper_2001_04179_b200.multirhs import DeviceMatrix32
+    from paper_2001_04179_b200.workloads import c5_arrays
+
+    a32, b32, xs = c5_arrays(m, n, R)
+    rp = P.contiguous_partition(m, blk, "row")
+    cp = P.contiguous_partition(n, blk, "col") if algorithm in ("rebk", "rek") else None
+    a64 = P.Matrix.from_dense(a32.astype(np.float64))
+    beta = 0.02
+    kw = dict(algorithm=algorithm, alpha=1.0 / beta, seed=17, max_iters=max_iters, row_partition=rp,
+              stop=P.StoppingRule(mode=mode, tol=1.0, check_stride=stride), beta_max=beta)
+    if cp is not None:
+        kw["col_partition"] = cp
+    return a32, b32, xs, a64, DeviceMatrix32(a32), P.SolverConfig(**kw)
+
+
+@pytest.mark.parametrize("algorithm,blk", [("rebk", 64), ("rebk", 100), ("rebk", 256), ("rabk", 64)])
+def test_multi_rhs_persistent_kernel_matches_per_product_kernels(monkeypatch, algorithm, blk):
+    """The persistent whole-run tcgen05 kernel (default) and the per-product
+    kernels compute the same iteration: X (and Z) after 40 iterations agree
+    to fp32 rounding of the different split-K orders; the persistent kernel
+    replays bit for bit.  Ragged blocks (100), blocks wider than one 128-row
+    MMA tile (256) and the no-column-sweep RABK variant included."""
+    from paper_2001_04179_b200.multirhs import run_multi
+
+    a32, b32, xs, a64, dm, cfg = _mini_mrhs(algorithm, blk)
+    monkeypatch.setenv("REBK_MRHS_PK", "1")
+    t1 = run_multi(a32, b32, cfg, device_matrix=dm, a64=a64)
+    t1b = run_multi(a32, b32, cfg, device_matrix=dm, a64=a64)
+    monkeypatch.setenv("REBK_MRHS_PK", "0")
+    t0 = run_multi(a32, b32, cfg, device_matrix=dm, a64=a64)
+    assert t1.iters == t0.iters == 40
+    assert np.array_equal(t1.X, t1b.X)
+    assert rel(t1.X, t0.X) <= 1e-5
+    if algorithm == "rebk":
+        assert np.array_equal(t1.Z, t1b.Z)
+        assert rel(t1.Z, t0.Z) <= 1e-5
+
+
+def test_multi_rhs_persistent_stop_state(monkeypatch):
+    """Per-column stopping inside the persistent kernel: with a check stride
+    of 7 the run ends at the first multiple of 7 (or max_iters) at which
+    every column has crossed, and X at that iteration equals a
+    max_iters-only run of exactly that many iterations."""
+    from paper_2001_04179_b200.multirhs import run_multi
+
+    g = load("c5mini_golden.npz")
+    a32, b32, xs, a64, dm, cfg = _mini_mrhs("rebk", 64, max_iters=50_000, stride=7, mode="oracle_error")
+    cfg.alpha = float(g["alpha"])
+    monkeypatch.setenv("REBK_MRHS_PK", "1")
+    t = run_multi(a32, b32, cfg, X_star=xs, tols=g["tols"], device_matrix=dm, a64=a64)
+    assert t.converged and t.iters % 7 == 0
+    assert np.all(t.iters_per_rhs % 7 == 0) and t.iters == t.iters_per_rhs.max()
+    assert np.all(np.abs(t.iters_per_rhs - g["iters"]) <= 7)
+    cfg2 = P.SolverConfig(algorithm="rebk", alpha=cfg.alpha, seed=17, max_iters=int(t.iters),
+                          row_partition=cfg.row_partition, col_partition=cfg.col_partition,
+                          stop=P.StoppingRule(mode="max_iters_only"), beta_max=cfg.beta_max)
+    t2 = run_multi(a32, b32, cfg2, device_matrix=dm, a64=a64)
+    assert np.array_equal(t.X, t2.X) and np.array_equal(t.Z, t2.Z)
+
+
 @pytest.mark.parametrize("ranks", [1, 2, 4])
 def test_sharded_kernels_c1(ranks):
     """Config-3 layout (interleaved row shards, u and dx allreduced) on the
