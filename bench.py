@@ -283,7 +283,14 @@ def run_ours(args):
     kernel_ms = loop_ms_total / args.steps
     achieved = bytes_per_iter * per_solve_iters / (kernel_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
-    traffic = profiled_traffic(args.workload)
+    tr_info = profiled_traffic(args.workload)
+    traffic = None
+    if isinstance(tr_info, dict) and tr_info.get("bytes_per_iter"):
+        # per launch like `achieved`: the ncu per-iteration figure x the
+        # iterations one launch of this run covers
+        traffic = float(tr_info["bytes_per_iter"]) * per_solve_iters
+    elif isinstance(tr_info, (int, float)):
+        traffic = float(tr_info)
 
     # e2e through the public API from pinned host buffers, A re-uploaded each step
     e2e = None
@@ -345,6 +352,7 @@ def run_ours(args):
             "achieved_gbps": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_note": (tr_info or {}).get("note") if isinstance(tr_info, dict) else None,
                          "kernel": ["rebk_dense_kernel", "rebk_dense_fast_kernel", "rebk_dense_fast_kernel",
                                     "rebk_csr_kernel", "", "", "rebk_dense_split_kernel",
                                     "rebk_dense_stream_kernel"][int(tr.kernel_path)],

@@ -37,7 +37,13 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// REBK_STATIC_CLUSTER (profiling builds, tools/build_variants.sh): the cluster
+// shape is a kernel attribute instead of a launch attribute; ncu replays the
+// kernel with its clusters only in this form
 __global__ void __launch_bounds__(kSplitThreads, 1)
+#ifdef REBK_STATIC_CLUSTER
+    __cluster_dims__(REBK_STATIC_CLUSTER, 1, 1)
+#endif
     rebk_dense_split_kernel(const __grid_constant__ SplitParams spp, const __grid_constant__ CUtensorMap tm_ct,
                             const __grid_constant__ CUtensorMap tm_rt) {
   extern __shared__ __align__(128) double sm[];
@@ -554,6 +560,11 @@ cudaError_t launch_dense_split(const SplitParams& sp, const CUtensorMap& tm_ct, 
   attr[1].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = cooperative ? 2 : 1;
+#ifdef REBK_STATIC_CLUSTER
+  if (cluster_size != REBK_STATIC_CLUSTER) return cudaErrorInvalidValue;
+  cfg.attrs = attr + 1;
+  cfg.numAttrs = cooperative ? 1 : 0;
+#endif
   return cudaLaunchKernelEx(&cfg, rebk_dense_split_kernel, sp, tm_ct, tm_rt);
 }
 
