@@ -184,6 +184,16 @@ int rebk_sample_sequence(const rebk_cfg* cfg, int64_t k0, int64_t count, int32_t
 int rebk_block_frobenius_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* ptr,
                             double* out);
 
+/* Device block spectral norms: sigma_1(B_b)^2 for the nb contiguous blocks
+ * ptr[nb+1] along axis 0 (row blocks A[I,:]) or 1 (column blocks A[:,J]),
+ * by Lanczos with full reorthogonalisation on the block's small Gram
+ * operator (at most max_steps steps per block; <= 0 selects 300).  Replaces
+ * the per-block Jacobi SVD of the reference's _block_beta (rates.py:76-90):
+ * beta = max_b sigma1_sq_out[b] / ||B_b||_F^2.  steps_out (nullable)
+ * receives the Lanczos steps each block took. */
+int rebk_block_sigma1_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* ptr, int max_steps,
+                         double* sigma1_sq_out, int32_t* steps_out);
+
 /* ---- host-side helpers (no GPU needed) ---------------------------------- */
 /* numpy SeedSequence(entropy, spawn_key).generate_state(2, uint64): the
  * Philox key of Rng(seed, spawn_key) (sampling.py:33-37). entropy / spawn

@@ -98,6 +98,7 @@ SIGNATURES = {
     "rebk_shard_err2": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "rebk_sample_sequence": (c_int, [POINTER(RebkCfg), c_int64, c_int64, POINTER(c_int32)]),
     "rebk_block_frobenius_sq": (c_int, [c_void_p, c_int, c_int64, _P_I64, _P_D]),
+    "rebk_block_sigma1_sq": (c_int, [c_void_p, c_int, c_int64, _P_I64, c_int, _P_D, POINTER(c_int32)]),
     "rebk_philox_key": (c_int, [POINTER(c_uint32), c_int64, POINTER(c_uint32), c_int64, POINTER(c_uint64)]),
     "rebk_philox_uniforms_host": (c_int, [POINTER(c_uint64), c_uint64, c_int64, _P_D]),
 }

@@ -1687,6 +1687,25 @@ int rebk_block_frobenius_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* 
   return rc;
 }
 
+int rebk_block_sigma1_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* ptr, int max_steps,
+                         double* sigma1_sq_out, int32_t* steps_out) {
+  if (!ctx || !ptr || !sigma1_sq_out || nb < 1 || (axis != 0 && axis != 1))
+    return fail(REBK_EINVAL, "bad argument");
+  if (ctx->kind != 0) return fail(REBK_EINVAL, "device block spectral norms are implemented for dense matrices");
+  const int64_t len = axis == 0 ? ctx->m : ctx->n;
+  if (ptr[0] != 0 || ptr[nb] != len) return fail(REBK_EINVAL, "partition does not cover the axis");
+  for (int64_t b = 0; b < nb; ++b)
+    if (ptr[b + 1] <= ptr[b]) return fail(REBK_EINVAL, "empty block in partition");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t stream;
+  CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  const cudaError_t e = block_sigma1_sq(ctx->A, ctx->lda, ctx->m, ctx->n, axis, nb, ptr,
+                                        max_steps > 0 ? max_steps : 300, sigma1_sq_out, steps_out, stream);
+  cudaStreamDestroy(stream);
+  if (e != cudaSuccess) return fail(REBK_ECUDA, "block spectral norms failed: %s", cudaGetErrorString(e));
+  return REBK_OK;
+}
+
 int rebk_philox_key(const uint32_t* entropy_words, int64_t n_entropy_words, const uint32_t* spawn_words,
                     int64_t n_spawn_words, uint64_t key_out[2]) {
   if (!key_out || n_entropy_words < 0 || n_spawn_words < 0) return fail(REBK_EINVAL, "bad argument");

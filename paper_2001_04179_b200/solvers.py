@@ -28,6 +28,8 @@ import math
 import time
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -130,6 +132,36 @@ def compute_beta_max(a: Matrix, row_p: Partition, col_p: Partition) -> tuple[flo
     return br, bc, max(br, bc)
 
 
+def _device_block_beta(a: Matrix, p: Partition, weights=None) -> float:
+    """Same quantity as _block_beta (rates.py:76-90) with the spectral norms
+    from device Lanczos on the immutable device copy of A (rebk_beta.cu).
+    The Frobenius denominators are the host block norms the samplers use
+    (matrix.py:170-189), so the ratio differs from the host one only by the
+    eigenvalue solver's rounding."""
+    sizes = np.array([len(idx) for idx in p.blocks])
+    fro = np.asarray(weights if weights is not None else
+                     [a.block_frobenius_sq(a.block(p.axis, idx)) for idx in p.blocks], dtype=np.float64)
+    if np.any(fro <= 0.0):
+        raise ValueError("zero block has no spectral-to-Frobenius ratio")
+    worst = 1.0 if np.any(sizes == 1) else 0.0
+    if np.all(sizes == 1):
+        return worst
+    order = None if p.is_contiguous_in_order() else p.order()
+    dm = a.device(order, None) if p.axis == "row" else a.device(None, order)
+    sig, _ = dm.block_sigma1_sq(0 if p.axis == "row" else 1, p.pointers())
+    multi = sizes > 1
+    return max(worst, float(np.max(sig[multi] / fro[multi])))
+
+
+def device_beta_max(a: Matrix, row_p: Partition, col_p: Partition, row_w=None, col_w=None) -> tuple[float, float, float]:
+    """compute_beta_max with the block spectral norms computed on the B200
+    (dense A; SURVEY §8f #1).  Sparse matrices keep the host eigensolver."""
+    if a.is_sparse:
+        return compute_beta_max(a, row_p, col_p)
+    br, bc = _device_block_beta(a, row_p, row_w), _device_block_beta(a, col_p, col_w)
+    return br, bc, max(br, bc)
+
+
 class SolverContext:
     """Validated, immutable per-run data (solvers.py:123-187) plus the device
     binding: the device copy of A (permuted once when a partition is not
@@ -182,7 +214,16 @@ class SolverContext:
         self.beta_max = config.beta_max
         if self.beta_max is None and algo in _STEPSIZE_RATE_ALGOS:
             col_p = self.col_partition or singleton_partition(self.a.cols, "col")
-            self.beta_max = compute_beta_max(self.a, row_p, col_p)[2]
+            col_w = self.col_sampler.weights if self.col_partition is not None else None
+            # device Lanczos by default; REBK_BETA_BACKEND=host selects the host
+            # eigensolver explicitly (prepare-only use on a machine without a GPU)
+            backend = os.environ.get("REBK_BETA_BACKEND", "device")
+            if backend not in ("device", "host"):
+                raise ValueError(f"REBK_BETA_BACKEND must be 'device' or 'host', got {backend!r}")
+            if backend == "device":
+                self.beta_max = device_beta_max(self.a, row_p, col_p, self.row_sampler.weights, col_w)[2]
+            else:
+                self.beta_max = compute_beta_max(self.a, row_p, col_p)[2]
         if self.beta_max is not None and self.alpha >= 2.0 / self.beta_max:
             self.warnings.append(OutOfRegimeWarning)
 

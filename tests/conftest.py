@@ -18,3 +18,12 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden_dir():
     return GOLDEN
+
+
+@pytest.fixture(autouse=True)
+def _beta_backend(request, monkeypatch):
+    """prepare() resolves beta_max on the device (REBK_BETA_BACKEND=device,
+    the default).  Host-logic tests without a GPU select the host
+    eigensolver explicitly."""
+    if request.node.get_closest_marker("gpu") is None:
+        monkeypatch.setenv("REBK_BETA_BACKEND", "host")
