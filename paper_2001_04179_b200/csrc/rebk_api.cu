@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -764,6 +765,25 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
   return REBK_OK;
 }
 
+// REBK_HOST_TIMING=1: host wall-clock marks of one dense run's phases (stderr)
+struct HostMarks {
+  bool on = false;
+  std::chrono::steady_clock::time_point t0, last;
+  HostMarks() {
+    const char* e = getenv("REBK_HOST_TIMING");
+    on = e && atoi(e) != 0;
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[rebk host] %-28s +%8.3f ms (total %8.3f ms)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(),
+            std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
+
 int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev,
                     double* x_dev, double* z_dev, cudaStream_t stream, rebk_trace* trace) {
   const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
@@ -786,6 +806,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   if (ctx->kind == 1) return run_csr_impl(ctx, cfg, b_dev, xs_dev, x_dev, z_dev, stream, trace);
 
   CUDA_TRY(cudaSetDevice(ctx->device));
+  HostMarks hm;
 
   // geometry: find the largest grid that is co-resident with our smem need
   int G0 = choose_grid(ctx, cfg, 1 << 20);
@@ -796,6 +817,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   if (G0 > occ * ctx->sm_count) {
     geo = plan_geometry(ctx, cfg, occ * ctx->sm_count, extended);
   }
+  hm.mark("geometry + occupancy");
   // fast path: clustered kernel (oracle_error / max_iters_only, TMA-able tiles,
   // at least one full cluster).  The choice depends only on the problem shape,
   // partitions and stopping mode, so repeated runs take the same path.
@@ -830,6 +852,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
       }
     }
   }
+  hm.mark("fast-path probe");
   // split path: column and row sweeps on two concurrent CTA groups
   // (rebk_dense_split.cu); needs a column sweep and oracle/no stopping
   bool use_split = false;
@@ -856,6 +879,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
       use_fast = encode_box(&tm_ct, ctx, fg.ct_box_w, fg.ct_box_h) && encode_box(&tm_rt, ctx, fg.rt_box_w, fg.rt_box_h);
     }
   }
+  hm.mark("split-path probe");
   // streaming path: blocks whose per-CTA slices the general kernel cannot
   // stage in shared memory (C3) stream through a TMA ring instead
   bool use_stream = false;
@@ -881,6 +905,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
   int64_t *d_row_ptr, *d_col_ptr = nullptr;
   double *d_row_cum, *d_row_scale, *d_col_cum = nullptr, *d_col_scale = nullptr;
+  hm.mark("path selection");
   CUDA_TRY(arena.alloc(&d_row_ptr, s + 1));
   CUDA_TRY(arena.alloc(&d_row_cum, s));
   CUDA_TRY(arena.alloc(&d_row_scale, s));
@@ -1037,6 +1062,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   CUDA_TRY(cudaEventCreate(&ev0));
   CUDA_TRY(cudaEventCreate(&ev1));
   cudaError_t err = cudaEventRecord(ev0, stream);
+  hm.mark("workspace + uploads");
   int64_t k = 1;
   do {
     const int64_t count = std::min(chunk, cfg->max_iters - k + 1);
@@ -1108,6 +1134,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     }
   } while (err == cudaSuccess && k <= cfg->max_iters);
   if (err == cudaSuccess) err = cudaEventRecord(ev1, stream);
+  hm.mark("launch loop (async)");
   Control ctl{};
   if (err == cudaSuccess) err = cudaMemcpyAsync(&ctl, d_ctl, sizeof ctl, cudaMemcpyDeviceToHost, stream);
   if (err == cudaSuccess && errs_cap > 0) {
@@ -1120,6 +1147,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   if (err != cudaSuccess) return fail(REBK_ECUDA, "REBK run failed: %s", cudaGetErrorString(err));
+  hm.mark("sync + control readback");
   if (ctl.fault) return fail(REBK_ECUDA, "clustered kernel launched without its %d-CTA clusters", fg.CS);
   if (d_trace) {
     std::vector<unsigned long long> h((size_t)trace_n * G * 8);
