@@ -543,6 +543,37 @@ __device__ __forceinline__ bool pk_job(const PkArgs& a, int phase, int64_t k, in
   return false;
 }
 
+// Persistent kernel data path.  The GEMM phases are bound by the number of
+// tcgen05.mma instructions (~110-130 cycles each at M = 128, K = 8, N = 64
+// or 128, measured: tools/umma_ts_test.cu and the per-job trace), so each
+// 8-wide k-step issues two MMAs instead of three: A_hi·[B_hi | B_lo] as one
+// N = 128 MMA into the adjacent D_hh | D_hl accumulators, and A_lo·B_hi.
+// A's hi and lo parts live in TMEM (the "TS" MMA form reads A from TMEM:
+// converter warps 4-7 own TMEM lane quadrants 0-3 and write their rows with
+// tcgen05.st), which also takes A's operand reads off shared memory.
+// Rings: PK_NRAW raw stages in shared memory (A 16 KB, B 8 KB, B lo 8 KB
+// written by converter warps 2-3 right behind B); PK_NA A stages in TMEM
+// (hi 32 + lo 32 columns each, after the two 128-column accumulators).
+#ifndef PK_NRAW
+#define PK_NRAW 4  // measured on C5: 4/4 100.9 ms, 5/3 105.0, 5/4 104.9 per solve
+#endif
+#ifndef PK_NA
+#define PK_NA 4
+#endif
+// one raw stage: A tile, B tile, and B's lo part right behind it, so that
+// [B hi; B lo] is a single 128-row K-major operand: one N = 128 MMA
+// computes A_hi·B_hi and A_hi·B_lo into the two adjacent accumulators
+constexpr int RAW_FLOATS = (TM + 2 * RHS) * BK;
+constexpr size_t PK_SMEM_BYTES = (size_t)PK_NRAW * RAW_FLOATS * 4 + 1024;
+static_assert(PK_SMEM_BYTES <= 227 * 1024, "persistent ring exceeds shared memory");
+static_assert(256 + 64 * PK_NA <= 512, "TMEM: two accumulators + the A ring");
+constexpr int PK_TMEM_COLS = 512;
+struct PkPipe {
+  uint64_t full[PK_NRAW], rempty[PK_NRAW], conv[PK_NA], lempty[PK_NA];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem;
+};
+
 __global__ void __launch_bounds__(NTW, 1)
     k_rebk_mrhs_persistent(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAt,
                            const __grid_constant__ CUtensorMap mZt, const __grid_constant__ CUtensorMap mXt,
@@ -550,7 +581,7 @@ __global__ void __launch_bounds__(NTW, 1)
                            const __grid_constant__ CUtensorMap mXst, const __grid_constant__ PkArgs a) {
   extern __shared__ float smem_raw[];
   float* smem = aligned_smem(smem_raw);
-  __shared__ Pipe P;
+  __shared__ PkPipe P;
   __shared__ int s_crossed[RHS];
   __shared__ volatile int s_stop;
   __shared__ double s_d2[16][TM];  // stop check: (x - x*)^2 of one 16-column chunk of a tile
@@ -559,12 +590,15 @@ __global__ void __launch_bounds__(NTW, 1)
   __shared__ float s_half[NRED];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x;
-  if (warp == 0) umma::tmem_alloc<256>(&P.tmem);
+  if (warp == 0) umma::tmem_alloc<PK_TMEM_COLS>(&P.tmem);
   if (tid == 32) {
-    for (int q = 0; q < NSTAGE; ++q) {
+    for (int q = 0; q < PK_NRAW; ++q) {
       mbar_init(&P.full[q], 1);
+      mbar_init(&P.rempty[q], 1);
+    }
+    for (int q = 0; q < PK_NA; ++q) {
       mbar_init(&P.conv[q], NCONV);
-      mbar_init(&P.empty[q], 1);
+      mbar_init(&P.lempty[q], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&P.tfull[b], 1);
@@ -582,10 +616,10 @@ __global__ void __launch_bounds__(NTW, 1)
   auto phase_end = [&](int64_t k, int ph) -> unsigned long long {
     return (unsigned long long)G * (unsigned long long)(4 * (k - a.k_begin) + ph + 1);
   };
-  auto a_raw = [&](int q) { return smem + (size_t)q * STAGE_FLOATS; };
-  auto a_lo = [&](int q) { return smem + (size_t)q * STAGE_FLOATS + TM * BK; };
-  auto b_raw = [&](int q) { return smem + (size_t)q * STAGE_FLOATS + 2 * TM * BK; };
-  auto b_lo = [&](int q) { return smem + (size_t)q * STAGE_FLOATS + 2 * TM * BK + RHS * BK; };
+  auto a_raw = [&](int q) { return smem + (size_t)q * RAW_FLOATS; };
+  auto b_raw = [&](int q) { return smem + (size_t)q * RAW_FLOATS + TM * BK; };
+  auto b_lo = [&](int q) { return smem + (size_t)q * RAW_FLOATS + (TM + RHS) * BK; };
+  auto ta_hi = [&](int l) { return tmem + 256u + 64u * (uint32_t)l; };  // A hi; lo 32 columns on
   const int64_t k_last = a.k_end + 1;  // final round: P4(k_end) and its check only
 
   if (warp == 0) {
@@ -619,9 +653,9 @@ __global__ void __launch_bounds__(NTW, 1)
               }
             }
             for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
-              const int q = it % NSTAGE;
-              if (it >= NSTAGE) {
-                mbar_wait(&P.empty[q], (ph >> q) & 1u);
+              const int q = it % PK_NRAW;
+              if (it >= PK_NRAW) {
+                mbar_wait(&P.rempty[q], (ph >> q) & 1u);
                 ph ^= 1u << q;
               }
               mbar_arrive_expect_tx(&P.full[q], (TM + RHS) * BK * 4);
@@ -649,6 +683,7 @@ __global__ void __launch_bounds__(NTW, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
       const uint32_t idesc = umma::idesc_tf32(TM, RHS);
+      const uint32_t idesc2 = umma::idesc_tf32(TM, 2 * RHS);
       uint32_t phc = 0, pht = 0;
       int it = 0, jt = 0;
       for (int64_t k = a.k_begin; k <= k_last; ++k) {
@@ -667,22 +702,21 @@ __global__ void __launch_bounds__(NTW, 1)
             }
             const uint32_t dh = tmem + b * 128, dl = dh + RHS;
             for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
-              const int q = it % NSTAGE;
-              mbar_wait(&P.conv[q], (phc >> q) & 1u);
-              phc ^= 1u << q;
+              const int q = it % PK_NRAW, l = it % PK_NA;
+              mbar_wait(&P.conv[l], (phc >> l) & 1u);
+              phc ^= 1u << l;
               if (kb == J.kb0) pk_jstamp(a, k, phase, j, 2);
               umma::fence_after_sync();
+              const uint32_t tah = ta_hi(l), tal = tah + 32;
               for (int ks = 0; ks < BK / 8; ++ks) {
-                const uint64_t ah = umma::make_desc_sw128(smem_u32(a_raw(q)) + 32 * ks);
-                const uint64_t al = umma::make_desc_sw128(smem_u32(a_lo(q)) + 32 * ks);
-                const uint64_t bh = umma::make_desc_sw128(smem_u32(b_raw(q)) + 32 * ks);
-                const uint64_t bl = umma::make_desc_sw128(smem_u32(b_lo(q)) + 32 * ks);
+                // [B hi; B lo] as one N = 128 operand: D_hh | D_hl in one MMA
+                const uint64_t bhl = umma::make_desc_sw128(smem_u32(b_raw(q)) + 32 * ks);
                 const bool acc = kb > J.kb0 || ks > 0;
-                umma::mma_tf32(dh, ah, bh, idesc, acc);
-                umma::mma_tf32(dl, ah, bl, idesc, acc);
-                umma::mma_tf32(dh, al, bh, idesc, true);
+                umma::mma_tf32_ts(dh, tah + 8 * ks, bhl, idesc2, acc);
+                umma::mma_tf32_ts(dh, tal + 8 * ks, bhl, idesc, true);
               }
-              umma::commit(&P.empty[q]);
+              umma::commit(&P.rempty[q]);
+              umma::commit(&P.lempty[l]);
             }
             umma::commit(&P.tfull[b]);
             pk_jstamp(a, k, phase, j, 3);
@@ -695,46 +729,71 @@ __global__ void __launch_bounds__(NTW, 1)
     // ---- converter warps (2-7) and epilogue warps (8-11); all of them run the reductions
     const bool conv = warp < EPI0;
     const int tr = tid - CONV0 * 32;  // 0 .. NRED-1
-    uint32_t phf = 0, pht = 0;
+    uint32_t phf = 0, pht = 0, phl = 0;
     int it = 0, jt = 0;
     for (int64_t k = a.k_begin; k <= k_last; ++k) {
       for (int phase = 0; phase < 2; ++phase) {
         if (phase == 1 && k == k_last) break;
         PJob J;
         if (conv) {
-          const int ct = tid - CONV0 * 32;
+          // warps 4-7: A rows of TMEM lane quadrant warp % 4 (hi = raw value,
+          // the MMA truncates it to tf32; lo = exact remainder) -> TMEM;
+          // warps 2-3: the B tile's lo part -> shared memory
+          const bool aconv = warp >= 4;
+          const int arow = 32 * (warp & 3) + lane;
+          const int bt = tid - CONV0 * 32;  // 0..63 for the B warps
           for (int j = 0; pk_job(a, phase, k, j, J); ++j)
             for (int kb = J.kb0; kb < J.kb1; ++kb, ++it) {
-              const int q = it % NSTAGE;
+              const int q = it % PK_NRAW, l = it % PK_NA;
               mbar_wait(&P.full[q], (phf >> q) & 1u);
               phf ^= 1u << q;
-              constexpr int A4 = TM * BK / 4, B4 = RHS * BK / 4, PER = (A4 + B4) / (NCONV * 32);
-              static_assert((A4 + B4) % (NCONV * 32) == 0, "converter split");
-              const float4* srcA = reinterpret_cast<const float4*>(a_raw(q));
-              const float4* srcB = reinterpret_cast<const float4*>(b_raw(q));
-              float4* dstA = reinterpret_cast<float4*>(a_lo(q));
-              float4* dstB = reinterpret_cast<float4*>(b_lo(q));
-              float4 v[PER];
+              if (aconv) {
+                float hi[BK], lo[BK];
+                const float* src = a_raw(q) + arow * BK;  // row r at r * 128 bytes, 16-byte chunks swizzled
 #pragma unroll
-              for (int i = 0; i < PER; ++i) {
-                const int e = ct + i * NCONV * 32;
-                v[i] = e < A4 ? srcA[e] : srcB[e - A4];
-              }
+                for (int c = 0; c < BK / 4; ++c) {
+                  const float4 v = *reinterpret_cast<const float4*>(src + (((c ^ arow) & 7) << 2));
+                  hi[4 * c + 0] = v.x;
+                  hi[4 * c + 1] = v.y;
+                  hi[4 * c + 2] = v.z;
+                  hi[4 * c + 3] = v.w;
+                }
 #pragma unroll
-              for (int i = 0; i < PER; ++i) {
-                const int e = ct + i * NCONV * 32;
-                float4 lo;
-                float h;
-                umma::split_tf32(v[i].x, h, lo.x);
-                umma::split_tf32(v[i].y, h, lo.y);
-                umma::split_tf32(v[i].z, h, lo.z);
-                umma::split_tf32(v[i].w, h, lo.w);
-                if (e < A4) dstA[e] = lo;
-                else dstB[e - A4] = lo;
+                for (int e = 0; e < BK; ++e) {
+                  float h;
+                  umma::split_tf32(hi[e], h, lo[e]);
+                }
+                if (it >= PK_NA) {  // the MMAs of stage it - PK_NA are done with slot l
+                  mbar_wait(&P.lempty[l], (phl >> l) & 1u);
+                  phl ^= 1u << l;
+                }
+                const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+                umma::tmem_st32(ta_hi(l) + lane_base, hi);
+                umma::tmem_st32(ta_hi(l) + 32 + lane_base, lo);
+                umma::tmem_wait_st();
+                umma::fence_before_sync();
+              } else {
+                constexpr int B4 = RHS * BK / 4, PERB = B4 / 64;
+                static_assert(B4 % 64 == 0, "B converter split");
+                const float4* srcB = reinterpret_cast<const float4*>(b_raw(q));
+                float4 v[PERB];
+#pragma unroll
+                for (int i = 0; i < PERB; ++i) v[i] = srcB[bt + i * 64];
+                float4* dstB = reinterpret_cast<float4*>(b_lo(q));
+#pragma unroll
+                for (int i = 0; i < PERB; ++i) {
+                  float4 lo;
+                  float h;
+                  umma::split_tf32(v[i].x, h, lo.x);
+                  umma::split_tf32(v[i].y, h, lo.y);
+                  umma::split_tf32(v[i].z, h, lo.z);
+                  umma::split_tf32(v[i].w, h, lo.w);
+                  dstB[bt + i * 64] = lo;
+                }
+                fence_proxy_async();
               }
-              fence_proxy_async();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&P.conv[q]);
+              if (lane == 0) mbar_arrive(&P.conv[l]);
             }
         } else {
           const int ew = warp & 3, rlane = ew * 32;
@@ -956,7 +1015,7 @@ __global__ void __launch_bounds__(NTW, 1)
   }
   umma::fence_before_sync();
   __syncthreads();
-  if (warp == 0) umma::tmem_dealloc<256>(tmem);
+  if (warp == 0) umma::tmem_dealloc<PK_TMEM_COLS>(tmem);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1127,9 +1186,9 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
   const int nt2 = (int)((m + TM - 1) / TM), nt4 = (int)((n + TM - 1) / TM);
   bool use_pk = !(pk_env && pk_env[0] == '0') && G >= 2 && nt4 <= G && !(dbg & 3);
   if (use_pk) {
-    TC_TRY(cudaFuncSetAttribute(k_rebk_mrhs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    TC_TRY(cudaFuncSetAttribute(k_rebk_mrhs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PK_SMEM_BYTES));
     int occ = 0;
-    TC_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rebk_mrhs_persistent, NTW, SMEM_BYTES));
+    TC_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rebk_mrhs_persistent, NTW, PK_SMEM_BYTES));
     use_pk = occ >= 1;
   }
 
@@ -1221,7 +1280,7 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(G);
       lc.blockDim = dim3(NTW);
-      lc.dynamicSmemBytes = SMEM_BYTES;
+      lc.dynamicSmemBytes = PK_SMEM_BYTES;
       lc.stream = stream;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeCooperative;
