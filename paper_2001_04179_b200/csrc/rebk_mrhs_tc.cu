@@ -431,6 +431,7 @@ struct PJob {
   float s;
   int check;
 };
+constexpr int PK_TRACE_SLOTS = 16;  // globaltimer stamps per (iteration, CTA)
 constexpr int NRED = NTW - CONV0 * 32;  // threads of the reduction phases (converter + epilogue warps)
 
 // non-aligned named barrier: callers may arrive from divergent code (e.g.
@@ -438,8 +439,18 @@ constexpr int NRED = NTW - CONV0 * 32;  // threads of the reduction phases (conv
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// PK_GBAR_FENCE: 2 = __threadfence() before the release add (fence.sc),
+// 1 = fence.acq_rel.gpu, 0 = the release add alone (its release semantics are
+// cumulative over the CTA's writes ordered before it by the named barrier)
+#ifndef PK_GBAR_FENCE
+#define PK_GBAR_FENCE 0  // measured on C5: 0 98.8 ms, 1 101.4, 2 102.0 per solve
+#endif
 __device__ __forceinline__ void gbar_arrive(unsigned long long* g) {
+#if PK_GBAR_FENCE == 2
   __threadfence();
+#elif PK_GBAR_FENCE == 1
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
   asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(g) : "memory");
 }
 __device__ __forceinline__ void gbar_wait(const unsigned long long* g, unsigned long long target) {
@@ -466,7 +477,7 @@ __device__ __forceinline__ void pk_stamp(const PkArgs& a, int64_t k, int i) {
   if (a.trace && k >= a.trace_k0 && k < a.trace_k0 + a.trace_n) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[((size_t)(k - a.trace_k0) * gridDim.x + blockIdx.x) * 8 + i] = t;
+    a.trace[((size_t)(k - a.trace_k0) * gridDim.x + blockIdx.x) * PK_TRACE_SLOTS + i] = t;
   }
 }
 // per-job stamps of CTAs 0 and 120 at iteration trace_k0 (events: 0 producer
@@ -588,6 +599,7 @@ __global__ void __launch_bounds__(NTW, 1)
   __shared__ double s_g8[16][8];
   __shared__ double s_errt[RHS];
   __shared__ float s_half[NRED];
+  __shared__ double s_errp[NRED / RHS][RHS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x;
   if (warp == 0) umma::tmem_alloc<PK_TMEM_COLS>(&P.tmem);
@@ -913,6 +925,7 @@ __global__ void __launch_bounds__(NTW, 1)
             if (phase == 1) gbar_wait(a.gbar, phase_end(k, 1));
             else if (k > a.k_begin) gbar_wait(a.gbar, phase_end(k - 1, 3));
             gbar_arrive(a.gbar);
+            pk_stamp(a, k, phase == 0 ? 8 : 10);
           }
         }
         // ---- reduction phase (B after A, D after C): one thread polls
@@ -926,14 +939,37 @@ __global__ void __launch_bounds__(NTW, 1)
 #endif
         __syncwarp();
         named_bar(2, NRED);
+        if (tr == 0) pk_stamp(a, k, phase == 0 ? 9 : 11);
         const int b = blockIdx.x;
         if (phase == 0) {
           // stop check of iteration k-1 (every CTA, same bits)
           if (k - 1 >= a.k_begin && pk_is_check(a, k - 1)) {
+            // per-column Σ over the nt4 tile partials: NRED / RHS threads per
+            // column take tiles pp, pp + NP, ... (loads issued together), then a
+            // fixed-order combine, so the check costs one L2 round trip
+            {
+              constexpr int NP = NRED / RHS;
+              const int c = tr % RHS, pp = tr / RHS;
+              if (pp < NP) {
+                double s = 0.0;
+                if (c < a.R) {
+                  for (int t0 = pp; t0 < a.nt4; t0 += 8 * NP) {
+                    double v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                      v[u] = (t0 + u * NP < a.nt4) ? ld_cg_f64(a.errpart + (size_t)(t0 + u * NP) * RHS + c) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) s += v[u];
+                  }
+                }
+                s_errp[pp][c] = s;
+              }
+            }
+            named_bar(2, NRED);
             if (tr < a.R) {
               double s = 0.0;
-#pragma unroll 8
-              for (int t = 0; t < a.nt4; ++t) s += ld_cg_f64(a.errpart + (size_t)t * RHS + tr);
+#pragma unroll
+              for (int pp = 0; pp < NRED / RHS; ++pp) s += s_errp[pp][tr];
               const double e = sqrt(s);
               if (!s_crossed[tr] && e <= a.tol[tr]) {
                 s_crossed[tr] = 1;
@@ -1265,8 +1301,8 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
     pa.trace_k0 = 100;
     unsigned long long* d_tr = nullptr;
     if (pa.trace_n > 0) {
-      TC_TRY(cudaMallocAsync((void**)&d_tr, sizeof(unsigned long long) * pa.trace_n * G * 8, stream));
-      TC_TRY(cudaMemsetAsync(d_tr, 0, sizeof(unsigned long long) * pa.trace_n * G * 8, stream));
+      TC_TRY(cudaMallocAsync((void**)&d_tr, sizeof(unsigned long long) * pa.trace_n * G * PK_TRACE_SLOTS, stream));
+      TC_TRY(cudaMemsetAsync(d_tr, 0, sizeof(unsigned long long) * pa.trace_n * G * PK_TRACE_SLOTS, stream));
       pa.trace = d_tr;
       TC_TRY(cudaMallocAsync((void**)&pa.trace2, sizeof(unsigned long long) * 2 * 2 * 4 * 8, stream));
       TC_TRY(cudaMemsetAsync(pa.trace2, 0, sizeof(unsigned long long) * 2 * 2 * 4 * 8, stream));
@@ -1298,7 +1334,7 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
       if (st) break;
     }
     if (d_tr) {
-      std::vector<unsigned long long> h((size_t)pa.trace_n * G * 8);
+      std::vector<unsigned long long> h((size_t)pa.trace_n * G * PK_TRACE_SLOTS);
       TC_TRY(cudaMemcpy(h.data(), d_tr, h.size() * 8, cudaMemcpyDeviceToHost));
       const char* fn = getenv("REBK_PK_TRACE_FILE");
       FILE* f = fopen(fn ? fn : "pk_trace.bin", "wb");
