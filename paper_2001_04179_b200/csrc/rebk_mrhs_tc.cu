@@ -595,9 +595,7 @@ __global__ void __launch_bounds__(NTW, 1)
   __shared__ PkPipe P;
   __shared__ int s_crossed[RHS];
   __shared__ volatile int s_stop;
-  __shared__ double s_d2[16][TM];  // stop check: (x - x*)^2 of one 16-column chunk of a tile
-  __shared__ double s_g8[16][8];
-  __shared__ double s_errt[RHS];
+  __shared__ double s_wsum[4][RHS];  // stop check: per-warp column sums of (x - x*)^2 of a tile
   __shared__ float s_half[NRED];
   __shared__ double s_errp[NRED / RHS][RHS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -724,8 +722,10 @@ __global__ void __launch_bounds__(NTW, 1)
                 // [B hi; B lo] as one N = 128 operand: D_hh | D_hl in one MMA
                 const uint64_t bhl = umma::make_desc_sw128(smem_u32(b_raw(q)) + 32 * ks);
                 const bool acc = kb > J.kb0 || ks > 0;
-                umma::mma_tf32_ts(dh, tah + 8 * ks, bhl, idesc2, acc);
-                umma::mma_tf32_ts(dh, tal + 8 * ks, bhl, idesc, true);
+                if (!(a.dbg & 32)) {  // REBK_PK_DBG=32: no MMAs (timing experiments only)
+                  umma::mma_tf32_ts(dh, tah + 8 * ks, bhl, idesc2, acc);
+                  umma::mma_tf32_ts(dh, tal + 8 * ks, bhl, idesc, true);
+                }
               }
               umma::commit(&P.rempty[q]);
               umma::commit(&P.lempty[l]);
@@ -759,7 +759,12 @@ __global__ void __launch_bounds__(NTW, 1)
               const int q = it % PK_NRAW, l = it % PK_NA;
               mbar_wait(&P.full[q], (phf >> q) & 1u);
               phf ^= 1u << q;
-              if (aconv) {
+              if (a.dbg & 64) {  // REBK_PK_DBG=64: no conversion (timing experiments only)
+                if (it >= PK_NA) {
+                  mbar_wait(&P.lempty[l], (phl >> l) & 1u);
+                  phl ^= 1u << l;
+                }
+              } else if (aconv) {
                 float hi[BK], lo[BK];
                 const float* src = a_raw(q) + arow * BK;  // row r at r * 128 bytes, 16-byte chunks swizzled
 #pragma unroll
@@ -849,8 +854,17 @@ __global__ void __launch_bounds__(NTW, 1)
                 }
               }
               float h[16], l[16];
-              umma::tmem_ld16(base + c0, h);
-              umma::tmem_ld16(base + RHS + c0, l);
+              {
+                uint32_t rh[16], rl[16];
+                umma::tmem_ld16_nowait(base + c0, rh);
+                umma::tmem_ld16_nowait(base + RHS + c0, rl);
+                umma::tmem_wait_ld();
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                  h[q] = __uint_as_float(rh[q]);
+                  l[q] = __uint_as_float(rl[q]);
+                }
+              }
               if (mode0) {
                 float4* dst = reinterpret_cast<float4*>(part + ((size_t)J.slot * 256 + J.prow + row) * RHS + c0);
 #pragma unroll
@@ -867,36 +881,36 @@ __global__ void __launch_bounds__(NTW, 1)
                   }
                 }
                 if (J.check) {
-                  // Σ over the tile's 128 rows of (x - x*)^2 for these 16
-                  // columns, through shared memory in a fixed order: thread
-                  // (q, g) sums rows g, g + 8, ... of column q, then the 8
-                  // group sums of each column in order
-                  const int et = tid - EPI0 * 32;
+                  // Σ over the warp's 32 rows of (x - x*)^2, 8 columns at a
+                  // time by a transposing butterfly (fixed order; after the
+                  // xor 16/8/4 halvings lane L holds column (L>>4&1)*4 +
+                  // (L>>3&1)*2 + (L>>2&1), then xor 2 and 1 finish the sum);
+                  // the four warp sums are added in order after the tile
 #pragma unroll
-                  for (int q = 0; q < 16; ++q) {
-                    double v = 0.0;
-                    if (chk) {
-                      const double d = (double)ycur[q] - (double)xcur[q];
-                      v = d * d;
+                  for (int hh = 0; hh < 2; ++hh) {
+                    double v[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                      const double d = chk ? (double)ycur[8 * hh + q] - (double)xcur[8 * hh + q] : 0.0;
+                      v[q] = d * d;
                     }
-                    s_d2[q][row] = v;
-                  }
-                  named_bar(1, 128);
-                  {
-                    const int q = et >> 3, g = et & 7;
-                    double acc = 0.0;
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) acc += s_d2[q][g + 8 * i];
-                    s_g8[q][g] = acc;
-                  }
-                  named_bar(1, 128);
-                  if (et < 16) {
-                    double acc = 0.0;
+                    for (int m = 16, n = 8; m >= 4; m >>= 1, n >>= 1) {
+                      const bool up = (lane & m) != 0;
 #pragma unroll
-                    for (int g = 0; g < 8; ++g) acc += s_g8[et][g];
-                    s_errt[c0 + et] = acc;
+                      for (int i = 0; i < n / 2; ++i) {
+                        const double send = up ? v[i] : v[i + n / 2];
+                        const double keep = up ? v[i + n / 2] : v[i];
+                        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                      }
+                    }
+                    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+                    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+                    if ((lane & 3) == 0) {
+                      const int col = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+                      s_wsum[ew][c0 + 8 * hh + col] = v[0];
+                    }
                   }
-                  named_bar(1, 128);
                 }
               }
 #pragma unroll
@@ -910,9 +924,10 @@ __global__ void __launch_bounds__(NTW, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&P.tempty[b]);
             if (tid == EPI0 * 32) pk_jstamp(a, k, phase, j, 5);
-            if (J.check && tr - (EPI0 - CONV0) * 32 < RHS) {
+            if (J.check) {
+              named_bar(1, 128);
               const int c = tr - (EPI0 - CONV0) * 32;
-              a.errpart[(size_t)J.slot * RHS + c] = s_errt[c];
+              if (c < RHS) a.errpart[(size_t)J.slot * RHS + c] = ((s_wsum[0][c] + s_wsum[1][c]) + s_wsum[2][c]) + s_wsum[3][c];
             }
           }
           // this CTA's part of the phase is written: arrive
