@@ -587,6 +587,7 @@ struct PkPipe {
 
 __global__ void __launch_bounds__(NTW, 1)
     k_rebk_mrhs_persistent(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mAt,
+                           const __grid_constant__ CUtensorMap mAtT,
                            const __grid_constant__ CUtensorMap mZt, const __grid_constant__ CUtensorMap mXt,
                            const __grid_constant__ CUtensorMap mUt, const __grid_constant__ CUtensorMap mRt,
                            const __grid_constant__ CUtensorMap mXst, const __grid_constant__ PkArgs a) {
@@ -669,8 +670,12 @@ __global__ void __launch_bounds__(NTW, 1)
                 ph ^= 1u << q;
               }
               mbar_arrive_expect_tx(&P.full[q], (TM + RHS) * BK * 4);
-              tma_load_2d(a_raw(q), ma, J.kc0 + kb * BK, J.row0, &P.full[q]);
-              tma_load_2d(b_raw(q), mb, kb * BK, 0, &P.full[q]);
+              const int kbe = kb;
+              if (J.kind == 2)  // Z update: A_J through At, box 128 rows of z x 32 columns of J (L2-warm from P1)
+                tma_load_2d(a_raw(q), &mAtT, J.row0, J.kc0 + kbe * BK, &P.full[q]);
+              else
+                tma_load_2d(a_raw(q), ma, J.kc0 + kbe * BK, J.row0, &P.full[q]);
+              tma_load_2d(b_raw(q), mb, kbe * BK, 0, &P.full[q]);
             }
             pk_jstamp(a, k, phase, j, 1);
           }
@@ -683,7 +688,10 @@ __global__ void __launch_bounds__(NTW, 1)
             if (nk <= k_last && !(nph == 1 && nk == k_last))
               for (int j = 0; pk_job(a, nph, nk, j, J); ++j) {
                 const CUtensorMap* ma = (J.kind == 1 || J.kind == 4) ? &mAt : &mA;
-                for (int kb = J.kb0; kb < J.kb1; ++kb) tma_prefetch_l2_2d(ma, J.kc0 + kb * BK, J.row0);
+                for (int kb = J.kb0; kb < J.kb1; ++kb) {
+                  if (J.kind == 2) tma_prefetch_l2_2d(&mAtT, J.row0, J.kc0 + kb * BK);
+                  else tma_prefetch_l2_2d(ma, J.kc0 + kb * BK, J.row0);
+                }
               }
           }
         }
@@ -766,14 +774,21 @@ __global__ void __launch_bounds__(NTW, 1)
                 }
               } else if (aconv) {
                 float hi[BK], lo[BK];
-                const float* src = a_raw(q) + arow * BK;  // row r at r * 128 bytes, 16-byte chunks swizzled
+                if (J.kind == 2) {
+                  // At box: row kk (column c_lo + kk of A) holds 128 z rows
+                  const float* src = a_raw(q) + arow;
 #pragma unroll
-                for (int c = 0; c < BK / 4; ++c) {
-                  const float4 v = *reinterpret_cast<const float4*>(src + (((c ^ arow) & 7) << 2));
-                  hi[4 * c + 0] = v.x;
-                  hi[4 * c + 1] = v.y;
-                  hi[4 * c + 2] = v.z;
-                  hi[4 * c + 3] = v.w;
+                  for (int kk = 0; kk < BK; ++kk) hi[kk] = src[kk * TM];
+                } else {
+                  const float* src = a_raw(q) + arow * BK;  // row r at r * 128 bytes, 16-byte chunks swizzled
+#pragma unroll
+                  for (int c = 0; c < BK / 4; ++c) {
+                    const float4 v = *reinterpret_cast<const float4*>(src + (((c ^ arow) & 7) << 2));
+                    hi[4 * c + 0] = v.x;
+                    hi[4 * c + 1] = v.y;
+                    hi[4 * c + 2] = v.z;
+                    hi[4 * c + 3] = v.w;
+                  }
                 }
 #pragma unroll
                 for (int e = 0; e < BK; ++e) {
@@ -1097,6 +1112,21 @@ static bool encode_kmajor(CUtensorMap* map, const float* base, int64_t rows, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// At (n x m, leading dim ld) read as the Z update's A operand: box of 128
+// consecutive z rows (At's inner dimension) x 32 columns of the block, no
+// swizzle (512-byte rows); the converter warps transpose it into TMEM
+static bool encode_at_rows(CUtensorMap* map, const float* At, int64_t n, int64_t m, int64_t ld) {
+  EncodeTiledFn fn = encoder();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)TM, (cuuint32_t)BK};
+  cuuint32_t es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)At, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace tc
 
 cudaError_t mrhs_transpose_a(const float* A, int64_t m, int64_t n, int64_t lda, float* At, int64_t ldat,
@@ -1186,11 +1216,12 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
   TC_TRY(cudaMemsetAsync(d_errs_at, 0, sizeof(double) * R, stream));
 
   // tensor maps: A and At views (128-row boxes), iterate views (64-row boxes)
-  CUtensorMap mA, mAt, mZt, mXt, mUt, mRt;
+  CUtensorMap mA, mAt, mAtT, mZt, mXt, mUt, mRt;
   bool ok = encode_kmajor(&mA, w.A, m, n, w.lda, TM) && encode_kmajor(&mXt, Xt, RHS, n, n, RHS) &&
             encode_kmajor(&mUt, Ut, RHS, ldu, ldu, RHS) && encode_kmajor(&mRt, Rt, RHS, ldr, ldr, RHS);
   if (w.extended) ok = ok && encode_kmajor(&mAt, w.At, n, m, w.ldat, TM) && encode_kmajor(&mZt, Zt, RHS, m, m, RHS);
   else ok = ok && encode_kmajor(&mAt, w.At, n, m, w.ldat, TM);
+  ok = ok && encode_at_rows(&mAtT, w.At, n, m, w.ldat);
   CUtensorMap mXst = mXt;
   if (ok && Xst) ok = encode_kmajor(&mXst, Xst, RHS, n, n, RHS);
   if (!ok) {
@@ -1338,7 +1369,7 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
       at[0].val.cooperative = 1;
       lc.attrs = at;
       lc.numAttrs = 1;
-      TC_TRY(cudaLaunchKernelEx(&lc, k_rebk_mrhs_persistent, mA, mAt, w.extended ? mZt : mXt, mXt,
+      TC_TRY(cudaLaunchKernelEx(&lc, k_rebk_mrhs_persistent, mA, mAt, mAtT, w.extended ? mZt : mXt, mXt,
                                 mUt, mRt, mXst, pa));
       int32_t st = 0;
       int64_t kf = 0;
