@@ -224,16 +224,19 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
       for (int64_t sg = s0 + tid; sg < s1; sg += kCsrThreads) {
         const int i = p.cseg_row[sg];
         if (i >= pl.r_lo && i < pl.r_hi) continue;  // done by the row-sweep threads below
+        const double zi = __ldcg(p.z + i);  // issued with the entry loads, not after the sum
         double acc = 0.0;
         const int64_t e1 = p.cseg_ptr[sg + 1];
         for (int64_t e = p.cseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.cval[e], __ldcg(p.u + p.ccol[e]));
-        __stcg(p.z + i, __dsub_rn(__ldcg(p.z + i), __dmul_rn(cs, acc)));
+        __stcg(p.z + i, __dsub_rn(zi, __dmul_rn(cs, acc)));
       }
     }
     PROF(1);
     // rows of I: one warp per row; r_i and the row's own z update
     for (int64_t i = pl.r_lo + gwarp; i < pl.r_hi; i += gwarps) {
       double ax = 0.0, au = 0.0;
+      const double bi = __ldg(p.b + i);
+      const double zi = p.extended ? __ldcg(p.z + i) : 0.0;  // nobody else writes z_i of a row of I in P(k)
       const int64_t lo = p.csr_ptr[i], hi = p.csr_ptr[i + 1];
       constexpr int kPf = 4;  // a row's gathers all in flight, then the ordered adds
       int64_t base = lo;
@@ -264,9 +267,9 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
         base += 32 * kPf;
       }
       if (lane == 0) {
-        double rv = __dsub_rn(ax, __ldg(p.b + i));
+        double rv = __dsub_rn(ax, bi);
         if (p.extended) {
-          const double zn = __dsub_rn(__ldcg(p.z + i), __dmul_rn(cs, au));
+          const double zn = __dsub_rn(zi, __dmul_rn(cs, au));
           __stcg(p.z + i, zn);
           rv = __dadd_rn(rv, zn);
         }
@@ -282,10 +285,11 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
       const int64_t s1 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g + 1];
       for (int64_t sg = s0 + tid; sg < s1; sg += kCsrThreads) {
         const int j = p.rseg_col[sg];
+        const double xj = __ldcg(p.x + j);
         double acc = 0.0;
         const int64_t e1 = p.rseg_ptr[sg + 1];
         for (int64_t e = p.rseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.rval[e], __ldcg(p.r + p.rrow[e]));
-        __stcg(p.x + j, __dsub_rn(__ldcg(p.x + j), __dmul_rn(rs, acc)));
+        __stcg(p.x + j, __dsub_rn(xj, __dmul_rn(rs, acc)));
       }
     }
     __syncthreads();

@@ -68,6 +68,13 @@ def test_argument_errors_are_einval():
     rc = lib.rebk_ctx_create_dense(None, 2, 2, 2, 0, ctypes.byref(h))
     assert rc == -1
     assert b"null" in lib.rebk_last_error()
+    # device beta_max: argument checks happen before any device work
+    ptr = np.array([0, 2], dtype=np.int64)
+    out = np.zeros(1)
+    rc = lib.rebk_block_sigma1_sq(None, 0, 1, _lib.i64ptr(ptr), 0, _lib.dptr(out), None)
+    assert rc == -1 and b"bad argument" in lib.rebk_last_error()
+    rc = lib.rebk_block_sigma1_sq(None, 2, 1, _lib.i64ptr(ptr), 0, _lib.dptr(out), None)
+    assert rc == -1
 
 
 @pytest.mark.skipif(_lib.device_count() > 0, reason="checks the no-GPU behaviour")
