@@ -164,7 +164,7 @@ int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float*
  * rowstep and xupdate it allreduces dx (n doubles), on its communicator.
  * Together they are one step_rebk (solvers.py:324-337) on the sharded A.
  * Fixed-order reductions; the ctx's scratch makes these calls non-reentrant
- * per ctx. */
+ * per ctx. rebk_shard_colstep takes column blocks up to 512 wide. */
 int rebk_shard_colstep(rebk_ctx* ctx, int64_t c_lo, int64_t c_hi, const double* z_dev, double* u_dev,
                        void* stream);
 int rebk_shard_zupdate(rebk_ctx* ctx, int64_t c_lo, int64_t c_hi, double scale, const double* u_dev,

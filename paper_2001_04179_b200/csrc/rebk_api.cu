@@ -1507,10 +1507,10 @@ static int shard_scratch(rebk_ctx* ctx, size_t len, double** out) {
 int rebk_shard_colstep(rebk_ctx* ctx, int64_t c_lo, int64_t c_hi, const double* z_dev, double* u_dev, void* stream) {
   if (!ctx || ctx->kind != 0 || !z_dev || !u_dev || c_lo < 0 || c_hi > ctx->n || c_hi <= c_lo)
     return fail(REBK_EINVAL, "rebk_shard_colstep: bad argument");
+  if (c_hi - c_lo > 512) return fail(REBK_EINVAL, "rebk_shard_colstep: column blocks up to 512 wide");
   CUDA_TRY(cudaSetDevice(ctx->device));
   double* scr = nullptr;
-  const int64_t nparts = (ctx->m + 63) / 64;
-  int rc = shard_scratch(ctx, (size_t)nparts * (size_t)(c_hi - c_lo) + ctx->m, &scr);
+  int rc = shard_scratch(ctx, shard_colstep_scratch(ctx->m, c_hi - c_lo), &scr);
   if (rc) return rc;
   CUDA_TRY(shard_colstep(ctx->A, ctx->lda, ctx->m, c_lo, (int)(c_hi - c_lo), z_dev, u_dev, scr, (cudaStream_t)stream));
   return REBK_OK;
@@ -1531,8 +1531,7 @@ int rebk_shard_rowstep(rebk_ctx* ctx, const int64_t* rows_dev, int64_t nrows, co
     return fail(REBK_EINVAL, "rebk_shard_rowstep: bad argument");
   CUDA_TRY(cudaSetDevice(ctx->device));
   double* scr = nullptr;
-  const int64_t nparts = (ctx->m + 63) / 64;
-  int rc = shard_scratch(ctx, std::max<size_t>((size_t)nrows, 1) + (size_t)nparts, &scr);
+  int rc = shard_scratch(ctx, shard_rowstep_scratch(nrows, ctx->n), &scr);
   if (rc) return rc;
   CUDA_TRY(shard_rowstep(ctx->A, ctx->lda, ctx->n, rows_dev, nrows, x_dev, b_dev, z_dev, scr, dx_dev,
                          (cudaStream_t)stream));

@@ -245,6 +245,8 @@ cudaError_t shard_zupd(const double* A, int64_t lda, int64_t m, int64_t c_lo, in
                        double* z, cudaStream_t st);
 cudaError_t shard_rowstep(const double* A, int64_t lda, int64_t n, const int64_t* rows, int64_t nrows, const double* x,
                           const double* b, const double* z, double* r_scratch, double* dx, cudaStream_t st);
+size_t shard_colstep_scratch(int64_t m, int64_t nJ);
+size_t shard_rowstep_scratch(int64_t nrows, int64_t n);
 cudaError_t shard_xupd(int64_t n, double s, const double* dx, double* x, cudaStream_t st);
 cudaError_t shard_err(int64_t n, const double* x, const double* xs, double* out, cudaStream_t st);
 cudaError_t launch_block_norms(const double* A, int64_t lda, int64_t m, int64_t n, int axis,

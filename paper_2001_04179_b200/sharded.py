@@ -99,6 +99,38 @@ class CudaShardBackend:
         self.err_buf = torch.empty(1, dtype=torch.float64, device=self.dev)
         self.rows_cache: dict = {}
 
+    @classmethod
+    def from_device(cls, a_local, b_local, x_star, extended: bool, device: int = 0) -> "CudaShardBackend":
+        """Shard already on the GPU (torch CUDA tensors, e.g. gathered from a
+        device-built instance): no host round trip of A."""
+        import torch
+
+        from .matrix import DeviceMatrix
+
+        self = cls.__new__(cls)
+        self.torch = torch
+        self.dev = torch.device("cuda", device)
+        self.lib = _lib.load()
+        self.m_local, self.n = int(a_local.shape[0]), int(a_local.shape[1])
+        self.extended = extended
+        a = a_local.contiguous() if self.m_local else torch.zeros((1, self.n), dtype=torch.float64, device=self.dev)
+        self._a_keep = a
+        self.dm = DeviceMatrix.from_device_pointer(a.data_ptr(), a.shape[0], self.n, self.n, device)
+        self.b = (b_local if self.m_local else torch.zeros(1, dtype=torch.float64, device=self.dev)).clone()
+        self.z = self.b.clone() if extended else None
+        self.x = torch.zeros(self.n, dtype=torch.float64, device=self.dev)
+        self.xs = None if x_star is None else x_star.clone()
+        self.dx = torch.empty(self.n, dtype=torch.float64, device=self.dev)
+        self.err_buf = torch.empty(1, dtype=torch.float64, device=self.dev)
+        self.rows_cache = {}
+        return self
+
+    def err2_into(self, out):
+        """||x - x*||^2 into the device scalar `out` (no host sync)."""
+        _lib.check(self.lib.rebk_shard_err2(self.n, ctypes.c_void_p(self.x.data_ptr()),
+                                            ctypes.c_void_p(self.xs.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                            self._stream()), "err2")
+
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.dev).cuda_stream)
 
@@ -175,6 +207,72 @@ def run_sharded(backend, plan: ShardPlan, ranges: np.ndarray, max_iters: int, to
             if checking and max_iters % stride != 0:
                 final = backend.err()
                 converged = final <= tol
+    x, z = backend.state()
+    return dict(iters=iters, converged=converged, final_error=final, x=x, z_local=z)
+
+
+def run_sharded_chunked(backend, plan: ShardPlan, ranges: np.ndarray, max_iters: int, tol: float,
+                        stride: int = 1, allreduce=None, chunk: int = 32) -> dict:
+    """run_sharded without a host synchronisation per check: the errors of a
+    chunk of iterations are written on the device and read once per chunk.
+    x and z are snapshotted at the chunk start; when a check inside the chunk
+    crosses tol, the chunk is replayed from the snapshot up to exactly that
+    iteration (the kernels and the fixed-size allreduces are deterministic),
+    so the returned state is the reference's (solvers.py:444-474)."""
+    import torch
+
+    allreduce = allreduce or (lambda t: None)
+    errs = torch.empty(chunk, dtype=torch.float64, device=backend.dev)
+
+    def iterate(k):
+        j, i = int(plan.picks[k - 1, 0]), int(plan.picks[k - 1, 1])
+        if backend.extended:
+            c_lo, c_hi = int(plan.col_ptr[j]), int(plan.col_ptr[j + 1])
+            u = backend.colstep(c_lo, c_hi)
+            allreduce(u)
+            backend.zupdate(c_lo, c_hi, float(plan.col_scale[j]), u)
+        lo, hi = int(ranges[i, 0]), int(ranges[i, 1])
+        dx = backend.rowstep(lo, hi)
+        allreduce(dx)
+        backend.xupdate(float(plan.row_scale[i]), dx)
+
+    final = backend.err()
+    converged, iters = final <= tol, 0
+    k = 0
+    while not converged and k < max_iters:
+        cnt = min(chunk, max_iters - k)
+        x0 = backend.x.clone()
+        z0 = backend.z.clone() if backend.extended else None
+        checks = []
+        for t in range(cnt):
+            iterate(k + t + 1)
+            if (k + t + 1) % stride == 0:
+                backend.err2_into(errs[t:t + 1])
+                checks.append(t)
+        hit = None
+        if checks:
+            e = np.sqrt(errs[:cnt].cpu().numpy())
+            for t in checks:
+                if e[t] <= tol:
+                    hit = t
+                    break
+        if hit is not None:
+            if hit + 1 < cnt:  # replay to the crossing iteration exactly
+                backend.x.copy_(x0)
+                if z0 is not None:
+                    backend.z.copy_(z0)
+                for t in range(hit + 1):
+                    iterate(k + t + 1)
+            converged, iters, final = True, k + hit + 1, float(e[hit])
+            break
+        if checks:
+            final = float(e[checks[-1]])
+        k += cnt
+    if not converged:
+        iters = max_iters
+        if max_iters % stride != 0:
+            final = backend.err()
+            converged = final <= tol
     x, z = backend.state()
     return dict(iters=iters, converged=converged, final_error=final, x=x, z_local=z)
 

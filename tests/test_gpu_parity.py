@@ -607,3 +607,41 @@ def test_c3_full_size_matches_oracle():
     res = orc.run(wl.seed, 2000, tol, wl.x_star.cpu().numpy(), rng=NumpyRng(wl.seed))
     assert res["iters"] == tr.iters
     assert rel(x.cpu().numpy(), res["x"]) <= RTOL and rel(z.cpu().numpy(), res["z"]) <= RTOL
+
+
+def test_sharded_chunked_loop_over_nccl_c1():
+    """The multi-GPU driver as bench.py runs it (one process per GPU, NCCL
+    allreduces through torch.distributed, errors checked on the device once
+    per chunk with replay to the exact crossing) at world size 1 on the C1
+    instance: same ITER as the reference and iterates within 1e-10."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2001_04179_b200.sharded import (CudaShardBackend, owned_rows, plan_from_context,
+                                                run_sharded_chunked)
+
+    g, a, prob, cfg = c1_instance()
+    ctx = P.prepare(prob, cfg)
+    plan = plan_from_context(ctx, 2000)
+    rows, ranges = owned_rows(ctx._row_ptr, 1, 0)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        dev = torch.device("cuda", 0)
+        t = lambda v: torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+        be = CudaShardBackend.from_device(t(a[rows]), t(prob.b[rows]), t(g["x_star"]), True, 0)
+        res = run_sharded_chunked(be, plan, ranges, 2000, float(g["tol"]), allreduce=lambda v: dist.all_reduce(v),
+                                  chunk=32)
+    finally:
+        dist.destroy_process_group()
+    k = int(g["iters"])
+    assert res["converged"] and res["iters"] == k
+    assert rel(res["x"], g[f"x_{k}"]) <= RTOL
+    z = np.zeros(2000)
+    z[rows] = res["z_local"]
+    assert rel(z, g[f"z_{k}"]) <= RTOL
