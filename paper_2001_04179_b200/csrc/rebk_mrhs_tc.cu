@@ -575,7 +575,8 @@ __device__ __forceinline__ bool pk_job(const PkArgs& a, int phase, int64_t k, in
 // [B hi; B lo] is a single 128-row K-major operand: one N = 128 MMA
 // computes A_hi·B_hi and A_hi·B_lo into the two adjacent accumulators
 constexpr int RAW_FLOATS = (TM + 2 * RHS) * BK;
-constexpr size_t PK_SMEM_BYTES = (size_t)PK_NRAW * RAW_FLOATS * 4 + 1024;
+// + the epilogue's staging of the 64 x 128 Z / X values a tile updates
+constexpr size_t PK_SMEM_BYTES = (size_t)PK_NRAW * RAW_FLOATS * 4 + (size_t)RHS * TM * 4 + 1024;
 static_assert(PK_SMEM_BYTES <= 227 * 1024, "persistent ring exceeds shared memory");
 static_assert(256 + 64 * PK_NA <= 512, "TMEM: two accumulators + the A ring");
 constexpr int PK_TMEM_COLS = 512;
@@ -840,12 +841,19 @@ __global__ void __launch_bounds__(NTW, 1)
             const int r = J.row0 + row;
             const bool live = !mode0 && r < ldy;
             const bool chk = J.check && live && !(a.dbg & 16);
-            // chunk 0 of the rows this tile updates (final for this phase) is
-            // fetched while the MMAs run, chunk c+1 while chunk c is applied
-            float ycur[16], ynext[16], xcur[16], xnext[16];
+            // all 64 values of the row this thread updates (final for this
+            // phase) are copied to shared memory while the MMAs run (cp.async:
+            // no registers held, one round trip); x* chunks come through
+            // registers, chunk c+1 while chunk c is applied
+            float* s_y = smem + (size_t)PK_NRAW * RAW_FLOATS;  // [RHS][TM], this thread's row only
+            float xcur[16], xnext[16];
             if (live) {
-#pragma unroll
-              for (int q = 0; q < 16; ++q) ycur[q] = ld_cg_f32(Y + (size_t)q * ldy + r);
+#pragma unroll 8
+              for (int q = 0; q < RHS; ++q)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s_y + q * TM + row)),
+                             "l"(Y + (size_t)q * ldy + r)
+                             : "memory");
+              asm volatile("cp.async.commit_group;" ::: "memory");
             }
             if (chk) {
 #pragma unroll
@@ -855,14 +863,12 @@ __global__ void __launch_bounds__(NTW, 1)
             pht ^= 1u << b;
             if (tid == EPI0 * 32) pk_jstamp(a, k, phase, j, 4);
             umma::fence_after_sync();
+            if (live) asm volatile("cp.async.wait_all;" ::: "memory");
             const uint32_t base = tmem + ((uint32_t)rlane << 16) + b * 128;
 #pragma unroll
             for (int c0 = 0; c0 < RHS; c0 += 16) {
+              float ycur[16];
               if (c0 + 16 < RHS) {
-                if (live) {
-#pragma unroll
-                  for (int q = 0; q < 16; ++q) ynext[q] = ld_cg_f32(Y + (size_t)(c0 + 16 + q) * ldy + r);
-                }
                 if (chk) {
 #pragma unroll
                   for (int q = 0; q < 16; ++q) xnext[q] = __ldg(a.Xst + (size_t)(c0 + 16 + q) * ldy + r);
@@ -891,9 +897,12 @@ __global__ void __launch_bounds__(NTW, 1)
                 if (live && any) {
 #pragma unroll
                   for (int q = 0; q < 16; ++q) {
-                    ycur[q] = ycur[q] - J.s * (h[q] + l[q]);
+                    ycur[q] = s_y[(c0 + q) * TM + row] - J.s * (h[q] + l[q]);
                     __stcg(Y + (size_t)(c0 + q) * ldy + r, ycur[q]);
                   }
+                } else {
+#pragma unroll
+                  for (int q = 0; q < 16; ++q) ycur[q] = live ? s_y[(c0 + q) * TM + row] : 0.f;
                 }
                 if (J.check) {
                   // Σ over the warp's 32 rows of (x - x*)^2, 8 columns at a
@@ -929,10 +938,7 @@ __global__ void __launch_bounds__(NTW, 1)
                 }
               }
 #pragma unroll
-              for (int q = 0; q < 16; ++q) {
-                ycur[q] = ynext[q];
-                xcur[q] = xnext[q];
-              }
+              for (int q = 0; q < 16; ++q) xcur[q] = xnext[q];
             }
             fence_proxy_async_global();
             umma::fence_before_sync();
