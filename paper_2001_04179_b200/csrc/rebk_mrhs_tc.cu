@@ -599,6 +599,7 @@ __global__ void __launch_bounds__(NTW, 1)
   __shared__ volatile int s_stop;
   __shared__ double s_wsum[4][RHS];  // stop check: per-warp column sums of (x - x*)^2 of a tile
   __shared__ float s_half[NRED];
+  __shared__ float4 s_red4[NRED];
   __shared__ double s_errp[NRED / RHS][RHS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x;
@@ -1028,47 +1029,122 @@ __global__ void __launch_bounds__(NTW, 1)
               }
             }
           }
-          // U = Σ_q part1[q]: 128 chunks of 128 entries, two K halves per entry
+          // U = Σ_q part1[q]: 128 chunks of 128 entries (two rows j of 64
+          // columns); the chunk's 32 float4 groups get NRED / 32 threads each,
+          // thread `sub` summing slices [ns1*sub/T, ns1*(sub+1)/T) with all its
+          // loads in flight, then the T range sums are added in order
           if (a.extended && k <= a.k_end) {
             const Plan& pl = a.plan[k - a.k_begin];
             const int nJ = pl.c_hi - pl.c_lo;
-            const int e_loc = tr & 127, hf = tr >> 7;
+            constexpr int T = NRED / 32;
+            const int gi = tr / T, sub = tr % T;
             for (int ch = b; ch < 256 * RHS / 128; ch += G) {
-              const int e = ch * 128 + e_loc, j = e / RHS, c = e % RHS;
-              float s = 0.f;
-              if (hf < 2 && j < nJ) {
-                const int q0 = hf ? a.ns1 / 2 : 0, q1 = hf ? a.ns1 : a.ns1 / 2;
-#pragma unroll 8
-                for (int q = q0; q < q1; ++q) s += ld_cg_f32(a.part1 + ((size_t)q * 256 + j) * RHS + c);
+              const int j = 2 * ch + gi / 16, c4 = (gi % 16) * 4;
+              float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (j < nJ) {
+                const int q0 = (a.ns1 * sub) / T, q1 = (a.ns1 * (sub + 1)) / T;
+                const float4* src = reinterpret_cast<const float4*>(a.part1 + (size_t)j * RHS + c4);
+                constexpr int QB = 4;
+                for (int qb = q0; qb < q1; qb += QB) {
+                  float4 v[QB];
+#pragma unroll
+                  for (int u = 0; u < QB; ++u)
+                    if (qb + u < q1)
+                      asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                   : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
+                                   : "l"(src + (size_t)(qb + u) * (256 * RHS / 4))
+                                   : "memory");
+#pragma unroll
+                  for (int u = 0; u < QB; ++u)
+                    if (qb + u < q1) {
+                      acc.x += v[u].x;
+                      acc.y += v[u].y;
+                      acc.z += v[u].z;
+                      acc.w += v[u].w;
+                    }
+                }
               }
-              if (hf == 1) s_half[e_loc] = s;
+              s_red4[tr] = acc;
               named_bar(2, NRED);
-              if (hf == 0) a.Ut[(size_t)c * 256 + j] = s + s_half[e_loc];
+              if (sub == 0) {
+                for (int t = 1; t < T; ++t) {
+                  const float4 w = s_red4[tr + t];
+                  acc.x += w.x;
+                  acc.y += w.y;
+                  acc.z += w.z;
+                  acc.w += w.w;
+                }
+                const bool valid = j < nJ;
+                a.Ut[(size_t)(c4 + 0) * 256 + j] = valid ? acc.x : 0.f;
+                a.Ut[(size_t)(c4 + 1) * 256 + j] = valid ? acc.y : 0.f;
+                a.Ut[(size_t)(c4 + 2) * 256 + j] = valid ? acc.z : 0.f;
+                a.Ut[(size_t)(c4 + 3) * 256 + j] = valid ? acc.w : 0.f;
+              }
               named_bar(2, NRED);
             }
           }
         } else {
-          // R = ((Σ_q part3[q]) - B_I) + Z_I  (solvers.py:291-293 order), zero past |I|
+          // R = ((Σ_q part3[q]) - B_I) + Z_I  (solvers.py:291-293 order), zero past |I|;
+          // float4 groups as for U, b_I and z_I fetched before the partials
           const Plan& pl = a.plan[k - a.k_begin];
           const int nI = pl.r_hi - pl.r_lo;
-          const int e_loc = tr & 127, hf = tr >> 7;
+          constexpr int T = NRED / 32;
+          const int gi = tr / T, sub = tr % T;
           for (int ch = b; ch < 256 * RHS / 128; ch += G) {
-            const int e = ch * 128 + e_loc, i = e / RHS, c = e % RHS;
-            float s = 0.f;
-            if (hf < 2 && i < nI) {
-              const int q0 = hf ? a.ns3 / 2 : 0, q1 = hf ? a.ns3 : a.ns3 / 2;
-#pragma unroll 8
-              for (int q = q0; q < q1; ++q) s += ld_cg_f32(a.part3 + ((size_t)q * 256 + i) * RHS + c);
-            }
-            if (hf == 1) s_half[e_loc] = s;
-            named_bar(2, NRED);
-            if (hf == 0) {
-              float v = 0.f;
-              if (i < nI) {
-                v = (s + s_half[e_loc]) - a.Bt[(size_t)c * a.m + pl.r_lo + i];
-                if (a.extended) v += ld_cg_f32(a.Zt + (size_t)c * a.m + pl.r_lo + i);
+            const int i = 2 * ch + gi / 16, c4 = (gi % 16) * 4;
+            const bool valid = i < nI;
+            float bt[4] = {0.f, 0.f, 0.f, 0.f}, zt[4] = {0.f, 0.f, 0.f, 0.f};
+            if (sub == 0 && valid) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                bt[u] = ld_cg_f32(a.Bt + (size_t)(c4 + u) * a.m + pl.r_lo + i);
+                if (a.extended) zt[u] = ld_cg_f32(a.Zt + (size_t)(c4 + u) * a.m + pl.r_lo + i);
               }
-              a.Rt[(size_t)c * 256 + i] = v;
+            }
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid) {
+              const int q0 = (a.ns3 * sub) / T, q1 = (a.ns3 * (sub + 1)) / T;
+              const float4* src = reinterpret_cast<const float4*>(a.part3 + (size_t)i * RHS + c4);
+              constexpr int QB = 4;
+              for (int qb = q0; qb < q1; qb += QB) {
+                float4 v[QB];
+#pragma unroll
+                for (int u = 0; u < QB; ++u)
+                  if (qb + u < q1)
+                    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                 : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
+                                 : "l"(src + (size_t)(qb + u) * (256 * RHS / 4))
+                                 : "memory");
+#pragma unroll
+                for (int u = 0; u < QB; ++u)
+                  if (qb + u < q1) {
+                    acc.x += v[u].x;
+                    acc.y += v[u].y;
+                    acc.z += v[u].z;
+                    acc.w += v[u].w;
+                  }
+              }
+            }
+            s_red4[tr] = acc;
+            named_bar(2, NRED);
+            if (sub == 0) {
+              for (int t = 1; t < T; ++t) {
+                const float4 w = s_red4[tr + t];
+                acc.x += w.x;
+                acc.y += w.y;
+                acc.z += w.z;
+                acc.w += w.w;
+              }
+              const float sum[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                float v = 0.f;
+                if (valid) {
+                  v = sum[u] - bt[u];
+                  if (a.extended) v += zt[u];
+                }
+                a.Rt[(size_t)(c4 + u) * 256 + i] = v;
+              }
             }
             named_bar(2, NRED);
           }
