@@ -597,7 +597,10 @@ def run_ours_c3(args):
         "time_to_tol_s": ms / args.steps / 1e3,
         "achieved_gbps": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": profiled_traffic("c3"), "kernel": "rebk_dense_stream_kernel",
+                     "traffic": (float(profiled_traffic("c3")["bytes_per_iter"]) * per_solve
+                                 if isinstance(profiled_traffic("c3"), dict) else None),
+                     "traffic_note": (profiled_traffic("c3") or {}).get("note"),
+                     "kernel": "rebk_dense_stream_kernel",
                      "peak_source": peak_src, "algorithmic_bytes_per_iter": wl.algorithmic_bytes_per_iter,
                      "note": "the 800 MB column block is read twice per iteration (u sum, then z update): "
                              "frac <= ~0.52 by construction"},
