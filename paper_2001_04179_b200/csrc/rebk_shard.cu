@@ -42,7 +42,25 @@ __global__ void __launch_bounds__(kShardThreads) shard_colstep_part(const double
   for (int t = 0; t < kColPerLane; ++t) acc[t] = 0.0;
   constexpr int W = kShardThreads / 32;
   int64_t r = r0 + warp;
-  for (; r + W < r1; r += 2 * W) {  // two rows per step: 2 x kColPerLane loads in flight per lane
+  for (; r + 3 * W < r1; r += 4 * W) {  // four rows per step: 4 x kColPerLane loads in flight per lane
+    double zz[4];
+    double v[4][kColPerLane];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      zz[u] = __ldg(z + r + u * W);
+      const double* au = A + (r + u * W) * lda + c_lo;
+#pragma unroll
+      for (int t = 0; t < kColPerLane; ++t) {
+        const int j = lane + 32 * t;
+        v[u][t] = j < nJ ? __ldg(au + j) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int t = 0; t < kColPerLane; ++t) acc[t] = fma(v[u][t], zz[u], acc[t]);
+  }
+  for (; r + W < r1; r += 2 * W) {  // two rows per step
     const double z0 = __ldg(z + r), z1 = __ldg(z + r + W);
     const double* a0 = A + r * lda + c_lo;
     const double* a1 = a0 + W * lda;
@@ -101,13 +119,35 @@ __global__ void __launch_bounds__(256) shard_sum_parts(const double* __restrict_
   }
 }
 // z[r] -= s * Σ_j A[r, c_lo + j] u[j]  (one warp per row)
-__global__ void shard_zupdate(const double* __restrict__ A, int64_t lda, int64_t m, int64_t c_lo, int nJ, double s,
-                              const double* __restrict__ u, double* __restrict__ z) {
+__global__ void __launch_bounds__(kShardThreads) shard_zupdate(const double* __restrict__ A, int64_t lda, int64_t m,
+                                                              int64_t c_lo, int nJ, double s,
+                                                              const double* __restrict__ u, double* __restrict__ z) {
+  __shared__ double su[kColPerLane * 32];
   const int lane = threadIdx.x & 31;
+  const bool fits = nJ <= kColPerLane * 32;
+  if (fits)
+    for (int j = threadIdx.x; j < nJ; j += kShardThreads) su[j] = u[j];
+  __syncthreads();
   const int64_t r = ((int64_t)blockIdx.x * kShardThreads + threadIdx.x) >> 5;
   if (r >= m) return;
+  const double* a = A + r * lda + c_lo;
   double acc = 0.0;
-  for (int j = lane; j < nJ; j += 32) acc = fma(__ldg(A + r * lda + c_lo + j), u[j], acc);
+  if (fits) {
+    // the row's loads all in flight, then the FMAs in the lane's column order
+    double v[kColPerLane];
+#pragma unroll
+    for (int t = 0; t < kColPerLane; ++t) {
+      const int j = lane + 32 * t;
+      v[t] = j < nJ ? __ldg(a + j) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < kColPerLane; ++t) {
+      const int j = lane + 32 * t;
+      if (j < nJ) acc = fma(v[t], su[j], acc);
+    }
+  } else {
+    for (int j = lane; j < nJ; j += 32) acc = fma(__ldg(a + j), u[j], acc);
+  }
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) z[r] = z[r] - s * acc;
 }
