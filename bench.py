@@ -624,10 +624,16 @@ def run_ours_c3_sharded(args):
     import torch.distributed as dist
 
     from paper_2001_04179_b200 import _lib
-    from paper_2001_04179_b200.sharded import CudaShardBackend, ShardPlan, owned_rows, run_sharded_chunked
+    from paper_2001_04179_b200.sharded import (CudaShardBackend, NcclComm, ShardPlan, nccl_unique_id, owned_rows,
+                                                run_sharded_chunked, run_sharded_native)
     from paper_2001_04179_b200.workloads import c3_device
 
     ws, rank, local = dist_env()
+    # NCCL prints its version banner on the C-level stdout; keep stdout for
+    # the one JSON line by pointing fd 1 at stderr until the line is written
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     torch.cuda.set_device(local)
     if not dist.is_initialized():
         if ws == 1 and "MASTER_ADDR" not in os.environ:
@@ -658,10 +664,17 @@ def run_ours_c3_sharded(args):
     plan = ShardPlan(wl.row_ptr, wl.col_ptr, wl.alpha / wl.row_w, wl.alpha / wl.col_w, picks)
     log(f"[bench] c3 sharded rank {rank}/{ws}: {rows.size} rows of {m} ({time.time() - t0:.1f}s)")
 
+    # NCCL communicator owned by librebk: rank 0's unique id over torch.distributed
+    uid = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = NcclComm(uid[0], ws, rank, local)
+
     def solve():
         be = CudaShardBackend.from_device(a_local, b_local, wl.x_star, True, local)
-        return run_sharded_chunked(be, plan, ranges, args.max_iters, tol, allreduce=lambda v: dist.all_reduce(v),
-                                   chunk=32)
+        if args.python_loop:
+            return run_sharded_chunked(be, plan, ranges, args.max_iters, tol,
+                                       allreduce=lambda v: dist.all_reduce(v), chunk=32)
+        return run_sharded_native(be, comm, plan, ranges, args.max_iters, tol, chunk=32)
 
     for _ in range(max(args.warmup, 1)):
         res = solve()
@@ -694,6 +707,8 @@ def run_ours_c3_sharded(args):
                        "m": m, "n": n, "parallelism": f"row-sharded x{ws} (NCCL)", "iters_per_solve": iters / args.steps,
                        "timing": "host wall clock around whole solves, max over ranks (each solve syncs once per "
                                  "32-iteration chunk)",
+                       "driver": "python loop + torch.distributed NCCL" if args.python_loop else
+                                 "rebk_shard_run (C++ issue loop, NCCL via librebk)",
                        "l2_policy": "inputs larger than L2: A = 16 GB, no flush"},
             "time_to_tol_s": secs / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
@@ -702,8 +717,9 @@ def run_ours_c3_sharded(args):
                          "algorithmic_bytes_per_iter": abytes},
             "cpu_baseline": None, "e2e": None, "gpu_launches": 8 * iters, "clocks": clk,
         }
-        print(json.dumps(line), flush=True)
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.barrier()
+    comm.close()
     dist.destroy_process_group()
     return 0
 
@@ -720,6 +736,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="c3: row-sharded multi-GPU path (NCCL)")
+    ap.add_argument("--python-loop", action="store_true", help="--sharded: issue each iteration from Python")
     args = ap.parse_args()
     if args.impl == "reference":
         if args.workload in ("c3", "c5"):

@@ -174,6 +174,43 @@ int rebk_shard_rowstep(rebk_ctx* ctx, const int64_t* rows_dev, int64_t nrows, co
 int rebk_shard_xupdate(int64_t n, double scale, const double* dx_dev, double* x_dev, void* stream);
 int rebk_shard_err2(int64_t n, const double* x_dev, const double* xs_dev, double* out_dev, void* stream);
 
+/* ---- row-sharded multi-GPU solve over NCCL (rebk_nccl.cu) ---------------
+ * NCCL is loaded with dlopen from libnccl_path (the libnccl.so.2 torch uses;
+ * NULL/"" = the loader's default).  Rank 0 creates the unique id, the
+ * caller distributes it (e.g. torch.distributed broadcast), every rank
+ * creates its communicator.  rebk_shard_run then runs a whole solve of this
+ * rank's shard — the iteration sequence of run_sharded in sharded.py,
+ * replacing step_rebk/run (solvers.py:324-337, :425-474) — issuing the
+ * per-rank kernels and the two allreduces per iteration on one stream and
+ * reading the device-side stop checks once per `chunk` iterations (exact
+ * crossing by replay from the chunk's snapshot). */
+typedef struct rebk_shard_run_args {
+  int64_t max_iters;
+  int64_t stride;
+  double tol;              /* absolute, on ||x - x*|| */
+  int32_t chunk;
+  int32_t extended;        /* 1: REBK (column sweep), 0: RABK */
+  const int32_t* picks;    /* host [max_iters][2]: column block (or -1), row block */
+  int64_t n_col_blocks;
+  const int64_t* col_ptr;  /* host [n_col_blocks + 1] */
+  const double* col_scale; /* host [n_col_blocks] */
+  int64_t n_row_blocks;
+  const int64_t* row_ptr;  /* host [n_row_blocks + 1] (global; for validation) */
+  const double* row_scale; /* host [n_row_blocks] */
+  const int64_t* local_ranges;   /* host [n_row_blocks][2]: this rank's local rows of each block */
+  const int64_t* local_rows_dev; /* device [m_local]: 0, 1, ..., m_local - 1 */
+  const double* b_dev;     /* device [m_local] */
+  double* x_dev;           /* device [n], in/out (replicated) */
+  double* z_dev;           /* device [m_local], in/out */
+  const double* xs_dev;    /* device [n] */
+} rebk_shard_run_args;
+int rebk_nccl_get_unique_id(const char* libnccl_path, unsigned char id_out[128]);
+int rebk_nccl_comm_create(const char* libnccl_path, const unsigned char id[128], int nranks, int rank,
+                          int device, void** comm_out);
+int rebk_nccl_comm_destroy(void* comm);
+int rebk_shard_run(rebk_ctx* ctx, void* comm, const rebk_shard_run_args* args, int64_t* iters_out,
+                   int32_t* converged_out, double* final_err_out);
+
 /* ---- sampler (sampling.py:23-45 Rng, :137-145 WeightedSampler.sample) -----
  * Device sampling of the (col, row) block-index pairs of iterations
  * [k0, k0+count) (k is 1-based), written to picks_out[2*count] (host). */

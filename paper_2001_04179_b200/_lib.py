@@ -55,6 +55,29 @@ class RebkCfg(ctypes.Structure):
     ]
 
 
+class RebkShardRunArgs(ctypes.Structure):
+    _fields_ = [
+        ("max_iters", c_int64),
+        ("stride", c_int64),
+        ("tol", c_double),
+        ("chunk", c_int32),
+        ("extended", c_int32),
+        ("picks", POINTER(c_int32)),
+        ("n_col_blocks", c_int64),
+        ("col_ptr", POINTER(c_int64)),
+        ("col_scale", POINTER(c_double)),
+        ("n_row_blocks", c_int64),
+        ("row_ptr", POINTER(c_int64)),
+        ("row_scale", POINTER(c_double)),
+        ("local_ranges", POINTER(c_int64)),
+        ("local_rows_dev", c_void_p),
+        ("b_dev", c_void_p),
+        ("x_dev", c_void_p),
+        ("z_dev", c_void_p),
+        ("xs_dev", c_void_p),
+    ]
+
+
 class RebkTrace(ctypes.Structure):
     _fields_ = [
         ("iters", c_int64),
@@ -99,6 +122,10 @@ SIGNATURES = {
     "rebk_sample_sequence": (c_int, [POINTER(RebkCfg), c_int64, c_int64, POINTER(c_int32)]),
     "rebk_block_frobenius_sq": (c_int, [c_void_p, c_int, c_int64, _P_I64, _P_D]),
     "rebk_block_sigma1_sq": (c_int, [c_void_p, c_int, c_int64, _P_I64, c_int, _P_D, POINTER(c_int32)]),
+    "rebk_nccl_get_unique_id": (c_int, [c_char_p, ctypes.c_char_p]),
+    "rebk_nccl_comm_create": (c_int, [c_char_p, ctypes.c_char_p, c_int, c_int, c_int, POINTER(c_void_p)]),
+    "rebk_nccl_comm_destroy": (c_int, [c_void_p]),
+    "rebk_shard_run": (c_int, [c_void_p, c_void_p, POINTER(RebkShardRunArgs), _P_I64, POINTER(c_int32), _P_D]),
     "rebk_philox_key": (c_int, [POINTER(c_uint32), c_int64, POINTER(c_uint32), c_int64, POINTER(c_uint64)]),
     "rebk_philox_uniforms_host": (c_int, [POINTER(c_uint64), c_uint64, c_int64, _P_D]),
 }

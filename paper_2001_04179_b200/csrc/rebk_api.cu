@@ -1189,6 +1189,19 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
 
 }  // namespace
 
+namespace rebk {
+int set_error_msg(int code, const char* msg) { return fail(code, "%s", msg); }
+bool ctx_dense_view(const rebk_ctx* ctx, const double** A, int64_t* m, int64_t* n, int64_t* lda, int* device) {
+  if (!ctx || ctx->kind != 0) return false;
+  *A = ctx->A;
+  *m = ctx->m;
+  *n = ctx->n;
+  *lda = ctx->lda;
+  *device = ctx->device;
+  return true;
+}
+}  // namespace rebk
+
 extern "C" {
 
 int rebk_abi_version(void) { return REBK_ABI_VERSION; }

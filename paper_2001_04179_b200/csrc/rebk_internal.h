@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 struct rebk_cfg;
+struct rebk_ctx;
 namespace rebk {
 
 constexpr int kThreads = 256;
@@ -245,6 +246,9 @@ cudaError_t shard_zupd(const double* A, int64_t lda, int64_t m, int64_t c_lo, in
                        double* z, cudaStream_t st);
 cudaError_t shard_rowstep(const double* A, int64_t lda, int64_t n, const int64_t* rows, int64_t nrows, const double* x,
                           const double* b, const double* z, double* r_scratch, double* dx, cudaStream_t st);
+// rebk_api.cu helpers for the other C-ABI files
+int set_error_msg(int code, const char* msg);
+bool ctx_dense_view(const rebk_ctx* ctx, const double** A, int64_t* m, int64_t* n, int64_t* lda, int* device);
 size_t shard_colstep_scratch(int64_t m, int64_t nJ);
 size_t shard_rowstep_scratch(int64_t nrows, int64_t n);
 cudaError_t shard_xupd(int64_t n, double s, const double* dx, double* x, cudaStream_t st);

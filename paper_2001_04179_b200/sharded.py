@@ -313,3 +313,83 @@ def run_virtual_ranks(backends: list, plan: ShardPlan, ranges: list, max_iters: 
             iters = max_iters
     return dict(iters=iters, converged=converged, final_error=final,
                 states=[be.state() for be in backends])
+
+
+# ---------------------------------------------------------------- native (C++) driver
+def nccl_library_path() -> str:
+    """The libnccl.so.2 torch loads (the nvidia-nccl wheel), else the loader default."""
+    try:
+        import nvidia.nccl
+
+        import os
+
+        for base in nvidia.nccl.__path__:
+            cand = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                return cand
+    except Exception:
+        pass
+    return "libnccl.so.2"
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _lib.check(_lib.load().rebk_nccl_get_unique_id(nccl_library_path().encode(), buf), "rebk_nccl_get_unique_id")
+    return buf.raw
+
+
+class NcclComm:
+    """NCCL communicator owned by librebk (rebk_nccl_comm_create); every rank
+    passes the same 128-byte unique id (rank 0's, distributed by the caller)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int = 0):
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().rebk_nccl_comm_create(nccl_library_path().encode(), uid, nranks, rank, device,
+                                                     ctypes.byref(h)), "rebk_nccl_comm_create")
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.load().rebk_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
+def run_sharded_native(backend: CudaShardBackend, comm: NcclComm, plan: ShardPlan, ranges: np.ndarray,
+                       max_iters: int, tol: float, stride: int = 1, chunk: int = 32) -> dict:
+    """run_sharded_chunked with the whole loop in C++ (rebk_shard_run): the
+    per-rank kernels and both NCCL allreduces of every iteration are issued
+    from librebk on one stream, no Python per iteration."""
+    import torch
+
+    args = _lib.RebkShardRunArgs()
+    picks = np.ascontiguousarray(plan.picks[:max_iters], dtype=np.int32)
+    row_ptr = np.ascontiguousarray(plan.row_ptr, dtype=np.int64)
+    row_scale = np.ascontiguousarray(plan.row_scale, dtype=np.float64)
+    rng = np.ascontiguousarray(ranges, dtype=np.int64)
+    keep = [picks, row_ptr, row_scale, rng]
+    args.max_iters, args.stride, args.tol, args.chunk = int(max_iters), int(stride), float(tol), int(chunk)
+    args.extended = 1 if backend.extended else 0
+    args.picks = picks.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    if backend.extended:
+        col_ptr = np.ascontiguousarray(plan.col_ptr, dtype=np.int64)
+        col_scale = np.ascontiguousarray(plan.col_scale, dtype=np.float64)
+        keep += [col_ptr, col_scale]
+        args.n_col_blocks = col_ptr.size - 1
+        args.col_ptr, args.col_scale = _lib.i64ptr(col_ptr), _lib.dptr(col_scale)
+    args.n_row_blocks = row_ptr.size - 1
+    args.row_ptr, args.row_scale = _lib.i64ptr(row_ptr), _lib.dptr(row_scale)
+    args.local_ranges = _lib.i64ptr(rng)
+    rows = torch.arange(max(backend.m_local, 1), dtype=torch.int64, device=backend.dev)
+    args.local_rows_dev = rows.data_ptr()
+    args.b_dev, args.x_dev = backend.b.data_ptr(), backend.x.data_ptr()
+    args.z_dev = backend.z.data_ptr() if backend.extended else None
+    args.xs_dev = backend.xs.data_ptr()
+    torch.cuda.synchronize(backend.dev)  # x, z, b initialised on torch's stream
+    it = ctypes.c_int64()
+    conv = ctypes.c_int32()
+    err = ctypes.c_double()
+    _lib.check(_lib.load().rebk_shard_run(backend.dm.handle, comm.handle, ctypes.byref(args), ctypes.byref(it),
+                                          ctypes.byref(conv), ctypes.byref(err)), "rebk_shard_run")
+    del keep
+    x, z = backend.state()
+    return dict(iters=int(it.value), converged=bool(conv.value), final_error=float(err.value), x=x, z_local=z)

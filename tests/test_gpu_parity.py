@@ -645,3 +645,33 @@ def test_sharded_chunked_loop_over_nccl_c1():
     z = np.zeros(2000)
     z[rows] = res["z_local"]
     assert rel(z, g[f"z_{k}"]) <= RTOL
+
+
+def test_sharded_native_nccl_runner_c1():
+    """rebk_shard_run (the whole sharded loop in C++, NCCL loaded by librebk,
+    world size 1) on the C1 instance: same ITER as the reference and iterates
+    within 1e-10."""
+    import torch
+
+    from paper_2001_04179_b200.sharded import (CudaShardBackend, NcclComm, nccl_unique_id, owned_rows,
+                                                plan_from_context, run_sharded_native)
+
+    g, a, prob, cfg = c1_instance()
+    ctx = P.prepare(prob, cfg)
+    plan = plan_from_context(ctx, 2000)
+    rows, ranges = owned_rows(ctx._row_ptr, 1, 0)
+    dev = torch.device("cuda", 0)
+    t = lambda v: torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+    comm = NcclComm(nccl_unique_id(), 1, 0, 0)
+    try:
+        for chunk in (32, 7):
+            be = CudaShardBackend.from_device(t(a[rows]), t(prob.b[rows]), t(g["x_star"]), True, 0)
+            res = run_sharded_native(be, comm, plan, ranges, 2000, float(g["tol"]), chunk=chunk)
+            k = int(g["iters"])
+            assert res["converged"] and res["iters"] == k, (chunk, res["iters"])
+            assert rel(res["x"], g[f"x_{k}"]) <= RTOL
+            z = np.zeros(2000)
+            z[rows] = res["z_local"]
+            assert rel(z, g[f"z_{k}"]) <= RTOL
+    finally:
+        comm.close()
