@@ -251,7 +251,9 @@ def run_sharded_chunked(backend, plan: ShardPlan, ranges: np.ndarray, max_iters:
                 checks.append(t)
         hit = None
         if checks:
-            e = np.sqrt(errs[:cnt].cpu().numpy())
+            vals = errs[:cnt].cpu().numpy()
+            e = np.full(cnt, np.inf)
+            e[checks] = np.sqrt(vals[checks])  # only the checked slots were written
             for t in checks:
                 if e[t] <= tol:
                     hit = t

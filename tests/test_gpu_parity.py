@@ -675,3 +675,53 @@ def test_sharded_native_nccl_runner_c1():
             assert rel(z, g[f"z_{k}"]) <= RTOL
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("algorithm", ["rebk", "rabk"])
+def test_sharded_native_equals_python_loop(algorithm):
+    """The C++ issue loop (rebk_shard_run) and the Python loop
+    (run_sharded_chunked over torch.distributed) launch the same kernels in
+    the same order: identical ITER and bitwise-identical iterates, for REBK
+    and for RABK (no column sweep), with a check stride and a chunk that
+    does not divide it."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2001_04179_b200.sharded import (CudaShardBackend, NcclComm, nccl_unique_id, owned_rows,
+                                                plan_from_context, run_sharded_chunked, run_sharded_native)
+
+    g, a, prob, cfg = c1_instance()
+    cfg.algorithm = algorithm
+    if algorithm == "rabk":
+        cfg.col_partition = None
+    ctx = P.prepare(prob, cfg)
+    plan = plan_from_context(ctx, 3000)
+    rows, ranges = owned_rows(ctx._row_ptr, 1, 0)
+    dev = torch.device("cuda", 0)
+    t = lambda v: torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+    ext = algorithm == "rebk"
+    tol, stride = float(g["tol"]), 3
+    comm = NcclComm(nccl_unique_id(), 1, 0, 0)
+    try:
+        be = CudaShardBackend.from_device(t(a[rows]), t(prob.b[rows]), t(g["x_star"]), ext, 0)
+        nat = run_sharded_native(be, comm, plan, ranges, 3000, tol, stride=stride, chunk=10)
+    finally:
+        comm.close()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        be = CudaShardBackend.from_device(t(a[rows]), t(prob.b[rows]), t(g["x_star"]), ext, 0)
+        py = run_sharded_chunked(be, plan, ranges, 3000, tol, stride=stride, allreduce=lambda v: dist.all_reduce(v),
+                                 chunk=10)
+    finally:
+        dist.destroy_process_group()
+    assert nat["converged"] == py["converged"] and nat["iters"] == py["iters"]
+    assert nat["iters"] % stride == 0
+    assert np.array_equal(nat["x"], py["x"])
+    if ext:
+        assert np.array_equal(nat["z_local"], py["z_local"])
