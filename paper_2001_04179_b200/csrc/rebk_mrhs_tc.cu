@@ -442,6 +442,9 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // PK_GBAR_FENCE: 2 = __threadfence() before the release add (fence.sc),
 // 1 = fence.acq_rel.gpu, 0 = the release add alone (its release semantics are
 // cumulative over the CTA's writes ordered before it by the named barrier)
+#ifndef PK_P4_WEIGHT_X4
+#define PK_P4_WEIGHT_X4 6  // 4 x (cost of a P4 k-block in P1 stages): 6 measured best (82.9 vs 83.7 ms at 4, 8)
+#endif
 #ifndef PK_GBAR_FENCE
 #define PK_GBAR_FENCE 0  // measured on C5: 0 98.8 ms, 1 101.4, 2 102.0 per solve
 #endif
@@ -517,7 +520,7 @@ __device__ __forceinline__ bool pk_job(const PkArgs& a, int phase, int64_t k, in
         int kb4 = 0, np4 = 0;
         if (k - 1 >= a.k_begin) {
           const Plan& pp = a.plan[k - 1 - a.k_begin];
-          kb4 = (pp.r_hi - pp.r_lo + BK - 1) / BK;
+          kb4 = ((pp.r_hi - pp.r_lo + BK - 1) / BK) * PK_P4_WEIGHT_X4 / 4;  // P4 job cost in P1 stages
           np4 = (a.nt4 + 1) / 2;
         }
         const int64_t T = (int64_t)a.nkb_m + (int64_t)kb4 * np4;
