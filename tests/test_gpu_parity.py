@@ -725,3 +725,29 @@ def test_sharded_native_equals_python_loop(algorithm):
     assert np.array_equal(nat["x"], py["x"])
     if ext:
         assert np.array_equal(nat["z_local"], py["z_local"])
+
+
+@pytest.mark.parametrize("max_iters,stride", [(0, 1), (200, 10), (205, 10), (37, 1)])
+def test_run_budget_and_checkpoint_semantics_c1(max_iters, stride):
+    """run() semantics of solvers.py:425-474 on the device path (split kernel,
+    C1): a zero budget stops after the k = 0 check; checks every `stride`
+    iterations plus a final one when max_iters is not a multiple of it;
+    recorded errors and checkpoints, x and z equal the CPU restatement's."""
+    g, a, prob, cfg = c1_instance()
+    cfg.max_iters = max_iters
+    cfg.stop = P.StoppingRule(tol=1e-300, check_stride=stride)
+    cfg.record_errors = True
+    tr = P.run(prob, cfg)
+    orc = OracleSolver(a, prob.b, cfg.row_partition.pointers(), cfg.col_partition.pointers(), cfg.alpha, "rebk")
+    res = orc.run(int(g["seed"]), max_iters, 1e-300, g["x_star"], stride=stride, record=True)
+    assert not tr.converged and tr.iters == res["iters"] == max_iters
+    want = list(range(0, max_iters + 1, stride))
+    if max_iters % stride:
+        want.append(max_iters)
+    assert tr.checkpoints.tolist() == res["checkpoints"].tolist() == want
+    np.testing.assert_allclose(tr.errors, res["errors"], rtol=1e-10, atol=0)
+    assert tr.final_error == pytest.approx(float(res["errors"][-1]), rel=1e-10)
+    if max_iters == 0:
+        assert np.all(tr.x == 0.0) and np.array_equal(tr.z, prob.b)
+    else:
+        assert rel(tr.x, res["x"]) <= RTOL and rel(tr.z, res["z"]) <= RTOL
