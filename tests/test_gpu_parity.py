@@ -751,3 +751,23 @@ def test_run_budget_and_checkpoint_semantics_c1(max_iters, stride):
         assert np.all(tr.x == 0.0) and np.array_equal(tr.z, prob.b)
     else:
         assert rel(tr.x, res["x"]) <= RTOL and rel(tr.z, res["z"]) <= RTOL
+
+
+@pytest.mark.parametrize("with_z0", [False, True])
+def test_warm_start_x0_z0_c1(with_z0):
+    """Non-default starting points (SolverConfig.x0 / z0, solvers.py:231-265)
+    through the device path: same iterates as the CPU restatement started
+    from the same x0 (and z0)."""
+    g, a, prob, cfg = c1_instance()
+    rng = np.random.default_rng(5)
+    x0 = 0.1 * rng.standard_normal(500)
+    z0 = prob.b + 0.01 * rng.standard_normal(2000) if with_z0 else None
+    cfg.x0, cfg.z0 = x0, z0
+    cfg.max_iters = 150
+    cfg.stop = P.StoppingRule(tol=1e-300, check_stride=5)
+    tr = P.run(prob, cfg)
+    orc = OracleSolver(a, prob.b, cfg.row_partition.pointers(), cfg.col_partition.pointers(), cfg.alpha, "rebk")
+    res = orc.run(int(g["seed"]), 150, 1e-300, g["x_star"], stride=5, x0=x0, z0=z0)
+    assert tr.iters == res["iters"] == 150
+    assert rel(tr.x, res["x"]) <= RTOL and rel(tr.z, res["z"]) <= RTOL
+    assert tr.final_error == pytest.approx(float(res["final_error"]), rel=1e-10)
