@@ -294,12 +294,23 @@ def run_ours(args):
 
     # e2e through the public API from pinned host buffers, A re-uploaded each step
     e2e = None
-    if not args.no_e2e and not prob.a.is_sparse:
-        a_pin = torch.from_numpy(prob.a.to_dense()).pin_memory()
+    if not args.no_e2e:
         b_pin = torch.from_numpy(prob.b).pin_memory()
         xs_pin = torch.from_numpy(np.asarray(prob.x_star)).pin_memory()
-        mat = P.Matrix.from_dense(a_pin.numpy())
-        assert mat.to_dense().ctypes.data == a_pin.data_ptr()
+        if prob.a.is_sparse:
+            import scipy.sparse as sps
+
+            csr = prob.a._csr
+            pins = [torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for v in (csr.data, csr.indices,
+                                                                                   csr.indptr)]
+            mat = P.Matrix.from_sparse(sps.csr_matrix((pins[0].numpy(), pins[1].numpy(), pins[2].numpy()),
+                                                      shape=csr.shape))
+            a_bytes = int(csr.data.nbytes + csr.indices.nbytes + csr.indptr.nbytes)
+        else:
+            a_pin = torch.from_numpy(prob.a.to_dense()).pin_memory()
+            mat = P.Matrix.from_dense(a_pin.numpy())
+            assert mat.to_dense().ctypes.data == a_pin.data_ptr()
+            a_bytes = int(m * n * 8)
         prob2 = P.ProblemInstance(a=mat, b=b_pin.numpy(), x_star=xs_pin.numpy(), b_perp=None, meta=prob.meta)
         cfg2 = wl.config(max_iters=args.max_iters)
         cfg2.row_partition, cfg2.col_partition = wl.row_partition, wl.col_partition
@@ -321,7 +332,7 @@ def run_ours(args):
             dist.all_reduce(ei_t, op=dist.ReduceOp.SUM)
         e2e = {
             "value": float(ei_t.item()) / float(e_t.item()), "unit": UNIT,
-            "h2d_bytes_per_step": int(m * n * 8 + 2 * m * 8 + 2 * n * 8),
+            "h2d_bytes_per_step": int(a_bytes + 2 * m * 8 + 2 * n * 8),
             "d2h_bytes_per_step": int((m + n) * 8 + 64),
             "time_to_tol_s": float(e_t.item()) / args.steps,
             "path": "paper_2001_04179_b200.run(problem, config): A, b, x* uploaded from pinned host memory "
