@@ -243,6 +243,15 @@ int rebk_philox_key(const uint32_t* entropy_words, int64_t n_entropy_words,
 int rebk_philox_uniforms_host(const uint64_t key[2], uint64_t first, int64_t count,
                               double* out);
 
+/* Host-side helper for the sampler weights (matrix.py:170-189): one
+ * sequential pass over a row-major host matrix (row stride lda) that writes
+ * every column block ptr[k]..ptr[k+1] of a contiguous partition (ptr[0] = 0,
+ * ptr[nb] = cols) as its own C-order array at out + rows*ptr[k] — the array
+ * np.ravel(A[:, J]) builds — with up to nthreads host threads.  The weight
+ * stays numpy's `flat @ flat` on that array, keeping the reference's bits. */
+int rebk_host_gather_col_blocks(const double* a, int64_t rows, int64_t cols, int64_t lda, int64_t nb,
+                                const int64_t* ptr, double* out, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -128,6 +128,7 @@ SIGNATURES = {
     "rebk_shard_run": (c_int, [c_void_p, c_void_p, POINTER(RebkShardRunArgs), _P_I64, POINTER(c_int32), _P_D]),
     "rebk_philox_key": (c_int, [POINTER(c_uint32), c_int64, POINTER(c_uint32), c_int64, POINTER(c_uint64)]),
     "rebk_philox_uniforms_host": (c_int, [POINTER(c_uint64), c_uint64, c_int64, _P_D]),
+    "rebk_host_gather_col_blocks": (c_int, [_P_D, c_int64, c_int64, c_int64, c_int64, _P_I64, _P_D, c_int]),
 }
 
 _lib = None

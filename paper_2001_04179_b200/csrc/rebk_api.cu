@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/rebk.h"
@@ -1769,6 +1770,36 @@ int rebk_philox_uniforms_host(const uint64_t key[2], uint64_t first, int64_t cou
     const u64x4 blk = philox_block(d >> 2, key[0], key[1]);
     out[q] = u64_to_unit_double(blk.v[d & 3]);
   }
+  return REBK_OK;
+}
+
+int rebk_host_gather_col_blocks(const double* a, int64_t rows, int64_t cols, int64_t lda, int64_t nb,
+                                const int64_t* ptr, double* out, int nthreads) {
+  if (!a || !ptr || !out || rows < 0 || nb < 1 || cols > lda || ptr[0] != 0 || ptr[nb] != cols)
+    return fail(REBK_EINVAL, "rebk_host_gather_col_blocks: bad argument");
+  for (int64_t k = 0; k < nb; ++k)
+    if (ptr[k + 1] <= ptr[k]) return fail(REBK_EINVAL, "rebk_host_gather_col_blocks: empty or unordered block");
+  if (rows == 0) return REBK_OK;
+  // one sequential pass over A: row r's slice of block k lands at
+  // out[rows*ptr[k] + r*w_k], i.e. every block as its own C-order array.
+  // Threads own row slabs; the copy only moves bytes, so no result bit
+  // depends on the thread count.
+  int64_t nt = std::max<int64_t>(1, std::min<int64_t>(nthreads, (rows * cols) >> 16));
+  nt = std::min<int64_t>(nt, rows);
+  auto copy = [=](int64_t r0, int64_t r1) {
+    for (int64_t r = r0; r < r1; ++r) {
+      const double* src = a + r * lda;
+      for (int64_t k = 0; k < nb; ++k) {
+        const int64_t w = ptr[k + 1] - ptr[k];
+        memcpy(out + rows * ptr[k] + r * w, src + ptr[k], (size_t)w * sizeof(double));
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  pool.reserve(nt - 1);
+  for (int64_t t = 1; t < nt; ++t) pool.emplace_back(copy, rows * t / nt, rows * (t + 1) / nt);
+  copy(0, rows / nt);
+  for (auto& th : pool) th.join();
   return REBK_OK;
 }
 

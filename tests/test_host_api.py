@@ -112,3 +112,30 @@ def test_out_of_regime_warning_without_device():
 def test_run_without_gpu_raises_not_falls_back():
     with pytest.raises(_lib.RebkError):
         P.run(problem(), P.SolverConfig(algorithm="rek", max_iters=5))
+
+
+@pytest.mark.parametrize("shape,tau", [((300, 250), 40), ((64, 1000), 200), ((7, 9), 2)])
+def test_gathered_column_weights_bitwise(shape, tau):
+    """The threaded single-pass column-block gather (rebk_host_gather_col_blocks)
+    gives the exact bits of the reference's `flat @ flat` on np.ravel(A[:, J])
+    (matrix.py:170-189), ragged last block included."""
+    a = np.random.default_rng(5).standard_normal(shape)
+    m = P.Matrix.from_dense(a)
+    p = P.contiguous_partition(shape[1], tau, "col")
+    want = []
+    for blk in p.blocks:
+        flat = np.ravel(a[:, blk.start:blk.stop])
+        want.append(float(flat @ flat))
+    got = m.col_block_weights(p.pointers())
+    assert got == want
+    assert list(P.build_sampler(m, p).weights) == want
+    # a partition the gather does not cover keeps the per-block path
+    assert m.col_block_weights(np.array([0, shape[1]], dtype=np.int64)) == [float(np.ravel(a) @ np.ravel(a))]
+
+
+def test_gather_rejects_bad_pointers():
+    lib = _lib.load()
+    a = np.zeros((4, 6))
+    out = np.empty(a.size)
+    bad = np.array([0, 3, 3, 6], dtype=np.int64)
+    assert lib.rebk_host_gather_col_blocks(_lib.dptr(a), 4, 6, 6, 3, _lib.i64ptr(bad), _lib.dptr(out), 2) != 0
