@@ -190,6 +190,7 @@ class SolverContext:
 
         row_p = self._resolve_partition(config.row_partition, "row", self.a.rows)
         self.row_partition = row_p
+        self._prefetch_device(row_p, config.col_partition if (algo in _NEEDS_COL_PARTITION or algo == "rek") else None)
         self.row_sampler = build_sampler(self.a, row_p)
         self.row_scales = [float(self.alpha / w) for w in self.row_sampler.weights]
         self.row_selectors = [slice(i.start, i.stop) if isinstance(i, range) else i for i in row_p.blocks]
@@ -245,6 +246,17 @@ class SolverContext:
         return p
 
     # -- device binding ---------------------------------------------------------
+
+    def _prefetch_device(self, row_p: Partition, col_p: Partition | None) -> None:
+        """Overlap the H2D copy of a dense A with the host sampler setup when
+        the device layout is already known (contiguous column blocks, or no
+        column partition): the copy _bind_device/device_matrix will ask for."""
+        if self.a.is_sparse or os.environ.get("REBK_PREFETCH", "1") == "0":
+            return
+        if col_p is not None and not (isinstance(col_p, Partition) and col_p.is_contiguous_in_order()):
+            return
+        row_order = None if row_p.is_contiguous_in_order() else row_p.order()
+        self.a.prefetch_device(row_order, None)
 
     def _bind_device(self) -> None:
         self.row_order = None if self.row_partition.is_contiguous_in_order() else self.row_partition.order()
