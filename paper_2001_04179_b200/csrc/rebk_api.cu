@@ -465,6 +465,9 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
   std::vector<int64_t> coff(t + 1, 0), clo, chi, ccta, cptr(1, 0);
   std::vector<int32_t> crow, ccolv;
   std::vector<double> cval;
+  // the column-block lists (a pass over CSR) and the row-block lists (a pass
+  // over CSC) are independent: build them on two host threads
+  auto build_col_lists = [&]() {
   if (extended) {
     std::vector<int32_t> blk_of_col(n);
     for (int64_t b = 0; b < t; ++b)
@@ -517,11 +520,12 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
             std::lower_bound(crow.begin() + coff[b], crow.begin() + coff[b + 1], r0) - crow.begin();
       }
   }
+  };
   // row blocks -> column segments into CSC
   std::vector<int64_t> roff(s + 1, 0), rlo, rhi, rcta, rptr(1, 0);
   std::vector<int32_t> rcol, rrowv;
   std::vector<double> rval;
-  {
+  auto build_row_lists = [&]() {
     std::vector<int32_t> blk_of_row(m);
     for (int64_t b = 0; b < s; ++b)
       for (int64_t i = cfg->row_ptr[b]; i < cfg->row_ptr[b + 1]; ++i) blk_of_row[i] = (int32_t)b;
@@ -571,6 +575,11 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
         rcta[b * (G + 1) + q] =
             std::lower_bound(rcol.begin() + roff[b], rcol.begin() + roff[b + 1], c0) - rcol.begin();
       }
+  };
+  {
+    std::thread col_thread(build_col_lists);
+    build_row_lists();
+    col_thread.join();
   }
   cudaError_t e = cudaSuccess;
   if (!e) e = upload_vec(&sp->cseg_off, coff);

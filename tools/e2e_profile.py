@@ -14,9 +14,12 @@ import paper_2001_04179_b200 as P  # noqa: E402
 from paper_2001_04179_b200 import workloads  # noqa: E402
 
 wl = workloads.build(sys.argv[1] if len(sys.argv) > 1 else "c2")
-a_pin = torch.from_numpy(wl.problem.a.to_dense()).pin_memory()
-prob = P.ProblemInstance(a=P.Matrix.from_dense(a_pin.numpy()), b=wl.problem.b, x_star=wl.problem.x_star,
-                         b_perp=None, meta=wl.problem.meta)
+if wl.problem.a.is_sparse:
+    mat = wl.problem.a
+else:
+    a_pin = torch.from_numpy(wl.problem.a.to_dense()).pin_memory()
+    mat = P.Matrix.from_dense(a_pin.numpy())
+prob = P.ProblemInstance(a=mat, b=wl.problem.b, x_star=wl.problem.x_star, b_perp=None, meta=wl.problem.meta)
 cfg = wl.config()
 cfg.row_partition, cfg.col_partition = wl.row_partition, wl.col_partition
 for _ in range(2):
