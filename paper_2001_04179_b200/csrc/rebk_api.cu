@@ -443,6 +443,101 @@ void free_seg_plan(CsrSegPlan* sp) {
   delete sp;
 }
 
+// Segment lists of one orientation of a sparse matrix stored by major lines
+// (CSR: rows, CSC: columns).  The blocks partition the minor axis
+// (bptr[nb+1]); for every block: the major lines with nonzeros in it, in
+// major order, their [lo, hi) entry range, a compact copy of those entries
+// (minor index relative to the block start) and each of the G CTAs' first
+// segment (major axis split by split_rows).  T host threads own contiguous
+// major ranges; per-(thread, block) counts give every thread its write
+// offsets, so the lists are identical to a sequential pass.
+struct SegLists {
+  std::vector<int64_t> off, lo, hi, ptr, cta;
+  std::vector<int32_t> major_id, minor_local;
+  std::vector<double> val;
+};
+
+template <class F>
+void parallel_for_threads(int T, F&& f) {
+  std::vector<std::thread> pool;
+  pool.reserve(T - 1);
+  for (int th = 1; th < T; ++th) pool.emplace_back(f, th);
+  f(0);
+  for (auto& t : pool) t.join();
+}
+
+void seg_lists(int64_t nmajor, const int64_t* mptr, const int32_t* minor, const double* vals, int64_t nminor,
+               int64_t nb, const int64_t* bptr, int G, int T, SegLists& L) {
+  T = (int)std::max<int64_t>(1, std::min<int64_t>(T, nmajor / 4096));
+  std::vector<int32_t> blk(nminor);
+  for (int64_t q = 0; q < nb; ++q)
+    for (int64_t j = bptr[q]; j < bptr[q + 1]; ++j) blk[j] = (int32_t)q;
+  auto lo_of = [&](int th) { return nmajor * th / T; };
+  std::vector<int64_t> cnt((size_t)T * nb, 0);
+  parallel_for_threads(T, [&](int th) {
+    int64_t* c = cnt.data() + (size_t)th * nb;
+    for (int64_t i = lo_of(th); i < lo_of(th + 1); ++i) {
+      int32_t prev = -1;
+      for (int64_t e = mptr[i]; e < mptr[i + 1]; ++e) {
+        const int32_t q = blk[minor[e]];
+        if (q != prev) ++c[q];
+        prev = q;
+      }
+    }
+  });
+  L.off.assign(nb + 1, 0);
+  std::vector<int64_t> fill((size_t)T * nb);
+  for (int64_t q = 0; q < nb; ++q) {
+    int64_t acc = L.off[q];
+    for (int th = 0; th < T; ++th) {
+      fill[(size_t)th * nb + q] = acc;
+      acc += cnt[(size_t)th * nb + q];
+    }
+    L.off[q + 1] = acc;
+  }
+  const int64_t ns = L.off[nb];
+  L.lo.resize(ns); L.hi.resize(ns); L.major_id.resize(ns);
+  parallel_for_threads(T, [&](int th) {
+    int64_t* f = fill.data() + (size_t)th * nb;
+    for (int64_t i = lo_of(th); i < lo_of(th + 1); ++i) {
+      int32_t prev = -1;
+      int64_t cur = -1;
+      for (int64_t e = mptr[i]; e < mptr[i + 1]; ++e) {
+        const int32_t q = blk[minor[e]];
+        if (q != prev) {
+          cur = f[q]++;
+          L.major_id[cur] = (int32_t)i;
+          L.lo[cur] = e;
+        }
+        L.hi[cur] = e + 1;
+        prev = q;
+      }
+    }
+  });
+  L.ptr.resize(ns + 1);
+  L.ptr[0] = 0;
+  for (int64_t k = 0; k < ns; ++k) L.ptr[k + 1] = L.ptr[k] + (L.hi[k] - L.lo[k]);
+  L.val.resize(L.ptr[ns]);
+  L.minor_local.resize(L.ptr[ns]);
+  parallel_for_threads(T, [&](int th) {
+    for (int64_t q = th; q < nb; q += T)
+      for (int64_t k = L.off[q]; k < L.off[q + 1]; ++k)
+        for (int64_t e = L.lo[k]; e < L.hi[k]; ++e) {
+          const int64_t o = L.ptr[k] + (e - L.lo[k]);
+          L.val[o] = vals[e];
+          L.minor_local[o] = minor[e] - (int32_t)bptr[q];
+        }
+  });
+  L.cta.resize(nb * (G + 1));
+  for (int64_t q = 0; q < nb; ++q)
+    for (int g = 0; g <= G; ++g) {
+      const int32_t r0 = split_rows(nmajor, G, g);
+      L.cta[q * (G + 1) + g] =
+          std::lower_bound(L.major_id.begin() + L.off[q], L.major_id.begin() + L.off[q + 1], r0) -
+          L.major_id.begin();
+    }
+}
+
 // Segment lists of one partition: for every column block, the rows with
 // nonzeros in it and their [lo, hi) range in the CSR arrays (sorted by row);
 // for every row block, the columns with nonzeros in it and their range in the
@@ -461,126 +556,18 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
   sp->G = G;
   sp->row_ptr.assign(cfg->row_ptr, cfg->row_ptr + s + 1);
   if (extended) sp->col_ptr.assign(cfg->col_ptr, cfg->col_ptr + t + 1);
+  const int T = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  SegLists C, R;
+  C.off.assign(1, 0);
+  C.ptr.assign(1, 0);
   // column blocks -> row segments into CSR
-  std::vector<int64_t> coff(t + 1, 0), clo, chi, ccta, cptr(1, 0);
-  std::vector<int32_t> crow, ccolv;
-  std::vector<double> cval;
-  // the column-block lists (a pass over CSR) and the row-block lists (a pass
-  // over CSC) are independent: build them on two host threads
-  auto build_col_lists = [&]() {
-  if (extended) {
-    std::vector<int32_t> blk_of_col(n);
-    for (int64_t b = 0; b < t; ++b)
-      for (int64_t j = cfg->col_ptr[b]; j < cfg->col_ptr[b + 1]; ++j) blk_of_col[j] = (int32_t)b;
-    std::vector<int64_t> cnt(t, 0);
-    for (int64_t i = 0; i < m; ++i) {
-      int32_t prev = -1;
-      for (int64_t e = ctx->h_csr_ptr[i]; e < ctx->h_csr_ptr[i + 1]; ++e) {
-        const int32_t b = blk_of_col[ctx->h_csr_col[e]];
-        if (b != prev) ++cnt[b];
-        prev = b;
-      }
-    }
-    for (int64_t b = 0; b < t; ++b) coff[b + 1] = coff[b] + cnt[b];
-    const int64_t ns = coff[t];
-    clo.resize(ns); chi.resize(ns); crow.resize(ns);
-    std::vector<int64_t> fill(coff.begin(), coff.end() - 1);
-    for (int64_t i = 0; i < m; ++i) {
-      int32_t prev = -1;
-      int64_t cur = -1;
-      for (int64_t e = ctx->h_csr_ptr[i]; e < ctx->h_csr_ptr[i + 1]; ++e) {
-        const int32_t b = blk_of_col[ctx->h_csr_col[e]];
-        if (b != prev) {
-          cur = fill[b]++;
-          crow[cur] = (int32_t)i;
-          clo[cur] = e;
-        }
-        chi[cur] = e + 1;
-        prev = b;
-      }
-    }
-    // compact copies of each column block's entries, segment by segment
-    cptr.resize(ns + 1);
-    cptr[0] = 0;
-    for (int64_t q = 0; q < ns; ++q) cptr[q + 1] = cptr[q] + (chi[q] - clo[q]);
-    cval.resize(cptr[ns]);
-    ccolv.resize(cptr[ns]);
-    for (int64_t b = 0; b < t; ++b)
-      for (int64_t q = coff[b]; q < coff[b + 1]; ++q)
-        for (int64_t e = clo[q]; e < chi[q]; ++e) {
-          const int64_t o = cptr[q] + (e - clo[q]);
-          cval[o] = ctx->h_csr_val[e];
-          ccolv[o] = ctx->h_csr_col[e] - (int32_t)cfg->col_ptr[b];
-        }
-    ccta.resize(t * (G + 1));
-    for (int64_t b = 0; b < t; ++b)
-      for (int q = 0; q <= G; ++q) {
-        const int32_t r0 = split_rows(m, G, q);
-        ccta[b * (G + 1) + q] =
-            std::lower_bound(crow.begin() + coff[b], crow.begin() + coff[b + 1], r0) - crow.begin();
-      }
-  }
-  };
+  if (extended)
+    seg_lists(m, ctx->h_csr_ptr.data(), ctx->h_csr_col.data(), ctx->h_csr_val.data(), n, t, cfg->col_ptr, G, T, C);
   // row blocks -> column segments into CSC
-  std::vector<int64_t> roff(s + 1, 0), rlo, rhi, rcta, rptr(1, 0);
-  std::vector<int32_t> rcol, rrowv;
-  std::vector<double> rval;
-  auto build_row_lists = [&]() {
-    std::vector<int32_t> blk_of_row(m);
-    for (int64_t b = 0; b < s; ++b)
-      for (int64_t i = cfg->row_ptr[b]; i < cfg->row_ptr[b + 1]; ++i) blk_of_row[i] = (int32_t)b;
-    std::vector<int64_t> cnt(s, 0);
-    for (int64_t j = 0; j < n; ++j) {
-      int32_t prev = -1;
-      for (int64_t e = ctx->h_csc_ptr[j]; e < ctx->h_csc_ptr[j + 1]; ++e) {
-        const int32_t b = blk_of_row[ctx->h_csc_row[e]];
-        if (b != prev) ++cnt[b];
-        prev = b;
-      }
-    }
-    for (int64_t b = 0; b < s; ++b) roff[b + 1] = roff[b] + cnt[b];
-    const int64_t ns = roff[s];
-    rlo.resize(ns); rhi.resize(ns); rcol.resize(ns);
-    std::vector<int64_t> fill(roff.begin(), roff.end() - 1);
-    for (int64_t j = 0; j < n; ++j) {
-      int32_t prev = -1;
-      int64_t cur = -1;
-      for (int64_t e = ctx->h_csc_ptr[j]; e < ctx->h_csc_ptr[j + 1]; ++e) {
-        const int32_t b = blk_of_row[ctx->h_csc_row[e]];
-        if (b != prev) {
-          cur = fill[b]++;
-          rcol[cur] = (int32_t)j;
-          rlo[cur] = e;
-        }
-        rhi[cur] = e + 1;
-        prev = b;
-      }
-    }
-    rptr.resize(ns + 1);
-    rptr[0] = 0;
-    for (int64_t q = 0; q < ns; ++q) rptr[q + 1] = rptr[q] + (rhi[q] - rlo[q]);
-    rval.resize(rptr[ns]);
-    rrowv.resize(rptr[ns]);
-    for (int64_t b = 0; b < s; ++b)
-      for (int64_t q = roff[b]; q < roff[b + 1]; ++q)
-        for (int64_t e = rlo[q]; e < rhi[q]; ++e) {
-          const int64_t o = rptr[q] + (e - rlo[q]);
-          rval[o] = ctx->h_csc_val[e];
-          rrowv[o] = ctx->h_csc_row[e] - (int32_t)cfg->row_ptr[b];
-        }
-    rcta.resize(s * (G + 1));
-    for (int64_t b = 0; b < s; ++b)
-      for (int q = 0; q <= G; ++q) {
-        const int32_t c0 = split_rows(n, G, q);
-        rcta[b * (G + 1) + q] =
-            std::lower_bound(rcol.begin() + roff[b], rcol.begin() + roff[b + 1], c0) - rcol.begin();
-      }
-  };
-  {
-    std::thread col_thread(build_col_lists);
-    build_row_lists();
-    col_thread.join();
-  }
+  seg_lists(n, ctx->h_csc_ptr.data(), ctx->h_csc_row.data(), ctx->h_csc_val.data(), m, s, cfg->row_ptr, G, T, R);
+  const auto &coff = C.off, &cptr = C.ptr, &ccta = C.cta, &roff = R.off, &rptr = R.ptr, &rcta = R.cta;
+  const auto &crow = C.major_id, &ccolv = C.minor_local, &rcol = R.major_id, &rrowv = R.minor_local;
+  const auto &cval = C.val, &rval = R.val;
   cudaError_t e = cudaSuccess;
   if (!e) e = upload_vec(&sp->cseg_off, coff);
   if (!e) e = upload_vec(&sp->cseg_ptr, cptr);
