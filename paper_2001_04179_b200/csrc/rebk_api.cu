@@ -1311,21 +1311,38 @@ int rebk_ctx_create_csr(const int64_t* indptr, const int32_t* indices, const dou
   c->nnz = nnz;
   c->h_csr_ptr.assign(indptr, indptr + m + 1);
   c->h_csr_col.assign(indices, indices + nnz);
-  // CSC twin (counting sort by column: rows stay ascending within a column)
+  // CSC twin (counting sort by column: rows stay ascending within a column).
+  // T host threads own contiguous row ranges; per-(thread, column) counts give
+  // each thread its write offsets, so the twin equals a sequential sort.
+  const int T = (int)std::max<int64_t>(
+      1, std::min<int64_t>({16, (int64_t)std::thread::hardware_concurrency(), nnz / (8 * (n + 1)), m / 4096}));
+  auto lo_of = [&](int th) { return m * th / T; };
+  std::vector<int64_t> cnt((size_t)T * n, 0);
+  parallel_for_threads(T, [&](int th) {
+    int64_t* cc = cnt.data() + (size_t)th * n;
+    for (int64_t e = indptr[lo_of(th)]; e < indptr[lo_of(th + 1)]; ++e) cc[indices[e]]++;
+  });
   c->h_csc_ptr.assign(n + 1, 0);
-  for (int64_t e = 0; e < nnz; ++e) c->h_csc_ptr[indices[e] + 1]++;
-  for (int64_t j = 0; j < n; ++j) c->h_csc_ptr[j + 1] += c->h_csc_ptr[j];
+  for (int64_t j = 0; j < n; ++j) {
+    int64_t acc = c->h_csc_ptr[j];
+    for (int th = 0; th < T; ++th) {
+      const int64_t k = cnt[(size_t)th * n + j];
+      cnt[(size_t)th * n + j] = acc;
+      acc += k;
+    }
+    c->h_csc_ptr[j + 1] = acc;
+  }
   c->h_csc_row.resize(nnz);
   std::vector<double> csc_val(nnz);
-  {
-    std::vector<int64_t> fill(c->h_csc_ptr.begin(), c->h_csc_ptr.end() - 1);
-    for (int64_t i = 0; i < m; ++i)
+  parallel_for_threads(T, [&](int th) {
+    int64_t* fill = cnt.data() + (size_t)th * n;
+    for (int64_t i = lo_of(th); i < lo_of(th + 1); ++i)
       for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
         const int64_t q = fill[indices[e]]++;
         c->h_csc_row[q] = (int32_t)i;
         csc_val[q] = data[e];
       }
-  }
+  });
   c->h_csr_val.assign(data, data + nnz);
   c->h_csc_val = std::move(csc_val);
   cudaError_t e = upload_vec(&c->csr_ptr, c->h_csr_ptr);
