@@ -25,7 +25,15 @@
  *    (sampling.py:122-132, solvers.py:151/:164), so the device reproduces the
  *    reference block-index sequence bit for bit.
  *  - A rebk_ctx is immutable after creation ("Matrices are
- *    immutable"); concurrent rebk_run calls on one ctx are allowed.
+ *    immutable"); concurrent rebk_run / rebk_run_device / rebk_run_mrhs
+ *    calls on one ctx from different host threads are allowed (SPEC.md:390:
+ *    distinct runs may execute concurrently): every run owns its workspace
+ *    and stream, and the ctx's lazily built caches (sparse segment lists,
+ *    the fp32 transposed copy) are built under the ctx's mutex and published
+ *    only after their device copies completed.  Persistent kernels are
+ *    launched cooperatively only, so two runs sharing a GPU serialise
+ *    instead of deadlocking.  The rebk_shard_* pieces are the exception
+ *    (documented below).
  */
 #ifndef REBK_H
 #define REBK_H
@@ -36,7 +44,7 @@
 extern "C" {
 #endif
 
-#define REBK_ABI_VERSION 1
+#define REBK_ABI_VERSION 2
 
 /* error codes */
 #define REBK_OK 0
@@ -88,6 +96,12 @@ typedef struct rebk_cfg {
   int32_t record_errors;    /* SolverConfig.record_errors */
   int32_t grid_ctas;        /* 0 = automatic */
   double residual_scale;    /* sqrt(||A||_F^2) * ||b|| (solvers.py:411-413) */
+  /* NaN/Inf in a stopping reduction: 0 = keep iterating like the reference
+   * (run() has no finiteness check; the error stays NaN until max_iters,
+   * solvers.py:444-474) and report it in rebk_trace.nonfinite_at; 1 = stop
+   * at that check and return REBK_ENONFINITE (outputs hold that state). */
+  int32_t nonfinite_stop;
+  int32_t reserved0;
 } rebk_cfg;
 
 /* RunTrace (solvers.py:96-112). errors is caller-allocated (capacity
@@ -103,10 +117,14 @@ typedef struct rebk_trace {
   int64_t n_checks;
   int32_t grid_ctas;        /* CTAs the persistent kernel used */
   int32_t kernel_path;      /* 0 dense general, 1 dense clustered, 2 same (cooperative), 3 sparse, 4/5 multi-RHS (5: BF16x9 tensor cores), 6 dense split column/row groups, 7 dense streaming (blocks larger than shared memory), 8 multi-RHS on hand-written tcgen05 3xTF32 kernels */
+  int64_t nonfinite_at;     /* first check (iteration k) whose error was NaN/Inf; -1 if none */
 } rebk_trace;
 
 /* ---- library / device ---------------------------------------------------- */
 int rebk_abi_version(void);
+/* sizeof(rebk_cfg), sizeof(rebk_trace), sizeof(rebk_shard_run_args) as this
+ * library was compiled (bindings check their struct mirrors against it) */
+int rebk_abi_struct_sizes(int64_t* cfg_size, int64_t* trace_size, int64_t* shard_args_size);
 const char* rebk_last_error(void);
 int rebk_device_count(int* count);
 
@@ -203,6 +221,7 @@ typedef struct rebk_shard_run_args {
   double* x_dev;           /* device [n], in/out (replicated) */
   double* z_dev;           /* device [m_local], in/out */
   const double* xs_dev;    /* device [n] */
+  int64_t n_picks;         /* entries of picks (>= max_iters); every pick is range-checked */
 } rebk_shard_run_args;
 int rebk_nccl_get_unique_id(const char* libnccl_path, unsigned char id_out[128]);
 int rebk_nccl_comm_create(const char* libnccl_path, const unsigned char id[128], int nranks, int rank,

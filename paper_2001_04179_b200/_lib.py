@@ -17,6 +17,7 @@ import numpy as np
 LIB_PATH = os.environ.get("REBK_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "librebk.so")
 
 REBK_OK = 0
+ABI_VERSION = 2  # include/rebk.h REBK_ABI_VERSION (struct layouts below)
 ERRORS = {
     -1: "REBK_EINVAL",
     -2: "REBK_ECUDA",
@@ -52,6 +53,8 @@ class RebkCfg(ctypes.Structure):
         ("record_errors", c_int32),
         ("grid_ctas", c_int32),
         ("residual_scale", c_double),
+        ("nonfinite_stop", c_int32),
+        ("reserved0", c_int32),
     ]
 
 
@@ -75,6 +78,7 @@ class RebkShardRunArgs(ctypes.Structure):
         ("x_dev", c_void_p),
         ("z_dev", c_void_p),
         ("xs_dev", c_void_p),
+        ("n_picks", c_int64),
     ]
 
 
@@ -90,6 +94,7 @@ class RebkTrace(ctypes.Structure):
         ("n_checks", c_int64),
         ("grid_ctas", c_int32),
         ("kernel_path", c_int32),
+        ("nonfinite_at", c_int64),
     ]
 
 
@@ -98,6 +103,7 @@ _P_D = POINTER(c_double)
 _P_I64 = POINTER(c_int64)
 SIGNATURES = {
     "rebk_abi_version": (c_int, []),
+    "rebk_abi_struct_sizes": (c_int, [_P_I64, _P_I64, _P_I64]),
     "rebk_last_error": (c_char_p, []),
     "rebk_device_count": (c_int, [POINTER(c_int)]),
     "rebk_ctx_create_dense": (c_int, [_P_D, c_int64, c_int64, c_int64, c_int, POINTER(c_void_p)]),
@@ -138,6 +144,11 @@ class RebkError(RuntimeError):
     """A failure reported by librebk (CUDA error, missing device, ...)."""
 
 
+class NonFiniteError(RebkError):
+    """REBK_ENONFINITE: a stopping reduction met NaN/Inf and the run was
+    configured to stop there (rebk_cfg.nonfinite_stop)."""
+
+
 def load() -> ctypes.CDLL:
     """Load librebk.so once; raise loudly if it has not been built."""
     global _lib
@@ -153,6 +164,8 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.rebk_abi_version() != ABI_VERSION:
+        raise RebkError(f"{LIB_PATH} has ABI {lib.rebk_abi_version()}, this binding expects {ABI_VERSION}: rebuild it")
     _lib = lib
     return lib
 
@@ -161,6 +174,8 @@ def check(rc: int, what: str) -> None:
     if rc != REBK_OK:
         msg = load().rebk_last_error().decode(errors="replace")
         code = ERRORS.get(rc, str(rc))
+        if rc == -5:
+            raise NonFiniteError(f"{what}: {msg}")
         if rc == -1:
             raise ValueError(f"{what}: {msg}")
         raise RebkError(f"{what} failed ({code}): {msg}")

@@ -17,6 +17,8 @@
 #include <thread>
 #include <vector>
 
+#include <mutex>
+
 #include "../../include/rebk.h"
 #include "philox.h"
 #include "rebk_internal.h"
@@ -50,9 +52,10 @@ struct rebk_ctx {
   std::vector<int64_t> h_csr_ptr, h_csc_ptr;
   std::vector<int32_t> h_csr_col, h_csc_row;
   std::vector<double> h_csr_val, h_csc_val;
-  std::vector<CsrSegPlan*> seg_cache;
+  std::vector<CsrSegPlan*> seg_cache;  // guarded by mu
   float* A32 = nullptr;  // dense fp32 A (multi-RHS contexts, kind 2)
-  float* A32t = nullptr;  // its transpose (n x ldat), built at the first tensor-core run
+  float* A32t = nullptr;  // its transpose (n x ldat), built at the first tensor-core run (under mu)
+  std::mutex mu;  // lazily built caches: seg_cache, A32t (concurrent runs on one ctx)
   int64_t ldat = 0;
   double* shard_scratch = nullptr;  // rebk_shard_* partials (not reentrant per ctx)
   size_t shard_scratch_len = 0;
@@ -544,6 +547,9 @@ void seg_lists(int64_t nmajor, const int64_t* mptr, const int32_t* minor, const 
 // CSC arrays (sorted by column); plus each CTA's first segment.
 int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, CsrSegPlan** out) {
   const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
+  // one builder at a time; a plan is published (push_back) only after its
+  // synchronous uploads completed, and plans are never freed before the ctx
+  std::lock_guard<std::mutex> lock(ctx->mu);
   for (CsrSegPlan* c : ctx->seg_cache) {
     if (c->G == G && same_vec(c->row_ptr, cfg->row_ptr, s + 1) &&
         (!extended || same_vec(c->col_ptr, cfg->col_ptr, t + 1))) {
@@ -706,6 +712,7 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
   p.max_iters = cfg->max_iters;
   p.res_scale = cfg->residual_scale > 0.0 ? cfg->residual_scale : 1.0;
   p.record = errs_cap > 0;
+  p.nonfinite_stop = cfg->nonfinite_stop;
   p.prof = d_prof;
 
   cudaEvent_t ev0, ev1;
@@ -758,7 +765,10 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
     trace->n_checks = ctl.n_checks;
     trace->grid_ctas = G;
     trace->kernel_path = 3;
+    trace->nonfinite_at = ctl.nonfinite_at - 1;
   }
+  if (ctl.nonfinite_at && cfg->nonfinite_stop)
+    return fail(REBK_ENONFINITE, "non-finite error at the check of iteration %lld", (long long)(ctl.nonfinite_at - 1));
   return REBK_OK;
 }
 
@@ -781,8 +791,12 @@ struct HostMarks {
   }
 };
 
-int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev,
-                    double* x_dev, double* z_dev, cudaStream_t stream, rebk_trace* trace) {
+// internal: the clustered kernels could not run (cooperative cluster launch
+// refused, or launched without their clusters); nothing was written yet
+constexpr int kRetryGeneral = 100;
+
+int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev,
+                         double* x_dev, double* z_dev, cudaStream_t stream, rebk_trace* trace, bool force_general) {
   const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
   if (cfg->algorithm < 0 || cfg->algorithm > 3) return fail(REBK_EINVAL, "unknown algorithm %d", cfg->algorithm);
   if (cfg->stop_mode < 0 || cfg->stop_mode > 2) return fail(REBK_EINVAL, "unknown stopping mode %d", cfg->stop_mode);
@@ -820,15 +834,14 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   // partitions and stopping mode, so repeated runs take the same path.
   FastGeometry fg;
   bool use_fast = false;
-  bool fast_coop = true;
   CUtensorMap tm_ct, tm_rt;
   {
-    const int CS = env_int("REBK_CLUSTER", 8);
+    const int CS = kClusterCS;  // the clustered kernels' compile-time cluster shape
     const bool aligned = (ctx->lda % 2 == 0) && ((uintptr_t)ctx->A % 16 == 0);
     // TMA boxes start on 16-byte aligned columns: the clustered kernels need
     // even column-block starts (the streaming kernel handles odd ones)
     const bool even_cols = !extended || blocks_even(cfg->n_col_blocks, cfg->col_ptr);
-    if (env_int("REBK_NO_FAST", 0) == 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY && aligned && even_cols && CS >= 1 &&
+    if (!force_general && env_int("REBK_NO_FAST", 0) == 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY && aligned && even_cols && CS >= 1 &&
         G0 >= CS && encode_fn() != nullptr) {
       int NC = std::max(1, G0 / CS);
       for (int attempt = 0; attempt < 3 && NC >= 1; ++attempt) {
@@ -1018,6 +1031,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   p.max_iters = cfg->max_iters;
   p.res_scale = cfg->residual_scale > 0.0 ? cfg->residual_scale : 1.0;
   p.record = errs_cap > 0;
+  p.nonfinite_stop = cfg->nonfinite_stop;
   p.nJ_max = geo.nJ_max;
   p.nI_max = geo.nI_max;
   p.nR_max = geo.nR_max;
@@ -1086,22 +1100,10 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
         spar.trace = d_trace;
         spar.trace_k0 = trace_k0;
         spar.trace_n = trace_n;
-        err = launch_dense_split(spar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
-        if (err != cudaSuccess && fast_coop) {
-          cudaGetLastError();
-          fast_coop = false;
-          err = launch_dense_split(spar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
-        }
+        err = launch_dense_split(spar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream);
       } else if (use_fast) {
         fpar.d = p;
-        err = launch_dense_fast(fpar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
-        if (err != cudaSuccess && fast_coop) {
-          // cooperative + cluster launch refused: the grid is sized to the
-          // co-resident cluster capacity, launch it as a plain cluster grid
-          cudaGetLastError();
-          fast_coop = false;
-          err = launch_dense_fast(fpar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream, fast_coop);
-        }
+        err = launch_dense_fast(fpar, tm_ct, tm_rt, G, fg.CS, fg.smem_bytes, stream);
       } else if (use_stream) {
         StreamParams spar{};
         spar.d = p;
@@ -1120,6 +1122,15 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
         err = launch_dense_stream(spar, tm_sc, tm_sr, G, stg.smem_bytes, stream);
       } else {
         err = launch_dense(p, G, geo.smem_bytes, stream);
+      }
+      // the spin-barrier kernels only ever run as cooperative launches (all
+      // CTAs co-resident); if the cooperative cluster launch is refused, the
+      // run goes to the general kernel instead of a grid that could hang
+      if (err != cudaSuccess && (use_fast || use_split) && k == 1) {
+        cudaGetLastError();
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        return kRetryGeneral;
       }
     }
     k += std::max<int64_t>(count, 1);
@@ -1145,7 +1156,10 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   cudaEventDestroy(ev1);
   if (err != cudaSuccess) return fail(REBK_ECUDA, "REBK run failed: %s", cudaGetErrorString(err));
   hm.mark("sync + control readback");
-  if (ctl.fault) return fail(REBK_ECUDA, "clustered kernel launched without its %d-CTA clusters", fg.CS);
+  // launched without its clusters (e.g. replayed by a profiler that drops
+  // the cluster shape): every CTA refused before touching x / z, so the run
+  // is repeated on the general kernel
+  if (ctl.fault) return kRetryGeneral;
   if (d_trace) {
     std::vector<unsigned long long> h((size_t)trace_n * G * 8);
     cudaMemcpy(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost);
@@ -1165,7 +1179,7 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx->device);
     const double it = (double)std::max<int64_t>(1, ctl.iters);
     fprintf(stderr, "[rebk prof] path=%s ncc=%d ",
-            use_split ? "split" : (use_fast ? (fast_coop ? "fast(coop)" : "fast") : (use_stream ? "stream" : "v1")),
+            use_split ? "split" : (use_fast ? "fast(coop)" : (use_stream ? "stream" : "v1")),
             split_ncc);
     fprintf(stderr, "[rebk prof] G=%d iters=%lld loop=%.3f ms (%.3f us/iter); per-iteration us: mark mean max\n", G,
             (long long)ctl.iters, ms, 1e3 * ms / it);
@@ -1179,9 +1193,20 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
     trace->loop_ms = ms;
     trace->n_checks = ctl.n_checks;
     trace->grid_ctas = G;
-    trace->kernel_path = use_split ? 6 : (use_fast ? (fast_coop ? 2 : 1) : (use_stream ? 7 : 0));
+    trace->kernel_path = use_split ? 6 : (use_fast ? 2 : (use_stream ? 7 : 0));
+    trace->nonfinite_at = ctl.nonfinite_at - 1;
   }
+  if (ctl.nonfinite_at && cfg->nonfinite_stop)
+    return fail(REBK_ENONFINITE, "non-finite error at the check of iteration %lld", (long long)(ctl.nonfinite_at - 1));
   return REBK_OK;
+}
+
+int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev,
+                    double* x_dev, double* z_dev, cudaStream_t stream, rebk_trace* trace) {
+  int rc = run_device_impl_once(ctx, cfg, b_dev, xs_dev, x_dev, z_dev, stream, trace, false);
+  if (rc == kRetryGeneral) rc = run_device_impl_once(ctx, cfg, b_dev, xs_dev, x_dev, z_dev, stream, trace, true);
+  if (rc == kRetryGeneral) rc = fail(REBK_ECUDA, "the general kernel refused its launch");
+  return rc;
 }
 
 }  // namespace
@@ -1202,6 +1227,13 @@ bool ctx_dense_view(const rebk_ctx* ctx, const double** A, int64_t* m, int64_t* 
 extern "C" {
 
 int rebk_abi_version(void) { return REBK_ABI_VERSION; }
+
+int rebk_abi_struct_sizes(int64_t* cfg_size, int64_t* trace_size, int64_t* shard_args_size) {
+  if (cfg_size) *cfg_size = (int64_t)sizeof(rebk_cfg);
+  if (trace_size) *trace_size = (int64_t)sizeof(rebk_trace);
+  if (shard_args_size) *shard_args_size = (int64_t)sizeof(rebk_shard_run_args);
+  return REBK_OK;
+}
 
 const char* rebk_last_error(void) { return g_last_error.c_str(); }
 
@@ -1463,20 +1495,31 @@ int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float*
       // the tensor-core path reads column blocks as rows of Aᵀ (kind::tf32
       // operands must be K-major): one transposed copy per context
       const char* mm = getenv("REBK_MRHS_MATH");
-      if (!ctx->A32t && (!mm || !strcmp(mm, "tc")) && m % 4 == 0 && n % 4 == 0) {
-        const int64_t ldat = m;
-        if (cudaMalloc(&ctx->A32t, sizeof(float) * n * ldat) == cudaSuccess) {
-          ctx->ldat = ldat;
-          if (mrhs_transpose_a(ctx->A32, m, n, ctx->lda, ctx->A32t, ldat, stream) != cudaSuccess) {
-            cudaFree(ctx->A32t);
-            ctx->A32t = nullptr;
+      float* a32t = nullptr;
+      int64_t ldat = 0;
+      if ((!mm || !strcmp(mm, "tc")) && m % 4 == 0 && n % 4 == 0) {
+        // built once per ctx under its mutex; published only after the
+        // transpose finished, so a concurrent run never reads a partial copy
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        if (!ctx->A32t) {
+          float* t32 = nullptr;
+          if (cudaMalloc(&t32, sizeof(float) * n * m) == cudaSuccess) {
+            if (mrhs_transpose_a(ctx->A32, m, n, ctx->lda, t32, m, stream) == cudaSuccess &&
+                cudaStreamSynchronize(stream) == cudaSuccess) {
+              ctx->ldat = m;
+              ctx->A32t = t32;
+            } else {
+              cudaGetLastError();
+              cudaFree(t32);
+            }
+          } else {
+            cudaGetLastError();
           }
-        } else {
-          cudaGetLastError();
-          ctx->A32t = nullptr;
         }
+        a32t = ctx->A32t;
+        ldat = ctx->ldat;
       }
-      MrhsRun w{ctx->A32, m, n, ctx->lda, ctx->A32t, ctx->ldat, (int)R, dB, dX, dZ, dXs, cfg, tols, extended};
+      MrhsRun w{ctx->A32, m, n, ctx->lda, a32t, ldat, (int)R, dB, dX, dZ, dXs, cfg, tols, extended};
       double ms = 0.0;
       int64_t K = 0;
       int math = 0;
@@ -1645,7 +1688,7 @@ int rebk_run(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b, const double* 
     } else {
       rc = run_device_impl(ctx, cfg, d_b, d_xs, d_x, d_z, stream, trace);
     }
-    if (rc == REBK_OK) {
+    if (rc == REBK_OK || rc == REBK_ENONFINITE) {  // ENONFINITE: outputs hold the state of that check
       e = cudaMemcpyAsync(x_out, d_x, n * 8, cudaMemcpyDeviceToHost, stream);
       if (e == cudaSuccess && z_out && extended)
         e = cudaMemcpyAsync(z_out, d_z, m * 8, cudaMemcpyDeviceToHost, stream);

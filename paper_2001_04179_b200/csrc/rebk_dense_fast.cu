@@ -33,7 +33,7 @@ namespace cg = cooperative_groups;
 namespace rebk {
 
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1) __cluster_dims__(kClusterCS, 1, 1)
     rebk_dense_fast_kernel(const __grid_constant__ FastParams fp, const __grid_constant__ CUtensorMap tm_ct,
                            const __grid_constant__ CUtensorMap tm_rt) {
   extern __shared__ __align__(128) double sm[];
@@ -164,19 +164,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   auto decide = [&](double sumsq, int64_t k) -> bool {
     const double err = sqrt(sumsq);
-    const bool conv = err <= p.tol;
-    if (g == 0 && tid == 0) {
-      const int64_t nc = ctl->n_checks;
-      if (p.record && nc < p.errs_cap) p.errs[nc] = err;
-      ctl->n_checks = nc + 1;
-      ctl->final_error = err;
-      ctl->has_error = 1;
-      if (conv) {
-        ctl->converged = 1;
-        ctl->iters = k;
-        ctl->done = 1;
-      }
-    }
+    const bool conv = check_stops(err, p.tol, p.nonfinite_stop);
+    if (g == 0 && tid == 0) record_check(ctl, p.errs, p.errs_cap, p.record, err, p.tol, p.nonfinite_stop, k);
     return conv;
   };
   // a stand-alone error exchange (check(0), end-of-chunk, off-stride final check)
@@ -400,7 +389,7 @@ cudaError_t fast_max_clusters(int cluster_size, size_t smem_bytes, int* clusters
 }
 
 cudaError_t launch_dense_fast(const FastParams& fp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
-                              int cluster_size, size_t smem_bytes, cudaStream_t stream, bool cooperative) {
+                              int cluster_size, size_t smem_bytes, cudaStream_t stream) {
   cudaError_t e = set_fast_attrs();
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -408,15 +397,12 @@ cudaError_t launch_dense_fast(const FastParams& fp, const CUtensorMap& tm_ct, co
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster_size;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeCooperative;
-  attr[1].val.cooperative = 1;
+  if (cluster_size != kClusterCS) return cudaErrorInvalidValue;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = cooperative ? 2 : 1;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, rebk_dense_fast_kernel, fp, tm_ct, tm_rt);
 }
 

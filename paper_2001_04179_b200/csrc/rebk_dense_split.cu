@@ -37,13 +37,9 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// REBK_STATIC_CLUSTER (profiling builds, tools/build_variants.sh): the cluster
-// shape is a kernel attribute instead of a launch attribute; ncu replays the
-// kernel with its clusters only in this form
-__global__ void __launch_bounds__(kSplitThreads, 1)
-#ifdef REBK_STATIC_CLUSTER
-    __cluster_dims__(REBK_STATIC_CLUSTER, 1, 1)
-#endif
+// The cluster shape is a kernel attribute (not a launch attribute), so the
+// kernel always runs with its clusters, also when a profiler replays it
+__global__ void __launch_bounds__(kSplitThreads, 1) __cluster_dims__(kClusterCS, 1, 1)
     rebk_dense_split_kernel(const __grid_constant__ SplitParams spp, const __grid_constant__ CUtensorMap tm_ct,
                             const __grid_constant__ CUtensorMap tm_rt) {
   extern __shared__ __align__(128) double sm[];
@@ -393,19 +389,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
     const bool leader = (gg == 0 && tid == 0);
     auto decide = [&](double sumsq, int64_t k) -> bool {
       const double err = sqrt(sumsq);
-      const bool conv = err <= p.tol;
+      const bool conv = check_stops(err, p.tol, p.nonfinite_stop);
       if (leader) {
-        const int64_t nc = ctl->n_checks;
-        if (p.record && nc < p.errs_cap) p.errs[nc] = err;
-        ctl->n_checks = nc + 1;
-        ctl->final_error = err;
-        ctl->has_error = 1;
-        if (conv) {
-          ctl->converged = 1;
-          ctl->iters = k;
-          ctl->done = 1;
-          st_release_u64(&sh->stop, (unsigned long long)k + 1);
-        }
+        record_check(ctl, p.errs, p.errs_cap, p.record, err, p.tol, p.nonfinite_stop, k);
+        if (conv) st_release_u64(&sh->stop, (unsigned long long)k + 1);
       }
       return conv;
     };
@@ -543,7 +530,7 @@ static cudaError_t set_split_attrs() {
 }
 
 cudaError_t launch_dense_split(const SplitParams& sp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
-                               int cluster_size, size_t smem_bytes, cudaStream_t stream, bool cooperative) {
+                               int cluster_size, size_t smem_bytes, cudaStream_t stream) {
   cudaError_t e = set_split_attrs();
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -551,20 +538,12 @@ cudaError_t launch_dense_split(const SplitParams& sp, const CUtensorMap& tm_ct, 
   cfg.blockDim = dim3(kSplitThreads);
   cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster_size;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeCooperative;
-  attr[1].val.cooperative = 1;
+  if (cluster_size != kClusterCS) return cudaErrorInvalidValue;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = cooperative ? 2 : 1;
-#ifdef REBK_STATIC_CLUSTER
-  if (cluster_size != REBK_STATIC_CLUSTER) return cudaErrorInvalidValue;
-  cfg.attrs = attr + 1;
-  cfg.numAttrs = cooperative ? 1 : 0;
-#endif
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, rebk_dense_split_kernel, sp, tm_ct, tm_rt);
 }
 

@@ -169,19 +169,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
     }
     __syncthreads();
     const double err = sqrt(s_bcast[0]);
-    const bool conv = err <= p.tol;
-    if (g == 0 && tid == 0) {
-      const int64_t nc = ctl->n_checks;
-      if (p.record && nc < p.errs_cap) p.errs[nc] = err;
-      ctl->n_checks = nc + 1;
-      ctl->final_error = err;
-      ctl->has_error = 1;
-      if (conv) {
-        ctl->converged = 1;
-        ctl->iters = k;
-        ctl->done = 1;
-      }
-    }
+    const bool conv = check_stops(err, p.tol, p.nonfinite_stop);
+    if (g == 0 && tid == 0) record_check(ctl, p.errs, p.errs_cap, p.record, err, p.tol, p.nonfinite_stop, k);
     __syncthreads();
     return conv;
   };

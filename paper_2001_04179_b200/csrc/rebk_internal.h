@@ -9,6 +9,9 @@ struct rebk_ctx;
 namespace rebk {
 
 constexpr int kThreads = 256;
+// cluster shape of the clustered dense kernels (rebk_dense_fast.cu,
+// rebk_dense_split.cu), fixed at compile time with __cluster_dims__
+constexpr int kClusterCS = 8;
 constexpr int kWarps = kThreads / 32;
 // dynamic shared memory we are willing to ask for (227 KB max per CTA on B200)
 constexpr int kSmemBudget = 218 * 1024;
@@ -35,6 +38,7 @@ struct Control {
   int32_t fault;  // launch-shape mismatch detected on the device
   unsigned long long xseq;  // exchanges completed (fast path), carried across chunk launches
   unsigned long long xseq_row;  // split path: row-group exchanges
+  int64_t nonfinite_at;  // 1 + first iteration whose stopping reduction was NaN/Inf (0: none)
 };
 
 // Split path: column-sweep group feeding the row-sweep group (rebk_dense_split.cu)
@@ -77,6 +81,7 @@ struct DenseParams {
   int64_t max_iters;
   double res_scale;
   int32_t record;
+  int32_t nonfinite_stop;  // stop the run at a NaN/Inf error (rebk_cfg.nonfinite_stop)
   // tile geometry (host-computed)
   int32_t nJ_max, nI_max;  // largest column / row block
   int32_t nR_max, nC_max;  // largest owned z-row / x-column slice
@@ -171,9 +176,32 @@ struct CsrParams {
   int64_t max_iters;
   double res_scale;
   int32_t record;
-  int32_t pad;
+  int32_t nonfinite_stop;
   long long* prof;  // optional per-CTA phase cycle counters [G][16] (REBK_PROF=1)
 };
+
+// One stopping check's bookkeeping, done by a single leader thread: the
+// recorded error list, RunTrace.final_error (solvers.py:444-474) and the
+// NaN/Inf detection.  Returns whether the run stops here; every CTA evaluates
+// check_stops() on the same err, so they all agree without communication.
+__host__ __device__ inline bool check_stops(double err, double tol, int32_t nonfinite_stop) {
+  const bool bad = !(err - err == 0.0);  // NaN or +-Inf
+  return err <= tol || (bad && nonfinite_stop);
+}
+__device__ inline void record_check(Control* ctl, double* errs, int64_t errs_cap, int32_t record, double err,
+                                    double tol, int32_t nonfinite_stop, int64_t k) {
+  const int64_t nc = ctl->n_checks;
+  if (record && nc < errs_cap) errs[nc] = err;
+  ctl->n_checks = nc + 1;
+  ctl->final_error = err;
+  ctl->has_error = 1;
+  if (!(err - err == 0.0) && ctl->nonfinite_at == 0) ctl->nonfinite_at = k + 1;
+  if (check_stops(err, tol, nonfinite_stop)) {
+    ctl->converged = err <= tol;
+    ctl->iters = k;
+    ctl->done = 1;
+  }
+}
 
 struct SampleParams {
   uint64_t key0, key1;
@@ -209,11 +237,11 @@ cudaError_t launch_sample_plan(const SampleParams& sp, int64_t k0, int64_t count
 cudaError_t launch_dense(const DenseParams& p, int G, size_t smem_bytes, cudaStream_t stream);
 cudaError_t dense_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
 cudaError_t launch_dense_fast(const FastParams& fp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
-                              int cluster_size, size_t smem_bytes, cudaStream_t stream, bool cooperative);
+                              int cluster_size, size_t smem_bytes, cudaStream_t stream);
 cudaError_t fast_max_clusters(int cluster_size, size_t smem_bytes, int* clusters);
 cudaError_t split_max_clusters(int cluster_size, size_t smem_bytes, int* clusters);
 cudaError_t launch_dense_split(const SplitParams& sp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
-                               int cluster_size, size_t smem_bytes, cudaStream_t stream, bool cooperative);
+                               int cluster_size, size_t smem_bytes, cudaStream_t stream);
 cudaError_t launch_dense_stream(const StreamParams& sp, const CUtensorMap& tm_c, const CUtensorMap& tm_r, int G,
                                 size_t smem_bytes, cudaStream_t stream);
 cudaError_t stream_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);

@@ -12,6 +12,7 @@
 // host reads a chunk of errors at once, and when a check inside the chunk
 // crosses tol the chunk is replayed from its start snapshot to exactly that
 // iteration (kernels and fixed-size allreduces are deterministic).
+#include <stdarg.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdio.h>
@@ -88,8 +89,11 @@ using namespace rebk;
 
 namespace {
 thread_local char g_nccl_err[512];
-int nfail(int code, const char* msg) {
-  snprintf(g_nccl_err, sizeof g_nccl_err, "%s", msg);
+int nfail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_nccl_err, sizeof g_nccl_err, fmt, ap);
+  va_end(ap);
   return set_error_msg(code, g_nccl_err);
 }
 }  // namespace
@@ -97,7 +101,7 @@ int nfail(int code, const char* msg) {
 extern "C" int rebk_nccl_get_unique_id(const char* libnccl_path, unsigned char id_out[128]) {
   char err[400];
   if (!id_out) return nfail(REBK_EINVAL, "rebk_nccl_get_unique_id: null output");
-  if (!nccl::load(libnccl_path, err, sizeof err)) return nfail(REBK_EINVAL, err);
+  if (!nccl::load(libnccl_path, err, sizeof err)) return nfail(REBK_EINVAL, "%s", err);
   nccl::ncclUniqueId id;
   const int r = nccl::g_api.get_unique_id(&id);
   if (r != 0) return nfail(REBK_ECUDA, nccl::g_api.err_str(r));
@@ -109,7 +113,7 @@ extern "C" int rebk_nccl_comm_create(const char* libnccl_path, const unsigned ch
                                      int device, void** comm_out) {
   char err[400];
   if (!id || !comm_out || nranks < 1 || rank < 0 || rank >= nranks) return nfail(REBK_EINVAL, "rebk_nccl_comm_create: bad argument");
-  if (!nccl::load(libnccl_path, err, sizeof err)) return nfail(REBK_EINVAL, err);
+  if (!nccl::load(libnccl_path, err, sizeof err)) return nfail(REBK_EINVAL, "%s", err);
   if (cudaSetDevice(device) != cudaSuccess) return nfail(REBK_ENODEV, "rebk_nccl_comm_create: no such device");
   nccl::ncclUniqueId uid;
   memcpy(uid.internal, id, 128);
@@ -134,6 +138,13 @@ extern "C" int rebk_shard_run(rebk_ctx* ctx, void* comm, const rebk_shard_run_ar
       !a->b_dev || !a->x_dev || !a->xs_dev || a->max_iters < 0 || a->stride < 1 || a->chunk < 1 ||
       (a->extended && (!a->col_ptr || !a->col_scale || !a->z_dev)))
     return nfail(REBK_EINVAL, "rebk_shard_run: bad argument");
+  if (a->n_picks < a->max_iters) return nfail(REBK_EINVAL, "rebk_shard_run: %lld picks for %lld iterations",
+                                              (long long)a->n_picks, (long long)a->max_iters);
+  for (int64_t k = 0; k < a->max_iters; ++k) {
+    const int32_t jb = a->picks[2 * k], ib = a->picks[2 * k + 1];
+    if (ib < 0 || ib >= a->n_row_blocks || (a->extended && (jb < 0 || jb >= a->n_col_blocks)))
+      return nfail(REBK_EINVAL, "rebk_shard_run: pick %lld = (%d, %d) out of range", (long long)k, jb, ib);
+  }
   nccl::Comm* cm = (nccl::Comm*)comm;
   const double* A = nullptr;
   int64_t m = 0, n = 0, lda = 0;
@@ -167,6 +178,24 @@ extern "C" int rebk_shard_run(rebk_ctx* ctx, void* comm, const rebk_shard_run_ar
   std::vector<double> herr(chunk);
   int rc = REBK_OK;
   const bool have_rows = m > 0;
+  // every rank agrees that setup succeeded before anyone enters a collective
+  // of the iteration loop (a rank that failed alone would leave its peers
+  // blocked in ncclAllReduce): allreduce one failure flag
+  {
+    double* flag = nullptr;
+    const double mine = e == cudaSuccess ? 0.0 : 1.0;
+    double any = 1.0;
+    cudaGetLastError();
+    cudaError_t fe = cudaMallocAsync((void**)&flag, sizeof(double), st);
+    if (fe == cudaSuccess) fe = cudaMemcpyAsync(flag, &mine, sizeof(double), cudaMemcpyHostToDevice, st);
+    if (fe == cudaSuccess &&
+        nccl::g_api.all_reduce(flag, flag, 1, nccl::kFloat64, nccl::kSum, cm->comm, st) != 0)
+      fe = cudaErrorUnknown;
+    if (fe == cudaSuccess) fe = cudaMemcpyAsync(&any, flag, sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (fe == cudaSuccess) fe = cudaStreamSynchronize(st);
+    if (flag) cudaFreeAsync(flag, st);
+    if (e == cudaSuccess && (fe != cudaSuccess || any != 0.0)) e = fe != cudaSuccess ? fe : cudaErrorMemoryAllocation;
+  }
 
   auto iterate = [&](int64_t k) -> cudaError_t {
     const int jb = a->picks[2 * (k - 1)], ib = a->picks[2 * (k - 1) + 1];

@@ -16,6 +16,8 @@ run stops when every column has crossed.
 from __future__ import annotations
 
 import ctypes
+import os
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -111,6 +113,12 @@ def run_multi(a32: np.ndarray, B: np.ndarray, config: SolverConfig, X_star: np.n
     rc = _lib.load().rebk_run_mrhs(dm.handle, ctypes.byref(cfg), R, p(B), p(X0), p(Z0), p(Xs), _lib.dptr(tol_arr),
                                    p(X), p(Z), _lib.i64ptr(iters), _lib.dptr(errs), ctypes.byref(tr))
     _lib.check(rc, "rebk_run_mrhs")
+    if int(tr.kernel_path) in (4, 5) and os.environ.get("REBK_MRHS_MATH", "tc") == "tc":
+        # not silent: the shape is outside the hand-written tcgen05 kernel's
+        # range (m, n divisible by 4, blocks <= 256 wide, <= 64 RHS) and the
+        # library ran its cuBLAS SGEMM path instead (trace.kernel_path 4)
+        warnings.warn(f"multi-RHS shape {m}x{n} with {R} RHS is outside the tcgen05 kernel's range; ran the cuBLAS "
+                      f"SGEMM path ({KERNEL_PATHS[int(tr.kernel_path)]})", RuntimeWarning, stacklevel=2)
     return MultiRhsTrace(iters=int(tr.iters), iters_per_rhs=iters, converged=bool(tr.converged),
                          wall_time=float(tr.loop_ms) / 1e3, errors_at_iters=errs, X=X, Z=Z,
                          kernel_path=int(tr.kernel_path))

@@ -372,6 +372,7 @@ def run_sharded_native(backend: CudaShardBackend, comm: NcclComm, plan: ShardPla
     args.max_iters, args.stride, args.tol, args.chunk = int(max_iters), int(stride), float(tol), int(chunk)
     args.extended = 1 if backend.extended else 0
     args.picks = picks.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    args.n_picks = picks.shape[0]
     if backend.extended:
         col_ptr = np.ascontiguousarray(plan.col_ptr, dtype=np.int64)
         col_scale = np.ascontiguousarray(plan.col_scale, dtype=np.float64)

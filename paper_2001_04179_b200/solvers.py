@@ -190,7 +190,19 @@ class SolverContext:
 
         row_p = self._resolve_partition(config.row_partition, "row", self.a.rows)
         self.row_partition = row_p
-        self._prefetch_device(row_p, config.col_partition if (algo in _NEEDS_COL_PARTITION or algo == "rek") else None)
+        # start the H2D copy of A only once the run is known to go to the
+        # device and the column partition has validated (a run that will
+        # raise must not leave a copy of A behind); the validation is
+        # repeated below in the reference's order, so error texts and
+        # their precedence are unchanged
+        needs_col = algo in _NEEDS_COL_PARTITION or algo == "rek"
+        if algo in DEVICE_ALGORITHMS:
+            try:
+                early_col = self._resolve_partition(config.col_partition, "col", self.a.cols) if needs_col else None
+            except ValueError:
+                pass
+            else:
+                self._prefetch_device(row_p, early_col)
         self.row_sampler = build_sampler(self.a, row_p)
         self.row_scales = [float(self.alpha / w) for w in self.row_sampler.weights]
         self.row_selectors = [slice(i.start, i.stop) if isinstance(i, range) else i for i in row_p.blocks]

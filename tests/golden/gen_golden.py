@@ -342,7 +342,77 @@ def c2():
     big_case("c2_golden", a, b, xs, 200, 200, beta, ks=(1, 10, 100, 1000))
 
 
+C5_PIN_COLS = (0, 1, 63)
+
+
+def c5_full():
+    """BASELINE config 5 at its stated size: fp32 A = randn(50000, 5000), 64
+    right-hand sides, row/column blocks of 256 (ragged last blocks of 80 rows
+    and 136 columns).  The reference solves one fp64 right-hand side per run
+    (solvers.py:141-143), so the oracle is 64 kaczmarz.run() calls on the fp64
+    upcast of the stored fp32 data: every column's ITER at its 1e-4 relative
+    tolerance, then max_iters_only runs to the common final iteration
+    K = max ITER for the pinned columns (0, 1, 63), whose b, x* and x_K are
+    stored (the rest of the instance is rebuilt by workloads.c5_arrays)."""
+    from paper_2001_04179_b200 import Matrix as M2, contiguous_partition as cpart
+    from paper_2001_04179_b200.solvers import compute_beta_max as gram_beta
+
+    t0 = time.time()
+    a32, b32, xs = workloads.c5_arrays()
+    m, n = a32.shape
+    a = K.Matrix.from_dense(a32.astype(np.float64))
+    rp, cp = K.contiguous_partition(m, 256, "row"), K.contiguous_partition(n, 256, "col")
+    # beta by the block Gram eigenvalues (the same quantity as the reference's
+    # Jacobi-SVD rule; only alpha = 1/beta enters the runs and it is stored)
+    beta = gram_beta(M2.from_dense(a32.astype(np.float64)), cpart(m, 256, "row"), cpart(n, 256, "col"))[2]
+    alpha = 1.0 / beta
+    tols = 1e-4 * np.linalg.norm(xs, axis=0)
+    print(f"c5 built ({time.time() - t0:.1f}s) beta={beta}", flush=True)
+    iters, errs, walls = [], [], []
+    for c in range(b32.shape[1]):
+        prob = K.ProblemInstance(a=a, b=b32[:, c].astype(np.float64), x_star=xs[:, c], b_perp=None,
+                                 meta=K.ProblemMeta(0, None, False, 0, 0.0))
+        tr = K.run(prob, K.SolverConfig(algorithm="rebk", alpha=alpha, seed=17, row_partition=rp, col_partition=cp,
+                                        max_iters=50_000, stop=K.StoppingRule(tol=float(tols[c])), beta_max=beta))
+        iters.append(tr.iters)
+        errs.append(tr.final_error)
+        walls.append(tr.wall_time)
+        print(f"c5 column {c}: ITER={tr.iters} conv={tr.converged} wall={tr.wall_time:.1f}s", flush=True)
+    kmax = max(iters)
+    xk = []
+    for c in C5_PIN_COLS:
+        prob = K.ProblemInstance(a=a, b=b32[:, c].astype(np.float64), x_star=xs[:, c], b_perp=None,
+                                 meta=K.ProblemMeta(0, None, False, 0, 0.0))
+        ctx, xsn, _ = snapshots(prob, K.SolverConfig(algorithm="rebk", alpha=alpha, seed=17, row_partition=rp,
+                                                     col_partition=cp, max_iters=kmax, beta_max=beta,
+                                                     stop=K.StoppingRule(mode="max_iters_only")), (kmax,))
+        xk.append(xsn[kmax])
+    cols = np.asarray(C5_PIN_COLS)
+    print(f"c5: ITER per RHS {min(iters)}..{max(iters)} (K={kmax}) ({time.time() - t0:.1f}s)", flush=True)
+    np.savez_compressed(os.path.join(HERE, "c5_golden.npz"), alpha=alpha, beta=beta, seed=17, tols=tols,
+                        iters=np.asarray(iters), errors=np.asarray(errs), ref_wall=np.asarray(walls), K=kmax,
+                        cols=cols, b_cols=b32[:, cols], x_star_cols=xs[:, cols], x_K=np.stack(xk, axis=1))
+
+
+def c2_beta_reference():
+    """C2's beta_max by the reference's own rule (rates.compute_beta_max:
+    one-sided Jacobi SVD of every materialised block; ~30 min here), so the
+    device beta is pinned to the reference, not to this repo's host code."""
+    a, _, _ = workloads.c2_arrays()
+    rp, cp = K.contiguous_partition(4000, 200, "row"), K.contiguous_partition(10000, 200, "col")
+    t0 = time.time()
+    br, bc, bmax = compute_beta_max(K.Matrix.from_dense(a), rp, cp)
+    print(f"c2 reference beta: rows {br} cols {bc} max {bmax} ({time.time() - t0:.0f}s)", flush=True)
+    np.savez(os.path.join(HERE, "c2_beta_ref.npz"), beta_rows=br, beta_cols=bc, beta=bmax, seconds=time.time() - t0)
+
+
 if __name__ == "__main__":
+    if "--c5-full" in sys.argv:
+        c5_full()
+        sys.exit(0)
+    if "--c2-beta" in sys.argv:
+        c2_beta_reference()
+        sys.exit(0)
     philox_fixture()
     small_cases()
     sparse_cases()

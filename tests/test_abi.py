@@ -30,13 +30,18 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert _lib.load().rebk_abi_version() == 1
+    assert _lib.load().rebk_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_struct_layout_matches_header():
-    # rebk_cfg / rebk_trace field order and sizes are what the C side reads
-    assert ctypes.sizeof(_lib.RebkCfg) == 4 + 4 + 8 + 8 + 8 + 16 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 4 + 4 + 8
-    assert ctypes.sizeof(_lib.RebkTrace) == 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8 + 4 + 4
+    # rebk_cfg / rebk_trace / rebk_shard_run_args: the ctypes mirrors have the
+    # sizes the compiled C side uses
+    sizes = [ctypes.c_int64() for _ in range(3)]
+    assert _lib.load().rebk_abi_struct_sizes(*[ctypes.byref(s) for s in sizes]) == 0
+    assert [s.value for s in sizes] == [ctypes.sizeof(_lib.RebkCfg), ctypes.sizeof(_lib.RebkTrace),
+                                        ctypes.sizeof(_lib.RebkShardRunArgs)]
+    assert ctypes.sizeof(_lib.RebkCfg) == 4 + 4 + 8 + 8 + 8 + 16 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 4 + 4 + 8 + 4 + 4
+    assert ctypes.sizeof(_lib.RebkTrace) == 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8 + 4 + 4 + 8
 
 
 @pytest.mark.parametrize("seed,spawn", [(0, ()), (17, ()), (2024, ()), (2**64 + 3, ()), (4, (0,)),
