@@ -1,16 +1,20 @@
-"""REABK benchmark (BASELINE.json metric) on BASELINE config 2.
+"""REABK benchmark (BASELINE.json metric), headline on BASELINE config 3.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c3|c1|c2|c4|c5]
 
 A step is one full solve of the workload to ||x - x*|| <= 1e-6 ||x*|| (the
-reference's run(), solvers.py:425-474).  `value` = iterations/s with A, b,
-x* resident in HBM (rebk_run_device); `e2e` = the same metric through the
-public API `paper_2001_04179_b200.run(problem, config)` from pinned host
-buffers, re-uploading A every step.  Multi-GPU: C2 does not shard
-(SURVEY §8e), so N ranks run independent replicas (weak scaling); timing is
-the max over ranks.  `--impl reference` times the reference's CPU algorithm
-(the oracle port, oracle/rebk_oracle.py) on the host cores on a bounded
-sample of the same workload.
+reference's run(), solvers.py:425-474).  The default workload is C3
+(200000 x 10000 fp64, 16 GB: the largest BASELINE config that fits one
+B200).  N = 1: the streaming kernel; `value` = iterations/s with A, b, x*
+resident in HBM (rebk_run_device); `e2e` = the same metric through the
+C-ABI from pinned host buffers (A re-uploaded every step).  N > 1
+(torchrun): A row-sharded over the ranks, one strong-scaled solve per step
+(SURVEY §8e), timed as the max over ranks.  The other workloads keep their
+own arms (C1/C2/C4 replicas at N > 1).  `--impl reference` times the
+reference's own CPU path (the installed, unmodified kaczmarz package in
+baseline/_ref; the oracle port if absent) on the host cores on a bounded
+sample of the same instance and prints the same `config` dict.
 """
 
 from __future__ import annotations
@@ -145,17 +149,30 @@ def profiled_traffic(workload):
 
 
 # ------------------------------------------------------------------ CPU arms
-def cpu_reference_run(wl, max_iters, time_cap_s=None):
-    """The reference algorithm on the host cores (oracle port with numpy's C
-    Philox), bounded to max_iters iterations.  Returns (iters, seconds)."""
-    from oracle.rebk_oracle import NumpyRng, OracleSolver
+def reference_module():
+    """The UNMODIFIED reference package, pip-installed into baseline/_ref
+    (DESIGN.md §6); None when that install is absent (then the oracle port
+    stands in, kind "port")."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(path, "kaczmarz", "solvers.py")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    import kaczmarz
 
-    a = wl.problem.a.to_dense()
-    orc = OracleSolver(a, wl.problem.b, wl.row_partition.pointers(), wl.col_partition.pointers(), wl.alpha,
-                       "rebk")
-    tol = wl.rel_tol * float(np.linalg.norm(wl.problem.x_star))
-    res = orc.run(wl.seed, max_iters, tol, wl.problem.x_star, rng=NumpyRng(wl.seed))
-    return res["iters"], res["wall_time"]
+    return kaczmarz
+
+
+def host_threads():
+    """Use every host core for the reference's BLAS (OpenBLAS may cap it)."""
+    ncpu = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(limits=ncpu, user_api="blas")
+    except Exception:
+        pass
+    return ncpu
 
 
 def blas_threads():
@@ -168,33 +185,162 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
+class ReferenceSampler:
+    """Times the reference's CPU path on a bounded sample of a workload.
+
+    kind "reference": the installed reference (baseline/_ref) — one
+    kaczmarz.prepare(problem, config) (setup, excluded like run()'s
+    wall_time, solvers.py:446/:465), then per sample `iters` iterations of
+    exactly run()'s loop body: ctx.step(state) and the oracle_error check
+    ||x - x*|| (solvers.py:398-407, :449-458) every iteration, timed with
+    perf_counter from the same start state.  kind "port": the oracle port
+    (oracle/rebk_oracle.py, the reference's numpy operations) when the
+    install is absent."""
+
+    def __init__(self, a, b, x_star, row_ptr, col_ptr, alpha, beta, seed, tol, sparse=False):
+        self.K = reference_module()
+        self.ncpu = host_threads()
+        self.tol, self.x_star = tol, np.asarray(x_star)
+        t0 = time.perf_counter()
+        if self.K is not None:
+            K = self.K
+            mat = K.Matrix.from_sparse(a) if sparse else K.Matrix.from_dense(a)
+            prob = K.ProblemInstance(a=mat, b=np.asarray(b), x_star=self.x_star, b_perp=None,
+                                     meta=K.ProblemMeta(0, None, False, 0, 0.0))
+            blocks = lambda p: tuple(range(int(p[i]), int(p[i + 1])) for i in range(len(p) - 1))
+            rp = K.Partition("row", int(row_ptr[-1]), blocks(row_ptr))
+            cp = K.Partition("col", int(col_ptr[-1]), blocks(col_ptr))
+            self.cfg = K.SolverConfig(algorithm="rebk", alpha=alpha, seed=seed, row_partition=rp, col_partition=cp,
+                                      max_iters=50_000, stop=K.StoppingRule(tol=tol), beta_max=beta)
+            self.ctx = K.prepare(prob, self.cfg)
+            self.kind = "reference"
+        else:
+            from oracle.rebk_oracle import OracleSolver
+
+            dense = a.toarray() if sparse else a
+            self.orc = OracleSolver(dense, np.asarray(b), np.asarray(row_ptr), np.asarray(col_ptr), alpha, "rebk")
+            self.seed = seed
+            self.kind = "port"
+        self.setup_s = time.perf_counter() - t0
+
+    def sample(self, iters):
+        """(iterations run, loop seconds) of the first `iters` iterations."""
+        if self.kind == "port":
+            from oracle.rebk_oracle import NumpyRng
+
+            res = self.orc.run(self.seed, iters, self.tol, self.x_star, rng=NumpyRng(self.seed))
+            return res["iters"], res["wall_time"]
+        ctx, xs, tol = self.ctx, self.x_star, self.tol
+        st = ctx.initial_state()
+        t0 = time.perf_counter()
+        k = 0
+        if not np.linalg.norm(st.x - xs) <= tol:
+            for k in range(1, iters + 1):
+                ctx.step(st)
+                if np.linalg.norm(st.x - xs) <= tol:
+                    break
+        return k, time.perf_counter() - t0
+
+    def describe(self, iters, workload):
+        what = ("the installed reference (baseline/_ref kaczmarz 0.1.0): prepare() once, then per sample the "
+                "run() loop body (ctx.step + oracle_error check)" if self.kind == "reference" else
+                "oracle port (the reference's numpy operations + numpy Philox)")
+        return (f"first {iters} REBK iterations of the same {workload} instance per sample; {what}; "
+                f"BLAS threads {blas_threads()} of {self.ncpu} host CPUs; setup (prepare) {self.setup_s:.1f} s "
+                f"excluded")
+
+
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
+    if args.workload == "c3":
+        return run_reference_c3(args)
+    if args.workload == "c5":
+        return run_reference_c5(args)
     wl = build_workload(args.workload)
-    sample_iters = args.ref_iters
+    sp = wl.problem.a.is_sparse
+    samp = ReferenceSampler(wl.problem.a._csr if sp else wl.problem.a.to_dense(), wl.problem.b,
+                            wl.problem.x_star, wl.row_partition.pointers(), wl.col_partition.pointers(), wl.alpha,
+                            wl.beta_max, wl.seed, wl.rel_tol * float(np.linalg.norm(wl.problem.x_star)), sparse=sp)
+    return reference_line(args, samp, args.ref_iters, workload_desc(args.workload, wl), ws)
+
+
+def reference_line(args, samp, sample_iters, config, ws, metric=METRIC, unit=UNIT, per=1.0):
     for _ in range(args.warmup):
-        cpu_reference_run(wl, min(sample_iters, 50))
+        samp.sample(min(sample_iters, 10))
     iters_tot, secs = 0, 0.0
     for _ in range(args.steps):
-        it, s = cpu_reference_run(wl, sample_iters)
+        it, s = samp.sample(sample_iters)
         iters_tot += it
         secs += s
-    v = iters_tot / secs
-    cores = blas_threads()
+    v = iters_tot / secs / per
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_desc(args.workload, wl),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{sample_iters} REBK iterations of {args.workload} per step (oracle port: the "
-                                   f"reference's numpy operations and numpy Philox stream), OpenBLAS {cores} threads"},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "scaling": "strong" if args.workload == "c3" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config,
+        "cpu_baseline": {"value": v, "unit": unit, "cores": blas_threads(), "host_cpus": os.cpu_count(),
+                         "kind": samp.kind, "sample": samp.describe(sample_iters, args.workload)},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def c3_config(wl):
+    """The config dict BOTH arms print for C3 (identical keys and values)."""
+    m, n = wl.shape
+    return {"workload": f"C3 dense fp64 {m}x{n} randn (16 GB), inconsistent (r in null(A^T), ||r|| = 0.1 ||A x*||); "
+                        "row/col blocks 1000/500; alpha=1/beta_max; stop ||x-x*||/||x*||<1e-6; seed 17; "
+                        "A row-sharded over the job's GPUs when N > 1",
+            "m": m, "n": n, "row_block": 1000, "col_block": 500, "alpha": wl.alpha, "beta_max": wl.beta_max,
+            "l2_policy": "inputs larger than L2: A = 16 GB, no flush"}
+
+
+def run_reference_c3(args):
+    """C3 on the host cores: the instance is built on the GPU exactly as the
+    ours arm builds it (workloads.c3_device; harness only) and copied to host
+    memory; the reference then runs on the CPU."""
+    import torch
+
+    from paper_2001_04179_b200.workloads import c3_device
+
+    t0 = time.time()
+    wl = c3_device(device=0)
+    a_h = wl.a.cpu().numpy()
+    b_h, xs_h = wl.b.cpu().numpy(), wl.x_star.cpu().numpy()
+    config = c3_config(wl)
+    tol = wl.rel_tol * float(np.linalg.norm(xs_h))
+    row_ptr, col_ptr, alpha, beta, seed = wl.row_ptr, wl.col_ptr, wl.alpha, wl.beta_max, wl.seed
+    del wl
+    torch.cuda.empty_cache()
+    log(f"[bench] c3 on host ({time.time() - t0:.1f}s)")
+    samp = ReferenceSampler(a_h, b_h, xs_h, row_ptr, col_ptr, alpha, beta, seed, tol)
+    log(f"[bench] reference prepare {samp.setup_s:.1f}s (kind {samp.kind})")
+    return reference_line(args, samp, args.ref_iters_c3, config, dist_env()[0])
+
+
+def run_reference_c5(args):
+    from paper_2001_04179_b200 import compute_beta_max, contiguous_partition, Matrix
+    from paper_2001_04179_b200.workloads import c5_arrays
+
+    a32, b32, xs = c5_arrays()
+    m, n = a32.shape
+    a64 = a32.astype(np.float64)
+    rp, cp = contiguous_partition(m, 256, "row"), contiguous_partition(n, 256, "col")
+    beta = compute_beta_max(Matrix.from_dense(a64), rp, cp)[2]
+    samp = ReferenceSampler(a64, b32[:, 0].astype(np.float64), xs[:, 0], rp.pointers(), cp.pointers(), 1.0 / beta,
+                            beta, 17, 1e-4 * float(np.linalg.norm(xs[:, 0])))
+    return reference_line(args, samp, 200, c5_config(beta), dist_env()[0],
+                          metric=METRIC + " (64 RHS per iteration)", per=b32.shape[1])
+
+
+def c5_config(beta):
+    return {"workload": "C5 dense fp32 50000x5000, 64 RHS sharing one block sequence, blocks 256/256, "
+                        "alpha=1/beta_max, stop per column ||x-x*||/||x*||<1e-4",
+            "m": 50000, "n": 5000, "nrhs": 64, "row_block": 256, "col_block": 256, "beta_max": beta,
+            "l2_policy": "inputs larger than L2: A = 1 GB (+1 GB transposed copy), no flush"}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -341,24 +487,27 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        it, s = cpu_reference_run(wl, args.ref_iters)
-        cores = blas_threads()
-        cpu = {"value": it / s, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"first {it} REBK iterations of the same {args.workload} instance (oracle port: the "
-                         f"reference's numpy ops + numpy Philox), OpenBLAS {cores} threads, {s:.1f} s"}
+        sp = prob.a.is_sparse
+        samp = ReferenceSampler(prob.a._csr if sp else prob.a.to_dense(), prob.b, prob.x_star,
+                                wl.row_partition.pointers(), wl.col_partition.pointers(), wl.alpha, wl.beta_max,
+                                wl.seed, tol, sparse=sp)
+        it, s = samp.sample(args.ref_iters)
+        cpu = {"value": it / s, "unit": UNIT, "cores": blas_threads(), "host_cpus": os.cpu_count(),
+               "kind": samp.kind, "sample": samp.describe(it, args.workload) + f"; {s:.1f} s"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {**workload_desc(args.workload, wl), "parallelism": f"replicas x{ws}",
-                       "iters_per_solve": per_solve_iters, "grid_ctas": int(tr.grid_ctas),
-                       "kernel_path": ["rebk_dense_kernel", "rebk_dense_fast_kernel (cluster)",
-                                       "rebk_dense_fast_kernel (cluster, cooperative)",
-                                       "rebk_csr_kernel", "", "",
-                                       "rebk_dense_split_kernel (column/row groups)",
-                                       "rebk_dense_stream_kernel (TMA ring)"][int(tr.kernel_path)]},
+            "config": workload_desc(args.workload, wl),
+            "details": {"parallelism": f"replicas x{ws}", "iters_per_solve": per_solve_iters,
+                        "grid_ctas": int(tr.grid_ctas),
+                        "kernel_path": ["rebk_dense_kernel", "rebk_dense_fast_kernel (cluster)",
+                                        "rebk_dense_fast_kernel (cluster, cooperative)",
+                                        "rebk_csr_kernel", "", "",
+                                        "rebk_dense_split_kernel (column/row groups)",
+                                        "rebk_dense_stream_kernel (TMA ring)"][int(tr.kernel_path)]},
             "time_to_tol_s": ms_max / args.steps / 1e3,
             "achieved_gbps": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -438,12 +587,12 @@ def run_ours_c5(args):
         a_pin = torch.from_numpy(a32).pin_memory()
         b_pin = torch.from_numpy(b32).pin_memory()
         xs_pin = torch.from_numpy(np.ascontiguousarray(xs, dtype=np.float32)).pin_memory()
-        run_multi(a_pin.numpy(), b_pin.numpy(), cfg, X_star=xs_pin.numpy(), tols=tols, a64=a64)  # warm
+        run_multi(a_pin.numpy(), b_pin.numpy(), cfg, X_star=xs_pin.numpy(), tols=tols)  # warm
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         e_its = 0
         for _ in range(args.steps):
-            tr2 = run_multi(a_pin.numpy(), b_pin.numpy(), cfg, X_star=xs_pin.numpy(), tols=tols, a64=a64)
+            tr2 = run_multi(a_pin.numpy(), b_pin.numpy(), cfg, X_star=xs_pin.numpy(), tols=tols)
             e_its += tr2.iters
         torch.cuda.synchronize()
         e_s = time.perf_counter() - t1
@@ -452,32 +601,28 @@ def run_ours_c5(args):
                "d2h_bytes_per_step": int(4 * (n * R + m * R) + 16 * R),
                "time_to_tol_s": e_s / args.steps,
                "path": "paper_2001_04179_b200.multirhs.run_multi(A, B, config): A (1 GB fp32), B and X* uploaded "
-                       "from pinned host memory every step (fresh fp32 device context incl. its transposed copy), "
+                       "from pinned host memory every step (fresh fp32 device context incl. its transposed copy; "
+                       "the sampler weights from the fp64 upcast on the host, as the public API does), "
                        "X and Z read back"}
 
     cpu = None
     if not args.no_cpu:
-        from oracle.rebk_oracle import NumpyRng, OracleSolver
-
-        orc = OracleSolver(a64.to_dense(), b32[:, 0].astype(np.float64), rp.pointers(), cp.pointers(),
-                           1.0 / beta, "rebk")
-        sample = 1500  # ~5 s of host work; tol 0 so the sample always runs to its end
-        res = orc.run(17, sample, 0.0, xs[:, 0].astype(np.float64), rng=NumpyRng(17))
-        cores = blas_threads()
-        cpu = {"value": res["iters"] / res["wall_time"] / R, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"first {res['iters']} REBK iterations of right-hand side 0 in fp64 (the reference solves "
-                         f"one RHS per run; 64 RHS per iteration = 64 such iterations), oracle port with numpy "
-                         f"Philox, OpenBLAS {cores} threads, {res['wall_time']:.2f} s"}
+        samp = ReferenceSampler(a64.to_dense(), b32[:, 0].astype(np.float64), xs[:, 0], rp.pointers(),
+                                cp.pointers(), 1.0 / beta, beta, 17, 1e-300)
+        it, s = samp.sample(200)
+        cpu = {"value": it / s / R, "unit": UNIT, "cores": blas_threads(), "host_cpus": os.cpu_count(),
+               "kind": samp.kind,
+               "sample": samp.describe(it, "c5") + f" (right-hand side 0 in fp64: the reference solves one RHS "
+                                                   f"per run, so 64 RHS per iteration = 64 such iterations); "
+                                                   f"{s:.2f} s"}
 
     line = {
         "metric": METRIC + " (64 RHS per iteration)", "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xTF32 tcgen05)", "data": "synthetic",
-        "config": {"workload": "C5 dense fp32 50000x5000, 64 RHS sharing one block sequence, blocks 256/256, "
-                               "alpha=1/beta_max, stop per column ||x-x*||/||x*||<1e-4", "K": tr.iters,
-                   "check_stride": stride, "iters_per_solve": per_solve,
-                   "l2_policy": "inputs larger than L2: A = 1 GB (+1 GB transposed copy), no flush",
-                   "kernel_path": "k_rebk_mrhs_persistent (tcgen05 kind::tf32, 3xTF32, TMEM accumulators)"},
+        "config": c5_config(beta),
+        "details": {"K": tr.iters, "check_stride": stride, "iters_per_solve": per_solve,
+                    "kernel_path": "k_rebk_mrhs_persistent (tcgen05 kind::tf32, 3xTF32, TMEM accumulators)"},
         "time_to_tol_s": secs / args.steps,
         "achieved_gbps": achieved,
         "achieved_tflops": flops_per_iter * value / 1e12,
@@ -496,15 +641,15 @@ def run_ours_c5(args):
 
 
 def run_ours_c3(args):
-    """Config 3 (16 GB dense fp64) on one GPU: instance built on the device,
-    the streaming kernel through the device-pointer C-ABI.  e2e: A, b, x*
-    uploaded from pinned host memory through rebk_ctx_create_dense + rebk_run
-    (the C-ABI a reference-side binding calls) every step."""
+    """Config 3 (16 GB dense fp64) on one GPU, the N = 1 headline: instance
+    built on the device, the streaming kernel through the device-pointer
+    C-ABI (rebk_run_device).  e2e: A, b, x* uploaded from pinned host memory
+    through rebk_ctx_create_dense + rebk_run (the C-ABI a reference-side
+    binding calls) every step, x and z read back."""
     import ctypes
 
     import torch
 
-    from oracle.rebk_oracle import NumpyRng, OracleSolver
     from paper_2001_04179_b200 import _lib
     from paper_2001_04179_b200.matrix import DeviceMatrix
     from paper_2001_04179_b200.workloads import c3_device
@@ -555,70 +700,87 @@ def run_ours_c3(args):
     ms = ev0.elapsed_time(ev1)
     value = iters / (ms / 1e3)
     per_solve = iters / args.steps
-    achieved = wl.algorithmic_bytes_per_iter * per_solve / (loop_ms / args.steps / 1e3) / 1e9
+    kernel_ms = loop_ms / args.steps
+    achieved = wl.algorithmic_bytes_per_iter * per_solve / (kernel_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
+    tr_info = profiled_traffic("c3")
 
     e2e = None
-    if not args.no_e2e:
+    cpu = None
+    if not (args.no_e2e and args.no_cpu):
         a_pin = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
         a_pin.copy_(wl.a)
         b_h, xs_h = wl.b.cpu().numpy(), wl.x_star.cpu().numpy()
+    if not args.no_e2e:
         x_h, z_h = np.empty(n), np.empty(m)
-        e_steps = max(1, min(args.steps, 2))
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        e_iters = 0
-        for _ in range(e_steps):
+        b_pin = torch.from_numpy(b_h).pin_memory()
+        xs_pin = torch.from_numpy(xs_h).pin_memory()
+        x_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+        z_pin = torch.empty(m, dtype=torch.float64).pin_memory()
+
+        def e2e_step():
             h = ctypes.c_void_p()
             _lib.check(lib.rebk_ctx_create_dense(ctypes.cast(ctypes.c_void_p(a_pin.data_ptr()),
                                                              ctypes.POINTER(ctypes.c_double)), m, n, n, local,
                                                  ctypes.byref(h)), "rebk_ctx_create_dense")
             tr2 = _lib.RebkTrace()
-            _lib.check(lib.rebk_run(h, ctypes.byref(c), _lib.dptr(b_h), None, None, _lib.dptr(xs_h), _lib.dptr(x_h),
-                                    _lib.dptr(z_h), ctypes.byref(tr2)), "rebk_run")
+            p = lambda t: ctypes.cast(ctypes.c_void_p(t.data_ptr()), ctypes.POINTER(ctypes.c_double))
+            _lib.check(lib.rebk_run(h, ctypes.byref(c), p(b_pin), None, None, p(xs_pin), p(x_pin), p(z_pin),
+                                    ctypes.byref(tr2)), "rebk_run")
             lib.rebk_ctx_destroy(h)
-            e_iters += int(tr2.iters)
+            return int(tr2.iters)
+
+        e2e_step()  # warm
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        e_iters = 0
+        for _ in range(args.steps):
+            e_iters += e2e_step()
         e_s = time.perf_counter() - t1
         e2e = {"value": e_iters / e_s, "unit": UNIT, "h2d_bytes_per_step": int(m * n * 8 + (m + n) * 8),
-               "d2h_bytes_per_step": int((m + n) * 8), "time_to_tol_s": e_s / e_steps, "steps": e_steps,
-               "path": "rebk_ctx_create_dense (A from pinned host memory) + rebk_run (host b, x*, x, z) per step"}
-        del a_pin
-
-    cpu = None
+               "d2h_bytes_per_step": int((m + n) * 8), "time_to_tol_s": e_s / args.steps,
+               "path": "rebk_ctx_create_dense (A from pinned host memory, 16 GB H2D) + rebk_run (host b, x*; x, z "
+                       "read back) + rebk_ctx_destroy per step; the sampler arrays (block weights, cumulative "
+                       "sums, alpha/w) are inputs of the C-ABI, computed once like the reference's SolverContext"}
+        del x_h, z_h
     if not args.no_cpu:
-        a_h = wl.a.cpu().numpy()
-        orc = OracleSolver(a_h, wl.b.cpu().numpy(), wl.row_ptr, wl.col_ptr, wl.alpha, "rebk")
-        res = orc.run(wl.seed, 10, tol, wl.x_star.cpu().numpy(), rng=NumpyRng(wl.seed))
-        cores = blas_threads()
-        cpu = {"value": res["iters"] / res["wall_time"], "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"first {res['iters']} REBK iterations of the same c3 instance (oracle port, numpy Philox), "
-                         f"OpenBLAS {cores} threads, {res['wall_time']:.2f} s"}
-        del a_h, orc
+        samp = ReferenceSampler(a_pin.numpy(), b_h, xs_h, wl.row_ptr, wl.col_ptr, wl.alpha, wl.beta_max, wl.seed, tol)
+        it, s = samp.sample(args.ref_iters_c3)
+        cpu = {"value": it / s, "unit": UNIT, "cores": blas_threads(), "host_cpus": os.cpu_count(),
+               "kind": samp.kind, "sample": samp.describe(it, "c3") + f"; {s:.1f} s"}
+        del samp
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (torch Philox on device)",
-        "config": {"workload": f"C3 dense fp64 {m}x{n} randn (16 GB), inconsistent; row/col blocks 1000/500; "
-                               "alpha=1/beta_max; stop ||x-x*||/||x*||<1e-6; seed 17",
-                   "m": m, "n": n, "row_block": 1000, "col_block": 500, "alpha": wl.alpha, "beta_max": wl.beta_max,
-                   "l2_policy": "inputs larger than L2: A = 16 GB, no flush", "parallelism": "1 GPU",
-                   "iters_per_solve": per_solve, "grid_ctas": int(tr.grid_ctas),
-                   "kernel_path": "rebk_dense_stream_kernel (TMA ring)" if tr.kernel_path == 7 else str(tr.kernel_path)},
+        "config": c3_config(wl),
+        "details": {"parallelism": "1 GPU", "iters_per_solve": per_solve, "grid_ctas": int(tr.grid_ctas),
+                    "kernel_path": "rebk_dense_stream_kernel (TMA ring)" if tr.kernel_path == 7 else str(tr.kernel_path)},
         "time_to_tol_s": ms / args.steps / 1e3,
         "achieved_gbps": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": (float(profiled_traffic("c3")["bytes_per_iter"]) * per_solve
-                                 if isinstance(profiled_traffic("c3"), dict) else None),
-                     "traffic_note": (profiled_traffic("c3") or {}).get("note"),
+                     "traffic": (float(tr_info["bytes_per_iter"]) * per_solve if isinstance(tr_info, dict) else None),
+                     "traffic_note": (tr_info or {}).get("note"),
                      "kernel": "rebk_dense_stream_kernel",
                      "peak_source": peak_src, "algorithmic_bytes_per_iter": wl.algorithmic_bytes_per_iter,
-                     "note": "the 800 MB column block is read twice per iteration (u sum, then z update): "
-                             "frac <= ~0.52 by construction"},
+                     "iters_per_launch": per_solve, "kernel_ms_per_launch": kernel_ms,
+                     "two_pass_cap": two_pass_cap(wl),
+                     "note": "the 800 MB column block cannot stay on chip between the u sum and the z update, so it "
+                             "is read twice per iteration: frac <= two_pass_cap by construction"},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * args.steps, "clocks": clk,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def two_pass_cap(wl):
+    """Largest reachable frac for C3 on one GPU: algorithmic (read-once)
+    bytes over the bytes that must move (column block twice, row block once)."""
+    m, n = wl.shape
+    tj = int(np.diff(wl.col_ptr).max())
+    ti = int(np.diff(wl.row_ptr).max())
+    return (m * tj + ti * n) / (2.0 * m * tj + ti * n)
 
 
 def run_ours_c3_sharded(args):
@@ -712,15 +874,12 @@ def run_ours_c3_sharded(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (torch Philox on device)",
-            "config": {"workload": f"C3 dense fp64 {m}x{n} randn (16 GB), row-sharded over {ws} GPU(s) "
-                                   "(interleaved rows of every row block), NCCL allreduce of u (|J|) and dx (n); "
-                                   "row/col blocks 1000/500; stop ||x-x*||/||x*||<1e-6; seed 17",
-                       "m": m, "n": n, "parallelism": f"row-sharded x{ws} (NCCL)", "iters_per_solve": iters / args.steps,
-                       "timing": "host wall clock around whole solves, max over ranks (each solve syncs once per "
-                                 "32-iteration chunk)",
-                       "driver": "python loop + torch.distributed NCCL" if args.python_loop else
-                                 "rebk_shard_run (C++ issue loop, NCCL via librebk)",
-                       "l2_policy": "inputs larger than L2: A = 16 GB, no flush"},
+            "config": c3_config(wl),
+            "details": {"parallelism": f"row-sharded x{ws} (interleaved rows of every row block)",
+                        "iters_per_solve": iters / args.steps,
+                        "timing": "CUDA events around whole solves on each rank, max over ranks",
+                        "driver": "python loop + torch.distributed NCCL" if args.python_loop else
+                                  "rebk_shard_run (C++ issue loop, NCCL via librebk)"},
             "time_to_tol_s": secs / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
                          "frac": achieved / (peak * ws), "traffic": None, "kernel": "rebk_shard_* (per rank)",
@@ -741,26 +900,24 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="BASELINE config; c3 (the largest config that fits one B200) is the headline")
     ap.add_argument("--max-iters", type=int, default=50_000)
-    ap.add_argument("--ref-iters", type=int, default=2000, help="iterations per CPU reference sample")
+    ap.add_argument("--ref-iters", type=int, default=2000, help="iterations per CPU reference sample (c1/c2/c4)")
+    ap.add_argument("--ref-iters-c3", type=int, default=20, help="iterations per CPU reference sample (c3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--sharded", action="store_true", help="c3: row-sharded multi-GPU path (NCCL)")
+    ap.add_argument("--sharded", action="store_true", help="c3: row-sharded path also at N = 1")
     ap.add_argument("--python-loop", action="store_true", help="--sharded: issue each iteration from Python")
     args = ap.parse_args()
+    ws = dist_env()[0]
     if args.impl == "reference":
-        if args.workload in ("c3", "c5"):
-            # the default (driver) workload is c2; for c3/c5 the ours arm's
-            # cpu_baseline times the oracle port on the same instance
-            print(json.dumps({"impl": "reference", "unavailable": f"--impl reference is implemented for c1/c2/c4; "
-                              f"{args.workload}'s CPU reference is the cpu_baseline of the ours arm"}), flush=True)
-            return 0
         return run_reference_arm(args)
     if args.workload == "c5":
         return run_ours_c5(args)
     if args.workload == "c3":
-        return run_ours_c3_sharded(args) if args.sharded else run_ours_c3(args)
+        # N > 1 (torchrun): A row-sharded over the ranks (strong scaling)
+        return run_ours_c3_sharded(args) if (args.sharded or ws > 1) else run_ours_c3(args)
     return run_ours(args)
 
 
