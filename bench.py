@@ -784,21 +784,24 @@ def two_pass_cap(wl):
 
 
 def run_ours_c3_sharded(args):
-    """Config 3 row-sharded over the job's GPUs: one process per
-    GPU, every rank builds the same device instance and keeps its interleaved
-    rows of every row block; per iteration the |J|-length column-block
-    product and the n-length x update are NCCL allreduces
-    (paper_2001_04179_b200.sharded.run_sharded_chunked: per-rank rebk_shard_*
-    kernels, errors checked on the device once per chunk).  Strong scaling:
-    the whole job does one solve per step."""
+    """Config 3 row-sharded over the job's GPUs: one
+    process per GPU; every rank builds the same device instance and keeps its
+    interleaved rows of every row block.  One persistent kernel per rank per
+    solve (rebk_shard_stream_kernel): the |J|-length column products and the
+    n-length x-update partials are exchanged INSIDE the kernel through peer
+    memory (CUDA IPC over NVLink) with system-scope release flags, summed in
+    rank order on every rank.  Strong scaling: the whole job does one solve
+    per step.  `--python-loop` / `--nccl-driver` select the earlier
+    host-driven variants (per-rank kernels + ncclAllReduce per iteration)."""
     import ctypes
 
     import torch
     import torch.distributed as dist
 
     from paper_2001_04179_b200 import _lib
-    from paper_2001_04179_b200.sharded import (CudaShardBackend, NcclComm, ShardPlan, nccl_unique_id, owned_rows,
-                                                run_sharded_chunked, run_sharded_native)
+    from paper_2001_04179_b200.matrix import DeviceMatrix
+    from paper_2001_04179_b200.sharded import (CudaShardBackend, NcclComm, ShardExchange, ShardPlan, nccl_unique_id,
+                                                owned_rows, run_sharded_chunked, run_sharded_native)
     from paper_2001_04179_b200.workloads import c3_device
 
     ws, rank, local = dist_env()
@@ -824,51 +827,123 @@ def run_ours_c3_sharded(args):
     abytes = wl.algorithmic_bytes_per_iter
     rows, ranges = owned_rows(wl.row_ptr, ws, rank)
     rows_t = torch.from_numpy(rows).to(dev)
-    a_local = wl.a.index_select(0, rows_t)
-    b_local = wl.b.index_select(0, rows_t)
+    a_local = wl.a.index_select(0, rows_t).contiguous()
+    b_local = wl.b.index_select(0, rows_t).contiguous()
     wl.a = None
     torch.cuda.empty_cache()
     tol = wl.rel_tol * float(wl.x_star.norm())
-    c = wl.cfg("max_iters_only", 1.0, args.max_iters)
-    picks = np.empty((args.max_iters, 2), dtype=np.int32)
-    _lib.check(_lib.load().rebk_sample_sequence(ctypes.byref(c), 1, args.max_iters,
-                                                picks.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))),
-               "rebk_sample_sequence")
-    plan = ShardPlan(wl.row_ptr, wl.col_ptr, wl.alpha / wl.row_w, wl.alpha / wl.col_w, picks)
     log(f"[bench] c3 sharded rank {rank}/{ws}: {rows.size} rows of {m} ({time.time() - t0:.1f}s)")
-
-    # NCCL communicator owned by librebk: rank 0's unique id over torch.distributed
-    uid = [nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0)
-    comm = NcclComm(uid[0], ws, rank, local)
+    host_driver = args.python_loop or args.nccl_driver
+    stream = torch.cuda.Stream(device=dev)
+    x_d = torch.zeros(n, dtype=torch.float64, device=dev)
+    z_d = torch.empty_like(b_local)
+    if host_driver:
+        c = wl.cfg("max_iters_only", 1.0, args.max_iters)
+        picks = np.empty((args.max_iters, 2), dtype=np.int32)
+        _lib.check(_lib.load().rebk_sample_sequence(ctypes.byref(c), 1, args.max_iters,
+                                                    picks.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))),
+                   "rebk_sample_sequence")
+        plan = ShardPlan(wl.row_ptr, wl.col_ptr, wl.alpha / wl.row_w, wl.alpha / wl.col_w, picks)
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = NcclComm(uid[0], ws, rank, local)
+    else:
+        c = wl.cfg("oracle_error", tol, args.max_iters)
+        xchg = ShardExchange(ws, rank, int(np.diff(wl.col_ptr).max()), n, local, dist.all_gather_object)
+        dm = DeviceMatrix.from_device_pointer(a_local.data_ptr(), a_local.shape[0], n, n, local)
 
     def solve():
-        be = CudaShardBackend.from_device(a_local, b_local, wl.x_star, True, local)
-        if args.python_loop:
-            return run_sharded_chunked(be, plan, ranges, args.max_iters, tol,
-                                       allreduce=lambda v: dist.all_reduce(v), chunk=32)
-        return run_sharded_native(be, comm, plan, ranges, args.max_iters, tol, chunk=32)
+        if host_driver:
+            be = CudaShardBackend.from_device(a_local, b_local, wl.x_star, True, local)
+            if args.python_loop:
+                res = run_sharded_chunked(be, plan, ranges, args.max_iters, tol,
+                                          allreduce=lambda v: dist.all_reduce(v), chunk=32)
+            else:
+                res = run_sharded_native(be, comm, plan, ranges, args.max_iters, tol, chunk=32)
+            return int(res["iters"]), bool(res["converged"]), float("nan")
+        with torch.cuda.stream(stream):
+            x_d.zero_()
+            z_d.copy_(b_local)
+        tr = xchg.run(dm, c, ranges, b_local.data_ptr(), wl.x_star.data_ptr(), x_d.data_ptr(), z_d.data_ptr(),
+                      stream.cuda_stream)
+        return int(tr.iters), bool(tr.converged), float(tr.loop_ms)
 
     for _ in range(max(args.warmup, 1)):
-        res = solve()
-    log(f"[bench] c3 sharded warm-up: ITER={res['iters']} converged={res['converged']}")
+        it, conv, _ = solve()
+    log(f"[bench] c3 sharded warm-up: ITER={it} converged={conv}")
     clocks = ClockSampler(local)
+    torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
-    t1 = time.perf_counter()
-    iters = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    iters, loop_ms = 0, 0.0
     for _ in range(args.steps):
-        res = solve()
-        iters += int(res["iters"])
+        it, conv, lm = solve()
+        iters += it
+        loop_ms += lm
+    ev1.record(stream)
     torch.cuda.synchronize()
-    el = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device=dev)
-    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    dist.barrier()
     clk = clocks.stop()
-    secs = float(el.item())
+    el = torch.tensor([ev0.elapsed_time(ev1) / 1e3, loop_ms / 1e3], dtype=torch.float64, device=dev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    secs, kernel_s = float(el[0].item()), float(el[1].item())
     value = iters / secs
+    per_solve = iters / args.steps
     peak, peak_src = measured_peak()
-    achieved = abytes * value / 1e9
+    achieved = abytes * per_solve / (kernel_s / args.steps) / 1e9 if kernel_s > 0 else abytes * value / 1e9
+
+    e2e = None
+    if not args.no_e2e and not host_driver:
+        # e2e per rank through the C-ABI: this rank's rows of A, b, x* from
+        # pinned host memory into a fresh ctx, one sharded solve, x and z back
+        a_pin = torch.empty(tuple(a_local.shape), dtype=torch.float64, pin_memory=True)
+        a_pin.copy_(a_local)
+        b_pin = b_local.cpu().pin_memory()
+        xs_pin = wl.x_star.cpu().pin_memory()
+        x_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+        z_pin = torch.empty(b_local.shape[0], dtype=torch.float64).pin_memory()
+        lib = _lib.load()
+
+        def e2e_step():
+            h = ctypes.c_void_p()
+            _lib.check(lib.rebk_ctx_create_dense(ctypes.cast(ctypes.c_void_p(a_pin.data_ptr()),
+                                                             ctypes.POINTER(ctypes.c_double)), a_pin.shape[0], n, n,
+                                                 local, ctypes.byref(h)), "rebk_ctx_create_dense")
+            with torch.cuda.stream(stream):
+                b2 = b_pin.to(dev, non_blocking=True)
+                xs2 = xs_pin.to(dev, non_blocking=True)
+                x2 = torch.zeros(n, dtype=torch.float64, device=dev)
+                z2 = b2.clone()
+            tr2 = _lib.RebkTrace()
+            _lib.check(lib.rebk_shard_run_device(h, xchg.handle, ctypes.byref(c), _lib.i64ptr(np.ascontiguousarray(
+                ranges, dtype=np.int64)), ctypes.c_void_p(b2.data_ptr()), ctypes.c_void_p(xs2.data_ptr()),
+                ctypes.c_void_p(x2.data_ptr()), ctypes.c_void_p(z2.data_ptr()), ctypes.c_void_p(stream.cuda_stream),
+                ctypes.byref(tr2)), "rebk_shard_run_device")
+            with torch.cuda.stream(stream):
+                x_pin.copy_(x2, non_blocking=True)
+                z_pin.copy_(z2, non_blocking=True)
+            stream.synchronize()
+            lib.rebk_ctx_destroy(h)
+            return int(tr2.iters)
+
+        e2e_step()
+        dist.barrier()
+        t1 = time.perf_counter()
+        e_iters = 0
+        for _ in range(args.steps):
+            e_iters += e2e_step()
+        e_t = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device=dev)
+        dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+        e_s = float(e_t.item())
+        e2e = {"value": e_iters / e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int((m * n + m + ws * n) * 8), "d2h_bytes_per_step": int((m + ws * n) * 8),
+               "time_to_tol_s": e_s / args.steps,
+               "path": "per rank: rebk_ctx_create_dense (its rows of A from pinned host memory) + b, x* H2D + "
+                       "rebk_shard_run_device + x, z D2H; job time = max over ranks (host clock around the "
+                       "synchronous steps)"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -876,20 +951,30 @@ def run_ours_c3_sharded(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (torch Philox on device)",
             "config": c3_config(wl),
             "details": {"parallelism": f"row-sharded x{ws} (interleaved rows of every row block)",
-                        "iters_per_solve": iters / args.steps,
-                        "timing": "CUDA events around whole solves on each rank, max over ranks",
-                        "driver": "python loop + torch.distributed NCCL" if args.python_loop else
-                                  "rebk_shard_run (C++ issue loop, NCCL via librebk)"},
+                        "iters_per_solve": per_solve,
+                        "timing": "CUDA events around the steps on each rank's stream, max over ranks",
+                        "driver": ("python loop + torch.distributed NCCL" if args.python_loop else
+                                   "rebk_shard_run (C++ issue loop, ncclAllReduce per iteration)" if host_driver else
+                                   "rebk_shard_stream_kernel: one persistent kernel per rank per solve, u and dx "
+                                   "exchanged in-kernel through peer memory (CUDA IPC) with release flags"),
+                        "grid_ctas_per_rank": int(getattr(xchg, "grid_ctas", 0)) if not host_driver else None},
             "time_to_tol_s": secs / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
-                         "frac": achieved / (peak * ws), "traffic": None, "kernel": "rebk_shard_* (per rank)",
+                         "frac": achieved / (peak * ws), "traffic": None,
+                         "kernel": "rebk_shard_stream_kernel (per rank)" if not host_driver else "rebk_shard_*",
                          "peak_source": peak_src + f" x {ws} GPUs",
-                         "algorithmic_bytes_per_iter": abytes},
-            "cpu_baseline": None, "e2e": None, "gpu_launches": 8 * iters, "clocks": clk,
+                         "algorithmic_bytes_per_iter": abytes, "iters_per_launch": per_solve,
+                         "kernel_ms_per_launch": 1e3 * kernel_s / args.steps},
+            "cpu_baseline": None, "e2e": e2e,
+            "gpu_launches": (8 * iters) if host_driver else 2 * args.steps, "clocks": clk,
         }
         os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.barrier()
-    comm.close()
+    if host_driver:
+        comm.close()
+    else:
+        dm.close()
+        xchg.close()
     dist.destroy_process_group()
     return 0
 
@@ -909,6 +994,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="c3: row-sharded path also at N = 1")
     ap.add_argument("--python-loop", action="store_true", help="--sharded: issue each iteration from Python")
+    ap.add_argument("--nccl-driver", action="store_true",
+                    help="--sharded: the C++ issue loop with ncclAllReduce per iteration instead of the in-kernel exchange")
     args = ap.parse_args()
     ws = dist_env()[0]
     if args.impl == "reference":

@@ -116,7 +116,7 @@ typedef struct rebk_trace {
   int64_t errors_cap;
   int64_t n_checks;
   int32_t grid_ctas;        /* CTAs the persistent kernel used */
-  int32_t kernel_path;      /* 0 dense general, 1 dense clustered, 2 same (cooperative), 3 sparse, 4/5 multi-RHS (5: BF16x9 tensor cores), 6 dense split column/row groups, 7 dense streaming (blocks larger than shared memory), 8 multi-RHS on hand-written tcgen05 3xTF32 kernels */
+  int32_t kernel_path;      /* 0 dense general, 1 dense clustered, 2 same (cooperative), 3 sparse, 4/5 multi-RHS (5: BF16x9 tensor cores), 6 dense split column/row groups, 7 dense streaming (blocks larger than shared memory), 8 multi-RHS on hand-written tcgen05 3xTF32 kernels, 9 row-sharded streaming kernel with the in-kernel cross-rank exchange */
   int64_t nonfinite_at;     /* first check (iteration k) whose error was NaN/Inf; -1 if none */
 } rebk_trace;
 
@@ -229,6 +229,44 @@ int rebk_nccl_comm_create(const char* libnccl_path, const unsigned char id[128],
 int rebk_nccl_comm_destroy(void* comm);
 int rebk_shard_run(rebk_ctx* ctx, void* comm, const rebk_shard_run_args* args, int64_t* iters_out,
                    int32_t* converged_out, double* final_err_out);
+
+/* ---- row-sharded multi-GPU solve with the exchange INSIDE the persistent
+ * kernel (rebk_shard_stream_kernel).  Every rank holds the
+ * interleaved rows of every row block (local row q of block b on rank
+ * floor(q P / |I_b|)), z and b follow the rows, x is replicated.  Per
+ * iteration the |J| column-product partials and the n-length x-update
+ * partials go straight from the kernel into every rank's exchange buffer
+ * (peer memory over NVLink, mapped with CUDA IPC), each followed by a
+ * release flag at system scope; every rank sums the P partials in rank
+ * order, so x stays bitwise replicated and all ranks stop at the same check.
+ * One launch per solve (per 2^20 iterations), no host work per iteration.
+ * Replaces step_rebk/run (solvers.py:324-337, :425-474) on the sharded A.
+ *
+ *   rebk_shard_grid_ctas    CTAs per rank this device runs (all ranks must use the same value: take the min)
+ *   rebk_shard_xchg_create  this rank's exchange buffer (nranks <= 8)
+ *   rebk_shard_xchg_ipc_handle / _open_peers  export the buffer, map every peer's (handles: [nranks][64])
+ *   rebk_shard_run_device   one solve of this rank's shard; ctx = this rank's rows; cfg = the GLOBAL partitions
+ *                           and sampler arrays (row_ptr of the whole matrix); local_ranges [n_row_blocks][2] =
+ *                           this rank's rows of each block in local numbering; b_dev, z_io_dev local; x_io_dev,
+ *                           x_star_dev replicated.  All ranks must call it the same number of times.
+ *   rebk_shard_run_virtual  the same kernel with `vranks` ranks emulated in ONE cooperative launch on one GPU
+ *                           (the ranks' rows stacked in ctx, rows_per_rank[vranks], local_ranges
+ *                           [vranks][n_row_blocks][2], b/z stacked, x_io_dev [vranks][n]): tests the exchange
+ *                           protocol where ranks that wait on each other must run at the same time.
+ * A rank whose peer never arrives fails after 60 s (REBK_ECUDA) instead of hanging. */
+typedef struct rebk_shard_xchg rebk_shard_xchg;
+int rebk_shard_grid_ctas(int device, int* grid_ctas);
+int rebk_shard_xchg_create(int nranks, int rank, int64_t nJ_cap, int64_t n_cap, int grid_ctas, int device,
+                           rebk_shard_xchg** out);
+int rebk_shard_xchg_ipc_handle(rebk_shard_xchg* x, unsigned char handle_out[64]);
+int rebk_shard_xchg_open_peers(rebk_shard_xchg* x, const unsigned char* handles);
+int rebk_shard_xchg_destroy(rebk_shard_xchg* x);
+int rebk_shard_run_device(rebk_ctx* ctx, rebk_shard_xchg* x, const rebk_cfg* cfg, const int64_t* local_ranges,
+                          const double* b_dev, const double* x_star_dev, double* x_io_dev, double* z_io_dev,
+                          void* stream, rebk_trace* trace);
+int rebk_shard_run_virtual(rebk_ctx* ctx, int vranks, const int64_t* rows_per_rank, const int64_t* local_ranges,
+                           const rebk_cfg* cfg, const double* b_dev, const double* x_star_dev, double* x_io_dev,
+                           double* z_io_dev, void* stream, rebk_trace* trace);
 
 /* ---- sampler (sampling.py:23-45 Rng, :137-145 WeightedSampler.sample) -----
  * Device sampling of the (col, row) block-index pairs of iterations

@@ -125,6 +125,15 @@ SIGNATURES = {
     "rebk_shard_rowstep": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "rebk_shard_xupdate": (c_int, [c_int64, c_double, c_void_p, c_void_p, c_void_p]),
     "rebk_shard_err2": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "rebk_shard_grid_ctas": (c_int, [c_int, POINTER(c_int)]),
+    "rebk_shard_xchg_create": (c_int, [c_int, c_int, c_int64, c_int64, c_int, c_int, POINTER(c_void_p)]),
+    "rebk_shard_xchg_ipc_handle": (c_int, [c_void_p, ctypes.c_char_p]),
+    "rebk_shard_xchg_open_peers": (c_int, [c_void_p, ctypes.c_char_p]),
+    "rebk_shard_xchg_destroy": (c_int, [c_void_p]),
+    "rebk_shard_run_device": (c_int, [c_void_p, c_void_p, POINTER(RebkCfg), _P_I64, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, POINTER(RebkTrace)]),
+    "rebk_shard_run_virtual": (c_int, [c_void_p, c_int, _P_I64, _P_I64, POINTER(RebkCfg), c_void_p, c_void_p,
+                                       c_void_p, c_void_p, c_void_p, POINTER(RebkTrace)]),
     "rebk_sample_sequence": (c_int, [POINTER(RebkCfg), c_int64, c_int64, POINTER(c_int32)]),
     "rebk_block_frobenius_sq": (c_int, [c_void_p, c_int, c_int64, _P_I64, _P_D]),
     "rebk_block_sigma1_sq": (c_int, [c_void_p, c_int, c_int64, _P_I64, c_int, _P_D, POINTER(c_int32)]),

@@ -356,15 +356,18 @@ int pow2floor_host(int v) {
   return p;
 }
 
-StreamGeometry stream_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int G, bool extended) {
+// m rows split over G CTAs, n columns split over G CTAs; the largest row /
+// column block; odd column-block starts need one extra leading column
+StreamGeometry stream_geometry_dims(int64_t m, int64_t n, int nI_max, int nJ_max, bool cols_even, int G,
+                                    bool extended) {
   StreamGeometry f;
   f.G = G;
   for (int q = 0; q < G; ++q) {
-    f.nR_max = std::max(f.nR_max, split_rows(ctx->m, G, q + 1) - split_rows(ctx->m, G, q));
-    f.nC_max = std::max(f.nC_max, split_even(ctx->n, G, q + 1) - split_even(ctx->n, G, q));
+    f.nR_max = std::max(f.nR_max, split_rows(m, G, q + 1) - split_rows(m, G, q));
+    f.nC_max = std::max(f.nC_max, split_even(n, G, q + 1) - split_even(n, G, q));
   }
-  f.nI_max = max_block(cfg->n_row_blocks, cfg->row_ptr);
-  f.nJ_max = extended ? max_block(cfg->n_col_blocks, cfg->col_ptr) : 0;
+  f.nI_max = nI_max;
+  f.nJ_max = extended ? nJ_max : 0;
   f.pad_nC = round_even(f.nC_max + 1);
   f.pad_nR = extended ? round_even(f.nR_max + 1) : 0;
   f.pad_nJ = round_even(f.nJ_max + 2);  // + a leading column for odd block starts
@@ -384,7 +387,7 @@ StreamGeometry stream_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int G, 
     return std::max(2, round_even((len + nsub - 1) / nsub));
   };
   if (extended) {
-    f.cw = width(f.nJ_max + (blocks_even(cfg->n_col_blocks, cfg->col_ptr) ? 0 : 1));
+    f.cw = width(f.nJ_max + (cols_even ? 0 : 1));
     f.ch = std::max(1, std::min({f.SD / f.cw, hcap, std::max(1, f.nR_max)}));
     f.lc = std::min(32, pow2floor_host(512 / f.ch));
   }
@@ -394,6 +397,12 @@ StreamGeometry stream_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int G, 
   f.smem_bytes = ((size_t)f.NS * f.SD + vec) * sizeof(double);
   f.ok = f.smem_bytes <= (size_t)kSmemBudget;
   return f;
+}
+
+StreamGeometry stream_geometry(const rebk_ctx* ctx, const rebk_cfg* cfg, int G, bool extended) {
+  return stream_geometry_dims(ctx->m, ctx->n, max_block(cfg->n_row_blocks, cfg->row_ptr),
+                              extended ? max_block(cfg->n_col_blocks, cfg->col_ptr) : 0,
+                              !extended || blocks_even(cfg->n_col_blocks, cfg->col_ptr), G, extended);
 }
 
 // REBK_PROF tables: per-iteration microseconds per mark, mean and max over
@@ -1209,6 +1218,273 @@ int run_device_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, con
   return rc;
 }
 
+
+// ---- row-sharded streaming path (rebk_shard_stream_kernel) -----
+// Exchange buffer of one rank: inbox_u [2][P][nJ_cap], inbox_x [2][P][n_cap],
+// flags [2][2][P][Gr] (layout documented at RankXchg).
+size_t xchg_bytes(int P, int64_t nJ_cap, int64_t n_cap, int Gr) {
+  return sizeof(double) * (size_t)(2 * P * nJ_cap + 2 * P * n_cap) + sizeof(unsigned long long) * (size_t)(4 * P * Gr);
+}
+void xchg_carve(char* base, int P, int64_t nJ_cap, int64_t n_cap, double** iu, double** ix, unsigned long long** fl) {
+  *iu = (double*)base;
+  *ix = *iu + 2 * P * nJ_cap;
+  *fl = (unsigned long long*)(*ix + 2 * P * n_cap);
+}
+
+struct ShardLaunch {
+  int vranks = 1, P = 1, rank = 0, Gr = 0;
+  const int64_t* rows = nullptr;    // [vranks] local rows of each (virtual) rank
+  const int64_t* ranges = nullptr;  // host [vranks][s][2]
+  char* xbuf[kMaxRanks] = {};       // exchange buffer of every rank, as seen from this GPU
+  int64_t nJ_cap = 0, n_cap = 0;
+  unsigned long long seq_base = 0;
+};
+
+int shard_stream_impl(rebk_ctx* ctx, const rebk_cfg* cfg, ShardLaunch& L, const double* b_dev, const double* xs_dev,
+                      double* x_dev, double* z_dev, cudaStream_t stream, rebk_trace* trace) {
+  const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
+  if (cfg->algorithm < 0 || cfg->algorithm > 3) return fail(REBK_EINVAL, "unknown algorithm %d", cfg->algorithm);
+  if (cfg->stop_mode != REBK_STOP_ORACLE_ERROR && cfg->stop_mode != REBK_STOP_MAX_ITERS_ONLY)
+    return fail(REBK_EINVAL, "the row-sharded path supports oracle_error and max_iters_only stopping");
+  if (cfg->stop_mode == REBK_STOP_ORACLE_ERROR && !(cfg->tol > 0.0)) return fail(REBK_EINVAL, "tol must be positive");
+  if (cfg->stop_mode == REBK_STOP_ORACLE_ERROR && !xs_dev)
+    return fail(REBK_EINVAL, "oracle_error stopping needs a problem with x_star");
+  if (cfg->check_stride < 1 || cfg->max_iters < 0) return fail(REBK_EINVAL, "bad check_stride / max_iters");
+  if (!b_dev || !x_dev || (extended && !z_dev)) return fail(REBK_EINVAL, "missing b / x / z buffer");
+  if (ctx->kind != 0) return fail(REBK_EINVAL, "the row-sharded path needs a dense fp64 context");
+  if (L.vranks < 1 || L.vranks > kMaxRanks || L.P < 1 || L.P > kMaxRanks || L.rank < 0 || L.rank >= L.P ||
+      (L.vranks > 1 && L.vranks != L.P))
+    return fail(REBK_EINVAL, "bad rank layout (P = %d, rank = %d, vranks = %d; at most %d ranks)", L.P, L.rank,
+                L.vranks, kMaxRanks);
+  const int64_t s = cfg->n_row_blocks;
+  if (s < 1 || !cfg->row_ptr) return fail(REBK_EINVAL, "row partition missing");
+  int rc = check_partition("row", s, cfg->row_ptr, cfg->row_cum, cfg->row_scale, cfg->row_ptr[s]);
+  if (rc) return rc;
+  if (extended) {
+    rc = check_partition("col", cfg->n_col_blocks, cfg->col_ptr, cfg->col_cum, cfg->col_scale, ctx->n);
+    if (rc) return rc;
+  }
+  // every rank's local ranges: block b's rows are [lo, hi), consecutive, and
+  // together they are the rank's rows; ranks stacked in the ctx for vranks > 1
+  int64_t stacked = 0, m_max = 0, nI_loc = 1;
+  for (int v = 0; v < L.vranks; ++v) {
+    const int64_t* rg = L.ranges + (int64_t)v * 2 * s;
+    int64_t pos = 0;
+    for (int64_t b = 0; b < s; ++b) {
+      if (rg[2 * b] != pos || rg[2 * b + 1] < pos || rg[2 * b + 1] - rg[2 * b] > cfg->row_ptr[b + 1] - cfg->row_ptr[b])
+        return fail(REBK_EINVAL, "rank %d: local row ranges must be consecutive shares of the row blocks", v);
+      pos = rg[2 * b + 1];
+      nI_loc = std::max(nI_loc, rg[2 * b + 1] - rg[2 * b]);
+    }
+    if (pos != L.rows[v]) return fail(REBK_EINVAL, "rank %d: ranges cover %lld rows, the rank holds %lld", v,
+                                      (long long)pos, (long long)L.rows[v]);
+    stacked += L.rows[v];
+    m_max = std::max(m_max, L.rows[v]);
+  }
+  if (stacked != ctx->m) return fail(REBK_EINVAL, "the ctx holds %lld rows, the ranks %lld", (long long)ctx->m,
+                                     (long long)stacked);
+  if (ctx->n > INT32_MAX || ctx->m > INT32_MAX) return fail(REBK_EINVAL, "matrix dimension exceeds 2^31");
+  if ((ctx->lda % 2) != 0 || ((uintptr_t)ctx->A % 16) != 0 || encode_fn() == nullptr)
+    return fail(REBK_EINVAL, "the row-sharded path needs a 16-byte aligned A with an even leading dimension");
+  const int nJ_max = extended ? max_block(cfg->n_col_blocks, cfg->col_ptr) : 0;
+  if (nJ_max > L.nJ_cap || ctx->n > L.n_cap) return fail(REBK_EINVAL, "exchange buffers too small for this problem");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  StreamGeometry stg = stream_geometry_dims(std::max<int64_t>(m_max, 1), ctx->n, (int)nI_loc, nJ_max,
+                                            !extended || blocks_even(cfg->n_col_blocks, cfg->col_ptr), L.Gr, extended);
+  int occ = 0;
+  if (!stg.ok || stream_kernel_occupancy(stg.smem_bytes, &occ) != cudaSuccess || occ < 1)
+    return fail(REBK_EINVAL, "row-sharded geometry does not fit shared memory");
+  if (L.vranks * L.Gr > occ * ctx->sm_count)
+    return fail(REBK_EINVAL, "%d ranks x %d CTAs are not co-resident on this GPU", L.vranks, L.Gr);
+  CUtensorMap tm_c, tm_r;
+  if (!(extended ? encode_box(&tm_c, ctx, stg.cw, stg.ch) : true) || !encode_box(&tm_r, ctx, stg.rw, stg.rh))
+    return fail(REBK_ECUDA, "tensor map encoding failed");
+  if (!extended) tm_c = tm_r;
+
+  DevArena arena;
+  arena.stream = stream;
+  const int64_t t = extended ? cfg->n_col_blocks : 0;
+  const int G = L.Gr;
+  int64_t *d_row_ptr, *d_col_ptr = nullptr, *d_ranges;
+  double *d_row_cum, *d_row_scale, *d_col_cum = nullptr, *d_col_scale = nullptr;
+  CUDA_TRY(arena.alloc(&d_row_ptr, s + 1));
+  CUDA_TRY(arena.alloc(&d_row_cum, s));
+  CUDA_TRY(arena.alloc(&d_row_scale, s));
+  CUDA_TRY(arena.alloc(&d_ranges, (size_t)L.vranks * 2 * s));
+  CUDA_TRY(cudaMemcpyAsync(d_row_ptr, cfg->row_ptr, (s + 1) * 8, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(d_row_cum, cfg->row_cum, s * 8, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(d_row_scale, cfg->row_scale, s * 8, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaMemcpyAsync(d_ranges, L.ranges, (size_t)L.vranks * 2 * s * 8, cudaMemcpyHostToDevice, stream));
+  if (extended) {
+    CUDA_TRY(arena.alloc(&d_col_ptr, t + 1));
+    CUDA_TRY(arena.alloc(&d_col_cum, t));
+    CUDA_TRY(arena.alloc(&d_col_scale, t));
+    CUDA_TRY(cudaMemcpyAsync(d_col_ptr, cfg->col_ptr, (t + 1) * 8, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d_col_cum, cfg->col_cum, t * 8, cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d_col_scale, cfg->col_scale, t * 8, cudaMemcpyHostToDevice, stream));
+  }
+  int32_t* d_picks = nullptr;
+  if (cfg->picks && cfg->max_iters > 0) {
+    CUDA_TRY(arena.alloc(&d_picks, 2 * cfg->max_iters));
+    CUDA_TRY(cudaMemcpyAsync(d_picks, cfg->picks, 2 * cfg->max_iters * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+  }
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(cfg->max_iters, (int64_t)1 << 20));
+  Plan* d_plan;
+  CUDA_TRY(arena.alloc(&d_plan, chunk));
+  // per-rank workspace, identical layout at vr * ws_stride
+  const int64_t nJw = std::max(nJ_max, 1), nIw = std::max<int64_t>(nI_loc, 1);
+  const int64_t o_rpart = nJw * G, o_u = o_rpart + nIw * G, o_r = o_u + nJw, o_err = o_r + nIw;
+  const int64_t ws_stride = (o_err + G + 1) & ~(int64_t)1;
+  double* d_ws;
+  CUDA_TRY(arena.alloc(&d_ws, (size_t)ws_stride * L.vranks));
+  Control* d_ctl;
+  CUDA_TRY(arena.alloc(&d_ctl, L.vranks));
+  CUDA_TRY(cudaMemsetAsync(d_ctl, 0, sizeof(Control) * L.vranks, stream));
+  const int64_t errs_cap = (cfg->record_errors && trace && trace->errors) ? trace->errors_cap : 0;
+  double* d_errs = nullptr;
+  if (errs_cap > 0) CUDA_TRY(arena.alloc(&d_errs, errs_cap));
+  // emulated ranks: one exchange buffer per virtual rank, fresh per run
+  char* vbuf = nullptr;
+  if (L.vranks > 1 || !L.xbuf[0]) {
+    const size_t xb = (xchg_bytes(L.P, L.nJ_cap, L.n_cap, G) + 255) & ~(size_t)255;
+    CUDA_TRY(arena.alloc(&vbuf, xb * L.P));
+    CUDA_TRY(cudaMemsetAsync(vbuf, 0, xb * L.P, stream));
+    for (int q = 0; q < L.P; ++q) L.xbuf[q] = vbuf + q * xb;
+  }
+
+  SampleParams sp{};
+  sp.key0 = cfg->philox_key[0];
+  sp.key1 = cfg->philox_key[1];
+  sp.draw_offset = cfg->draw_offset;
+  sp.extended = extended;
+  sp.n_row_blocks = (int32_t)s;
+  sp.n_col_blocks = (int32_t)t;
+  sp.row_ptr = d_row_ptr;
+  sp.row_cum = d_row_cum;
+  sp.row_total = cfg->row_total;
+  sp.row_scale = d_row_scale;
+  sp.col_ptr = d_col_ptr;
+  sp.col_cum = d_col_cum;
+  sp.col_total = cfg->col_total;
+  sp.col_scale = d_col_scale;
+  sp.picks = d_picks;
+
+  StreamParams spar{};
+  DenseParams& p = spar.d;
+  p.A = ctx->A;
+  p.lda = ctx->lda;
+  p.m = (int32_t)ctx->m;
+  p.n = (int32_t)ctx->n;
+  p.b = b_dev;
+  p.xs = xs_dev;
+  p.x = x_dev;
+  p.z = z_dev;
+  p.upart = d_ws;
+  p.rpart = d_ws + o_rpart;
+  p.u = d_ws + o_u;
+  p.r = d_ws + o_r;
+  p.errpart = d_ws + o_err;
+  p.errs = d_errs;
+  p.errs_cap = errs_cap;
+  p.plan = d_plan;
+  p.ctl = d_ctl;
+  p.extended = extended;
+  p.stop_mode = cfg->stop_mode;
+  p.tol = cfg->tol;
+  p.stride = cfg->check_stride;
+  p.max_iters = cfg->max_iters;
+  p.res_scale = 1.0;
+  p.record = errs_cap > 0;
+  p.nonfinite_stop = cfg->nonfinite_stop;
+  spar.stages = stg.NS;
+  spar.stage_doubles = stg.SD;
+  spar.cw = stg.cw;
+  spar.ch = stg.ch;
+  spar.rw = stg.rw;
+  spar.rh = stg.rh;
+  spar.lc = stg.lc;
+  spar.lr = stg.lr;
+  spar.pad_nC = stg.pad_nC;
+  spar.pad_nR = stg.pad_nR;
+  spar.pad_nJ = stg.pad_nJ;
+  spar.pad_nI = stg.pad_nI;
+  RankXchg& X = spar.x;
+  X.P = L.P;
+  X.rank = L.rank;
+  X.vranks = L.vranks;
+  X.Gr = G;
+  int64_t base = 0;
+  for (int v = 0; v < L.vranks; ++v) {
+    X.m[v] = (int32_t)L.rows[v];
+    X.row_base[v] = (int32_t)base;
+    base += L.rows[v];
+  }
+  X.x_stride = ctx->n;
+  X.ws_stride = ws_stride;
+  X.ranges = d_ranges;
+  X.n_row_blocks = (int32_t)s;
+  X.nJ_cap = (int32_t)L.nJ_cap;
+  X.n_cap = L.n_cap;
+  X.seq_base = L.seq_base;
+  for (int q = 0; q < L.P; ++q) xchg_carve(L.xbuf[q], L.P, L.nJ_cap, L.n_cap, &X.inbox_u[q], &X.inbox_x[q], &X.flags[q]);
+
+  cudaEvent_t ev0, ev1;
+  CUDA_TRY(cudaEventCreate(&ev0));
+  CUDA_TRY(cudaEventCreate(&ev1));
+  cudaError_t err = cudaEventRecord(ev0, stream);
+  int64_t k = 1;
+  do {
+    const int64_t count = std::min(chunk, cfg->max_iters - k + 1);
+    if (err == cudaSuccess) err = launch_sample_plan(sp, k, count, d_plan, nullptr, stream);
+    for (int v = 0; v < L.vranks && err == cudaSuccess; ++v)
+      err = cudaMemsetAsync(&d_ctl[v].bar, 0, sizeof(unsigned long long), stream);
+    p.k_begin = k;
+    p.k_end = k + count - 1;
+    if (err == cudaSuccess) err = launch_shard_stream(spar, tm_c, tm_r, stg.smem_bytes, stream);
+    k += std::max<int64_t>(count, 1);
+    if (err == cudaSuccess && k <= cfg->max_iters) {
+      int32_t done = 0;
+      err = cudaMemcpyAsync(&done, &d_ctl->done, sizeof done, cudaMemcpyDeviceToHost, stream);
+      if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
+      if (done) break;
+    }
+  } while (err == cudaSuccess && k <= cfg->max_iters);
+  if (err == cudaSuccess) err = cudaEventRecord(ev1, stream);
+  std::vector<Control> ctl(L.vranks);
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(ctl.data(), d_ctl, sizeof(Control) * L.vranks, cudaMemcpyDeviceToHost, stream);
+  if (err == cudaSuccess && errs_cap > 0)
+    err = cudaMemcpyAsync(trace->errors, d_errs, errs_cap * sizeof(double), cudaMemcpyDeviceToHost, stream);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
+  float ms = 0.f;
+  if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, ev0, ev1);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  if (err != cudaSuccess) return fail(REBK_ECUDA, "row-sharded REBK run failed: %s", cudaGetErrorString(err));
+  for (int v = 0; v < L.vranks; ++v)
+    if (ctl[v].fault)
+      return fail(REBK_ECUDA, "row-sharded run: a cross-rank exchange timed out (a peer rank never arrived)");
+  for (int v = 1; v < L.vranks; ++v)
+    if (ctl[v].iters != ctl[0].iters || ctl[v].converged != ctl[0].converged)
+      return fail(REBK_ECUDA, "row-sharded run: ranks stopped at different iterations (%lld vs %lld)",
+                  (long long)ctl[v].iters, (long long)ctl[0].iters);
+  if (trace) {
+    trace->iters = ctl[0].iters;
+    trace->converged = ctl[0].converged;
+    trace->has_error = ctl[0].has_error;
+    trace->final_error = ctl[0].final_error;
+    trace->loop_ms = ms;
+    trace->n_checks = ctl[0].n_checks;
+    trace->grid_ctas = G;
+    trace->kernel_path = 9;
+    trace->nonfinite_at = ctl[0].nonfinite_at - 1;
+  }
+  L.seq_base += (unsigned long long)ctl[0].iters;  // exchanges this solve completed
+  if (ctl[0].nonfinite_at && cfg->nonfinite_stop)
+    return fail(REBK_ENONFINITE, "non-finite error at the check of iteration %lld", (long long)(ctl[0].nonfinite_at - 1));
+  return REBK_OK;
+}
+
 }  // namespace
 
 namespace rebk {
@@ -1618,6 +1894,135 @@ int rebk_shard_err2(int64_t n, const double* x_dev, const double* xs_dev, double
   if (n < 1 || !x_dev || !xs_dev || !out_dev) return fail(REBK_EINVAL, "rebk_shard_err2: bad argument");
   CUDA_TRY(shard_err(n, x_dev, xs_dev, out_dev, (cudaStream_t)stream));
   return REBK_OK;
+}
+
+/* ---- row-sharded multi-GPU path with the in-kernel exchange -------------- */
+struct rebk_shard_xchg {
+  int device = 0, P = 1, rank = 0, Gr = 0;
+  int64_t nJ_cap = 0, n_cap = 0;
+  char* buf = nullptr;  // this rank's exchange buffer (cudaMalloc: exportable by CUDA IPC)
+  size_t bytes = 0;
+  char* peer[kMaxRanks] = {};  // every rank's buffer mapped into this process (peer[rank] = buf)
+  bool opened[kMaxRanks] = {};
+  unsigned long long seq_base = 0;  // exchanges completed by earlier solves (identical on every rank)
+  std::mutex mu;                    // one solve at a time per exchange object
+};
+
+int rebk_shard_grid_ctas(int device, int* grid_ctas) {
+  if (!grid_ctas) return fail(REBK_EINVAL, "null argument");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) return fail(REBK_ENODEV, "no CUDA device");
+  if (device < 0 || device >= n) return fail(REBK_EINVAL, "device %d out of range", device);
+  int sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  *grid_ctas = sms;  // one CTA per SM (the kernel's shared-memory ring takes the SM)
+  return REBK_OK;
+}
+
+int rebk_shard_xchg_create(int nranks, int rank, int64_t nJ_cap, int64_t n_cap, int grid_ctas, int device,
+                           rebk_shard_xchg** out) {
+  if (!out || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || nJ_cap < 1 || n_cap < 1 ||
+      grid_ctas < 1)
+    return fail(REBK_EINVAL, "rebk_shard_xchg_create: bad argument (at most %d ranks)", kMaxRanks);
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) return fail(REBK_ENODEV, "no CUDA device");
+  CUDA_TRY(cudaSetDevice(device));
+  rebk_shard_xchg* x = new rebk_shard_xchg();
+  x->device = device;
+  x->P = nranks;
+  x->rank = rank;
+  x->Gr = grid_ctas;
+  x->nJ_cap = (nJ_cap + 1) & ~(int64_t)1;
+  x->n_cap = (n_cap + 1) & ~(int64_t)1;
+  x->bytes = xchg_bytes(nranks, x->nJ_cap, x->n_cap, grid_ctas);
+  cudaError_t e = cudaMalloc(&x->buf, x->bytes);
+  if (e == cudaSuccess) e = cudaMemset(x->buf, 0, x->bytes);
+  if (e != cudaSuccess) {
+    cudaFree(x->buf);
+    delete x;
+    return fail(REBK_ENOMEM, "exchange buffer: %s", cudaGetErrorString(e));
+  }
+  x->peer[rank] = x->buf;
+  *out = x;
+  return REBK_OK;
+}
+
+int rebk_shard_xchg_ipc_handle(rebk_shard_xchg* x, unsigned char handle_out[64]) {
+  if (!x || !handle_out) return fail(REBK_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(x->device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, x->buf));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle_out, &h, 64);
+  return REBK_OK;
+}
+
+int rebk_shard_xchg_open_peers(rebk_shard_xchg* x, const unsigned char* handles) {
+  if (!x || !handles) return fail(REBK_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(x->device));
+  for (int q = 0; q < x->P; ++q) {
+    if (q == x->rank || x->opened[q]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + 64 * q, 64);
+    void* ptr = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    x->peer[q] = (char*)ptr;
+    x->opened[q] = true;
+  }
+  return REBK_OK;
+}
+
+int rebk_shard_xchg_destroy(rebk_shard_xchg* x) {
+  if (!x) return REBK_OK;
+  cudaSetDevice(x->device);
+  for (int q = 0; q < x->P; ++q)
+    if (x->opened[q]) cudaIpcCloseMemHandle(x->peer[q]);
+  cudaFree(x->buf);
+  delete x;
+  return REBK_OK;
+}
+
+int rebk_shard_run_device(rebk_ctx* ctx, rebk_shard_xchg* x, const rebk_cfg* cfg, const int64_t* local_ranges,
+                          const double* b_dev, const double* x_star_dev, double* x_io_dev, double* z_io_dev,
+                          void* stream, rebk_trace* trace) {
+  if (!ctx || !x || !cfg || !local_ranges) return fail(REBK_EINVAL, "null argument");
+  for (int q = 0; q < x->P; ++q)
+    if (!x->peer[q]) return fail(REBK_EINVAL, "rank %d's exchange buffer is not mapped (rebk_shard_xchg_open_peers)", q);
+  if (ctx->device != x->device) return fail(REBK_EINVAL, "ctx and exchange buffer live on different devices");
+  std::lock_guard<std::mutex> lock(x->mu);
+  ShardLaunch L;
+  L.vranks = 1;
+  L.P = x->P;
+  L.rank = x->rank;
+  L.Gr = x->Gr;
+  const int64_t rows = ctx->m;
+  L.rows = &rows;
+  L.ranges = local_ranges;
+  for (int q = 0; q < x->P; ++q) L.xbuf[q] = x->peer[q];
+  L.nJ_cap = x->nJ_cap;
+  L.n_cap = x->n_cap;
+  L.seq_base = x->seq_base;
+  const int rc = shard_stream_impl(ctx, cfg, L, b_dev, x_star_dev, x_io_dev, z_io_dev, (cudaStream_t)stream, trace);
+  if (rc == REBK_OK || rc == REBK_ENONFINITE) x->seq_base = L.seq_base;
+  return rc;
+}
+
+int rebk_shard_run_virtual(rebk_ctx* ctx, int vranks, const int64_t* rows_per_rank, const int64_t* local_ranges,
+                           const rebk_cfg* cfg, const double* b_dev, const double* x_star_dev, double* x_io_dev,
+                           double* z_io_dev, void* stream, rebk_trace* trace) {
+  if (!ctx || !cfg || !rows_per_rank || !local_ranges) return fail(REBK_EINVAL, "null argument");
+  if (vranks < 1 || vranks > kMaxRanks) return fail(REBK_EINVAL, "1..%d virtual ranks", kMaxRanks);
+  ShardLaunch L;
+  L.vranks = vranks;
+  L.P = vranks;
+  L.rank = 0;
+  int G = cfg->grid_ctas > 0 ? cfg->grid_ctas : ctx->sm_count;
+  L.Gr = std::max(1, G / vranks);
+  L.rows = rows_per_rank;
+  L.ranges = local_ranges;
+  L.nJ_cap = std::max<int64_t>(2, (cfg->n_col_blocks > 0 && cfg->col_ptr) ? (max_block(cfg->n_col_blocks, cfg->col_ptr) + 1) & ~1 : 2);
+  L.n_cap = (ctx->n + 1) & ~(int64_t)1;
+  return shard_stream_impl(ctx, cfg, L, b_dev, x_star_dev, x_io_dev, z_io_dev, (cudaStream_t)stream, trace);
 }
 
 int rebk_ctx_destroy(rebk_ctx* ctx) {

@@ -17,6 +17,16 @@
 //   R2  the same again       (x -= s_I A_Iᵀ r, column sums)      L2  (80 MB, just read by R1)
 // so the column block is read twice: the HBM floor is ~1.68 GB per C3
 // iteration, 0.52 of the "blocks read once" algorithmic figure.
+//
+// The same body, instantiated with SH = true, is the row-sharded kernel of
+// the multi-GPU path (rebk_shard_stream_kernel): each rank
+// streams only its interleaved rows; after the local u sum the |J| values go
+// to every rank's inbox (peer memory), and R2's column partials of x go the
+// same way, CTA g to CTA g (the x column split is identical on every rank),
+// each followed by a flag store with release semantics at system scope.
+// Every rank then sums the P partials in rank order: no host round trip, no
+// launch per iteration, x bitwise replicated so every rank stops at the
+// same check.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -37,20 +47,57 @@ struct Cursor {
   int i;
 };
 
-__global__ void __launch_bounds__(kStreamThreads, 1)
-    rebk_dense_stream_kernel(const __grid_constant__ StreamParams sp, const __grid_constant__ CUtensorMap tm_c,
-                             const __grid_constant__ CUtensorMap tm_r) {
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// a peer that never arrives (a rank that failed or was killed) must not hang
+// the others forever: every cross-rank wait, and the rank-local barrier of the
+// sharded kernel, gives up after this long and the run fails with an error
+constexpr unsigned long long kXchgTimeoutNs = 60ull * 1000ull * 1000ull * 1000ull;
+
+template <bool SH>
+__device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtensorMap& tm_c, const CUtensorMap& tm_r) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t sbar[kStreamMaxStages];
   __shared__ double s_bcast[2];
 
   const DenseParams& p = sp.d;
-  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const RankXchg& X = sp.x;
+  // (virtual) rank of this CTA and its share of the launch
+  const int vr = SH ? (int)blockIdx.x / X.Gr : 0;
+  const int G = SH ? X.Gr : (int)gridDim.x;
+  const int g = SH ? (int)blockIdx.x - vr * X.Gr : (int)blockIdx.x;
+  const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  Control* ctl = p.ctl;
+  const int P = SH ? X.P : 1;
+  const int rank = SH ? (X.vranks > 1 ? vr : X.rank) : 0;
+  const int m_loc = SH ? X.m[vr] : p.m;
+  const int rbase = SH ? X.row_base[vr] : 0;
+  const int64_t wso = SH ? (int64_t)vr * X.ws_stride : 0;
+  const double* gb = p.b + rbase;
+  double* gz = p.z ? p.z + rbase : nullptr;
+  double* gx = p.x + (SH ? (int64_t)vr * X.x_stride : 0);
+  double* upart = p.upart + wso;
+  double* rpart = p.rpart + wso;
+  double* gu = p.u + wso;
+  double* gr = p.r + wso;
+  double* errpart = p.errpart + wso;
+  const int64_t* lrange = SH ? X.ranges + (int64_t)vr * 2 * X.n_row_blocks : nullptr;
+  Control* ctl = p.ctl + vr;
   if (*((volatile int32_t*)&ctl->done)) return;
 
-  const int zr0 = split_rows(p.m, G, g), zr1 = split_rows(p.m, G, g + 1);
+  const int zr0 = split_rows(m_loc, G, g), zr1 = split_rows(m_loc, G, g + 1);
   const int xq0 = split_even(p.n, G, g), xq1 = split_even(p.n, G, g + 1);
   const int nR = zr1 - zr0, nC = xq1 - xq0;
   const int NS = sp.stages, SD = sp.stage_doubles;
@@ -64,11 +111,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   double* s_red = s_r + sp.pad_nI;  // 2 * kStreamThreads
 
   for (int c = tid; c < nC; c += kStreamThreads) {
-    s_x[c] = __ldcg(p.x + xq0 + c);
+    s_x[c] = __ldcg(gx + xq0 + c);
     s_xs[c] = p.xs ? __ldg(p.xs + xq0 + c) : 0.0;
   }
   if (p.extended)
-    for (int r = tid; r < nR; r += kStreamThreads) s_z[r] = __ldcg(p.z + zr0 + r);
+    for (int r = tid; r < nR; r += kStreamThreads) s_z[r] = __ldcg(gz + zr0 + r);
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&sbar[s], 1);
     fence_mbar_init();
@@ -78,13 +125,38 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   __syncthreads();
 
   unsigned long long bar_target = 0;
+  __shared__ int s_abort;  // SH: a cross-rank wait timed out (here or in another CTA of the rank)
+  if (SH && tid == 0) s_abort = 0;
   auto gsync = [&]() {
     bar_target += (unsigned long long)G;
-    grid_barrier(&ctl->bar, bar_target);
+    if (!SH) {
+      grid_barrier(&ctl->bar, bar_target);
+      return;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&ctl->bar) : "memory");
+      const unsigned long long t0 = globaltimer_ns();
+      unsigned long long v;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&ctl->bar) : "memory");
+        if (v >= bar_target) break;
+        if (*((volatile int32_t*)&ctl->fault) || globaltimer_ns() - t0 > kXchgTimeoutNs) {
+          atomicExch(&ctl->fault, 2);
+          s_abort = 1;
+          break;
+        }
+      }
+    }
+    __syncthreads();
   };
 
   // ---- the box sequence (identical walk on the producer and consumer side)
   auto plan_of = [&](int64_t k) -> const Plan& { return p.plan[k - p.k_begin]; };
+  // this rank's rows of the iteration's row block (sharded: its interleaved
+  // share, from the rank's range table; else the plan's global range)
+  auto r_lo = [&](const Plan& pl) -> int { return SH ? (int)lrange[2 * pl.rb] : pl.r_lo; };
+  auto r_hi = [&](const Plan& pl) -> int { return SH ? (int)lrange[2 * pl.rb + 1] : pl.r_hi; };
   auto cdiv = [](int a, int b) { return (a + b - 1) / b; };
   // TMA box columns start 16-byte aligned: a column block that starts on an
   // odd column is loaded from the even column before it (span = nJ + 1, the
@@ -97,7 +169,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       return cdiv(span_c(pl), cw) * cdiv(nR, ch);
     }
     if (nC <= 0) return 0;
-    return cdiv(pl.r_hi - pl.r_lo, rh) * cdiv(nC, rw);
+    return cdiv(r_hi(pl) - r_lo(pl), rh) * cdiv(nC, rw);
   };
   // skip empty phases; k > k_end means the walk is over
   auto settle = [&](Cursor& c) {
@@ -120,14 +192,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       const int s = c.ph == 0 ? c.i / nrc : c.i % nsc;
       const int rc = c.ph == 0 ? c.i % nrc : c.i / nsc;
       mbar_arrive_expect_tx(&sbar[stage], (uint32_t)(cw * ch * 8));
-      tma_load_2d(dst, &tm_c, (pl.c_lo & ~1) + s * cw, zr0 + rc * ch, &sbar[stage]);
+      tma_load_2d(dst, &tm_c, (pl.c_lo & ~1) + s * cw, rbase + zr0 + rc * ch, &sbar[stage]);
     } else {
-      const int nsr = cdiv(nC, rw), nrr = cdiv(pl.r_hi - pl.r_lo, rh);
+      const int nsr = cdiv(nC, rw), nrr = cdiv(r_hi(pl) - r_lo(pl), rh);
       // R1 row-chunk-major (row dots), R2 subtile-major (column sums)
       const int s = c.ph == 2 ? c.i % nsr : c.i / nrr;
       const int rr = c.ph == 2 ? c.i / nsr : c.i % nrr;
       mbar_arrive_expect_tx(&sbar[stage], (uint32_t)(rw * rh * 8));
-      tma_load_2d(dst, &tm_r, xq0 + s * rw, pl.r_lo + rr * rh, &sbar[stage]);
+      tma_load_2d(dst, &tm_r, xq0 + s * rw, rbase + r_lo(pl) + rr * rh, &sbar[stage]);
     }
   };
   Cursor prod{p.k_begin, 0, 0};
@@ -160,19 +232,52 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       acc = fma(d, d, acc);
     }
     const double s = block_sum<kStreamThreads>(acc, s_red);
-    if (tid == 0) __stcg(p.errpart + g, s);
+    if (tid == 0) __stcg(errpart + g, s);
   };
   auto decide = [&](int64_t k) -> bool {
     if (warp == 0) {
-      const double s = warp_sum_cg(p.errpart, G);
+      const double s = warp_sum_cg(errpart, G);
       if (lane == 0) s_bcast[0] = s;
     }
     __syncthreads();
     const double err = sqrt(s_bcast[0]);
     const bool conv = check_stops(err, p.tol, p.nonfinite_stop);
-    if (g == 0 && tid == 0) record_check(ctl, p.errs, p.errs_cap, p.record, err, p.tol, p.nonfinite_stop, k);
+    if (g == 0 && tid == 0 && (!SH || vr == 0))
+      record_check(ctl, p.errs, p.errs_cap, p.record, err, p.tol, p.nonfinite_stop, k);
+    else if (SH && g == 0 && tid == 0 && check_stops(err, p.tol, p.nonfinite_stop)) {
+      ctl->converged = err <= p.tol;  // the other virtual ranks: only what their CTAs read
+      ctl->iters = k;
+      ctl->done = 1;
+    }
     __syncthreads();
     return conv;
+  };
+
+  // ---- cross-rank exchange (SH): publish, then wait for every rank's flag
+  const unsigned long long seq_base = SH ? X.seq_base : 0ull;
+  auto flag_at = [&](int q, int kind, int slot, int from, int cta) -> unsigned long long* {
+    return X.flags[q] + (((int64_t)(kind * 2 + slot) * P + from) * G + cta);
+  };
+  // after this CTA's stores into the peers' inboxes: make them visible at
+  // system scope, then (CTA `cta` of this rank) raise the flag on every rank
+  auto publish = [&](int kind, int slot, int cta, unsigned long long seq) {
+    __threadfence_system();
+    __syncthreads();
+    if (tid < P) st_release_sys_u64(flag_at(tid, kind, slot, rank, cta), seq);
+  };
+  auto await_all = [&](int kind, int slot, int cta, unsigned long long seq) {
+    if (tid < P) {
+      const unsigned long long* f = flag_at(rank, kind, slot, tid, cta);
+      const unsigned long long t0 = globaltimer_ns();
+      while (ld_acquire_sys_u64(f) < seq) {
+        if (*((volatile int32_t*)&ctl->fault) || globaltimer_ns() - t0 > kXchgTimeoutNs) {
+          atomicExch(&ctl->fault, 2);
+          s_abort = 1;
+          break;
+        }
+      }
+    }
+    __syncthreads();
   };
 
   // Column sums of a box stream, subtile by subtile: out(c, Σ_r T[r][c] v[r])
@@ -281,7 +386,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   if (p.k_begin == 1 && checking) {
     oracle_partial();
     gsync();
-    if (decide(0)) finished = true;
+    if (SH && s_abort) finished = true;
+    else if (decide(0)) finished = true;
   }
   if (!finished) refill();
 
@@ -290,22 +396,31 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   int64_t k = p.k_begin;
   for (; !finished && k <= p.k_end; ++k) {
     const Plan pl = plan_of(k);
-    const int nJ = pl.c_hi - pl.c_lo, nI = pl.r_hi - pl.r_lo;
+    const int rl = r_lo(pl);
+    const int nJ = pl.c_hi - pl.c_lo, nI = r_hi(pl) - rl;
     const int co = pl.c_lo & 1, W = nJ + co;  // column span of the boxes
-    const int rl = pl.r_lo;
+    // exchange sequence number: continues across solves (seq_base = the
+    // exchanges of earlier solves), so a rank that starts the next solve
+    // early writes the other slot than the one a slow peer may still read
+    const unsigned long long seq = seq_base + (unsigned long long)k;
+    const int slot = (int)(seq & 1);
     const bool check_k = checking && (k % p.stride == 0);
     PROF(0);
     if (p.extended) {
       // C1: partial u over owned rows -> upart[e * G + g]
       if (nR > 0)
         colsum_stream(W, nR, cw, ch, s_z, [&](int c, double val) {
-          if (c >= co) __stcg(p.upart + (int64_t)(c - co) * G + g, val);
+          if (c >= co) __stcg(upart + (int64_t)(c - co) * G + g, val);
         });
       else
-        for (int c = tid; c < nJ; c += kStreamThreads) __stcg(p.upart + (int64_t)c * G + g, 0.0);
+        for (int c = tid; c < nJ; c += kStreamThreads) __stcg(upart + (int64_t)c * G + g, 0.0);
       PROF(1);
       gsync();
       PROF(2);
+      if (SH && s_abort) {
+        finished = true;
+        break;
+      }
       if (pending) {
         pending = false;
         if (decide(pending_k)) {
@@ -314,32 +429,64 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
         }
       }
       for (int e = g * kStreamWarps + warp; e < nJ; e += G * kStreamWarps) {
-        const double s = warp_sum_cg(p.upart + (int64_t)e * G, G);
-        if (lane == 0) __stcg(p.u + e, s);
+        const double s = warp_sum_cg(upart + (int64_t)e * G, G);
+        if (lane == 0) {
+          if (SH) {
+            for (int q = 0; q < P; ++q) __stcg(X.inbox_u[q] + ((int64_t)slot * P + rank) * X.nJ_cap + e, s);
+          } else {
+            __stcg(gu + e, s);
+          }
+        }
       }
       PROF(3);
+      if (SH) __threadfence_system();  // this CTA's inbox stores, before the rank-local barrier
       gsync();
+      if (SH) {
+        // the rank's u partial is complete in every inbox: CTA 0 raises the
+        // flag, everyone waits for all P ranks', then sums in rank order
+        if (g == 0 && tid < P && !s_abort) st_release_sys_u64(flag_at(tid, 0, slot, rank, 0), seq);
+        await_all(0, slot, 0, seq);
+        if (s_abort) {
+          finished = true;
+          break;
+        }
+      }
       PROF(4);
       // C2: z[zr] -= s_J · A[zr, J] u
-      for (int c = tid; c < W; c += kStreamThreads) s_u[c] = c < co ? 0.0 : __ldcg(p.u + c - co);
+      for (int c = tid; c < W; c += kStreamThreads) {
+        double uc = 0.0;
+        if (c >= co) {
+          if (SH) {
+            const double* ib = X.inbox_u[rank] + (int64_t)slot * P * X.nJ_cap + (c - co);
+            for (int q = 0; q < P; ++q) uc += __ldcg(ib + (int64_t)q * X.nJ_cap);
+          } else {
+            uc = __ldcg(gu + c - co);
+          }
+        }
+        s_u[c] = uc;
+      }
       __syncthreads();
       const double cs = pl.c_scale;
       if (nR > 0)
         rowdot_stream(W, nR, cw, ch, sp.lc, s_u, [&](int r, double acc) {
           const double zn = s_z[r] - cs * acc;
           s_z[r] = zn;
-          __stcg(p.z + zr0 + r, zn);
+          __stcg(gz + zr0 + r, zn);
         });
       PROF(5);
     }
     // R1: partial r over owned columns -> rpart[e * G + g]
     if (nC > 0)
-      rowdot_stream(nC, nI, rw, rh, sp.lr, s_x, [&](int r, double acc) { __stcg(p.rpart + (int64_t)r * G + g, acc); });
+      rowdot_stream(nC, nI, rw, rh, sp.lr, s_x, [&](int r, double acc) { __stcg(rpart + (int64_t)r * G + g, acc); });
     else
-      for (int r = tid; r < nI; r += kStreamThreads) __stcg(p.rpart + (int64_t)r * G + g, 0.0);
+      for (int r = tid; r < nI; r += kStreamThreads) __stcg(rpart + (int64_t)r * G + g, 0.0);
     PROF(6);
     gsync();
     PROF(7);
+    if (SH && s_abort) {
+      finished = true;
+      break;
+    }
     if (!p.extended && pending) {
       pending = false;
       if (decide(pending_k)) {
@@ -348,21 +495,52 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
       }
     }
     for (int e = g * kStreamWarps + warp; e < nI; e += G * kStreamWarps) {
-      const double s = warp_sum_cg(p.rpart + (int64_t)e * G, G);
+      const double s = warp_sum_cg(rpart + (int64_t)e * G, G);
       if (lane == 0) {
-        double rv = s - __ldg(p.b + rl + e);
-        if (p.extended) rv += __ldcg(p.z + rl + e);
-        __stcg(p.r + e, rv);
+        double rv = s - __ldg(gb + rl + e);
+        if (p.extended) rv += __ldcg(gz + rl + e);
+        __stcg(gr + e, rv);
       }
     }
     PROF(8);
     gsync();
     PROF(9);
+    if (SH && s_abort) {
+      finished = true;
+      break;
+    }
     // R2: x[xq] -= s_I · A[I, xq]ᵀ r
-    for (int c = tid; c < nI; c += kStreamThreads) s_r[c] = __ldcg(p.r + c);
+    for (int c = tid; c < nI; c += kStreamThreads) s_r[c] = __ldcg(gr + c);
     __syncthreads();
     const double rs = pl.r_scale;
-    if (nC > 0) colsum_stream(nC, nI, rw, rh, s_r, [&](int c, double acc) { s_x[c] = s_x[c] - rs * acc; });
+    if (!SH) {
+      if (nC > 0) colsum_stream(nC, nI, rw, rh, s_r, [&](int c, double acc) { s_x[c] = s_x[c] - rs * acc; });
+    } else {
+      // this rank's column partials of A[I_p, xq]ᵀ r_p go to CTA g of every
+      // rank (same column slice everywhere); then sum over ranks in order
+      if (nC > 0) {
+        if (nI > 0) {
+          colsum_stream(nC, nI, rw, rh, s_r, [&](int c, double acc) {
+            for (int q = 0; q < P; ++q) __stcg(X.inbox_x[q] + ((int64_t)slot * P + rank) * X.n_cap + xq0 + c, acc);
+          });
+        } else {
+          for (int c = tid; c < nC; c += kStreamThreads)
+            for (int q = 0; q < P; ++q) __stcg(X.inbox_x[q] + ((int64_t)slot * P + rank) * X.n_cap + xq0 + c, 0.0);
+        }
+      }
+      publish(1, slot, g, seq);
+      await_all(1, slot, g, seq);
+      if (s_abort) {
+        finished = true;
+        break;
+      }
+      const double* ib = X.inbox_x[rank] + (int64_t)slot * P * X.n_cap + xq0;
+      for (int c = tid; c < nC; c += kStreamThreads) {
+        double acc = 0.0;
+        for (int q = 0; q < P; ++q) acc += __ldcg(ib + (int64_t)q * X.n_cap + c);
+        s_x[c] = s_x[c] - rs * acc;
+      }
+    }
     __syncthreads();
     PROF(10);
     if (check_k) {
@@ -391,15 +569,27 @@ __global__ void __launch_bounds__(kStreamThreads, 1)
   if (p.prof && tid == 0)
     for (int i = 0; i < 16; ++i) p.prof[g * 16 + i] = prof_acc[i];
 #undef PROF
-  for (int c = tid; c < nC; c += kStreamThreads) __stcg(p.x + xq0 + c, s_x[c]);
+  for (int c = tid; c < nC; c += kStreamThreads) __stcg(gx + xq0 + c, s_x[c]);
   if (p.extended)
-    for (int r = tid; r < nR; r += kStreamThreads) __stcg(p.z + zr0 + r, s_z[r]);
+    for (int r = tid; r < nR; r += kStreamThreads) __stcg(gz + zr0 + r, s_z[r]);
   // boxes issued for iterations past a stop are still landing: drain them
   while (consumed < produced) {
     mbar_wait(&sbar[consumed % NS], (uint32_t)((consumed / NS) & 1));
     ++consumed;
   }
   __syncthreads();
+}
+
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    rebk_dense_stream_kernel(const __grid_constant__ StreamParams sp, const __grid_constant__ CUtensorMap tm_c,
+                             const __grid_constant__ CUtensorMap tm_r) {
+  stream_body<false>(sp, tm_c, tm_r);
+}
+
+__global__ void __launch_bounds__(kStreamThreads, 1)
+    rebk_shard_stream_kernel(const __grid_constant__ StreamParams sp, const __grid_constant__ CUtensorMap tm_c,
+                             const __grid_constant__ CUtensorMap tm_r) {
+  stream_body<true>(sp, tm_c, tm_r);
 }
 
 static cudaError_t set_stream_attrs() {
@@ -412,6 +602,8 @@ static cudaError_t set_stream_attrs() {
   e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(rebk_dense_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(rebk_shard_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024);
   if (e == cudaSuccess) configured_device = dev;
   return e;
 }
@@ -432,6 +624,20 @@ cudaError_t launch_dense_stream(const StreamParams& sp, const CUtensorMap& tm_c,
   void* args[] = {&spc, &a, &b};
   return cudaLaunchCooperativeKernel((const void*)rebk_dense_stream_kernel, dim3(G), dim3(kStreamThreads), args,
                                      smem_bytes, stream);
+}
+
+// Row-sharded launch: X.vranks * X.Gr CTAs (one rank per launch on a real
+// multi-GPU job; every emulated rank's CTAs co-resident in one cooperative
+// launch on a single GPU, so ranks that wait on each other always run together)
+cudaError_t launch_shard_stream(const StreamParams& sp, const CUtensorMap& tm_c, const CUtensorMap& tm_r,
+                                size_t smem_bytes, cudaStream_t stream) {
+  cudaError_t e = set_stream_attrs();
+  if (e != cudaSuccess) return e;
+  StreamParams spc = sp;
+  CUtensorMap a = tm_c, b = tm_r;
+  void* args[] = {&spc, &a, &b};
+  return cudaLaunchCooperativeKernel((const void*)rebk_shard_stream_kernel, dim3(sp.x.vranks * sp.x.Gr),
+                                     dim3(kStreamThreads), args, smem_bytes, stream);
 }
 
 }  // namespace rebk

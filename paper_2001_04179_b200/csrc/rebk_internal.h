@@ -122,8 +122,42 @@ struct SplitParams {
 // Streaming path for blocks too large for shared memory (rebk_dense_stream.cu):
 // every pass streams TMA boxes through a ring of `stages` shared-memory stages.
 constexpr int kStreamMaxStages = 8;
+// Cross-rank exchange of the row-sharded streaming kernel:
+// P ranks each hold interleaved rows of every row block; per iteration the
+// |J|-length column product u and the n-length x update are summed over the
+// ranks inside the persistent kernel.  Rank q's exchange buffer holds
+//   inbox_u[2 slots][P][nJ_cap]  u partials of every rank (slot = k & 1)
+//   inbox_x[2 slots][P][n_cap]   dx partials of every rank
+//   flags[2 kinds][2 slots][P][Gr] u64 sequence numbers (kind 0: u, written
+//                                  by CTA 0 of the sender; kind 1: x, written
+//                                  by CTA g of the sender for its column slice)
+// and every rank writes its partials into every rank's buffer (peer-mapped
+// device memory over NVLink on a multi-GPU job; one allocation per virtual
+// rank when `vranks` ranks are emulated in one launch on one GPU).  Every
+// rank sums the P partials in rank order, so x stays bitwise replicated.
+constexpr int kMaxRanks = 8;
+struct RankXchg {
+  int32_t P;        // ranks in the job (1: no exchange)
+  int32_t rank;     // this process's rank (when vranks == 1)
+  int32_t vranks;   // ranks emulated in this launch (1 on a real multi-GPU job)
+  int32_t Gr;       // CTAs per rank (equal on every rank: x slices line up)
+  int32_t m[kMaxRanks];         // local rows of each (virtual) rank
+  int32_t row_base[kMaxRanks];  // first row of each virtual rank in the stacked A / b / z
+  int64_t x_stride;   // doubles between virtual ranks' x arrays
+  int64_t ws_stride;  // doubles between virtual ranks' workspaces (upart .. errpart)
+  const int64_t* ranges;  // [vranks][n_row_blocks][2] local row range of each row block
+  int32_t n_row_blocks;
+  int32_t nJ_cap;
+  int64_t n_cap;
+  unsigned long long seq_base;  // per-solve epoch: sequence numbers are seq_base + k
+  double* inbox_u[kMaxRanks];
+  double* inbox_x[kMaxRanks];
+  unsigned long long* flags[kMaxRanks];
+};
+
 struct StreamParams {
   DenseParams d;
+  RankXchg x;  // row-sharded kernel only
   int32_t stages, stage_doubles;  // ring geometry (stage_doubles % 16 == 0)
   int32_t cw, ch;                 // column-block box: cw columns x ch rows
   int32_t rw, rh;                 // row-block box: rw columns x rh rows
@@ -245,6 +279,8 @@ cudaError_t launch_dense_split(const SplitParams& sp, const CUtensorMap& tm_ct, 
 cudaError_t launch_dense_stream(const StreamParams& sp, const CUtensorMap& tm_c, const CUtensorMap& tm_r, int G,
                                 size_t smem_bytes, cudaStream_t stream);
 cudaError_t stream_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
+cudaError_t launch_shard_stream(const StreamParams& sp, const CUtensorMap& tm_c, const CUtensorMap& tm_r,
+                                size_t smem_bytes, cudaStream_t stream);
 cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream);
 cudaError_t csr_kernel_occupancy(int* blocks_per_sm);
 struct MrhsRun {

@@ -396,3 +396,128 @@ def run_sharded_native(backend: CudaShardBackend, comm: NcclComm, plan: ShardPla
     del keep
     x, z = backend.state()
     return dict(iters=int(it.value), converged=bool(conv.value), final_error=float(err.value), x=x, z_local=z)
+
+
+# ---------------------------------------------------------------- persistent kernel with the in-kernel exchange
+def shard_layout(row_ptr: np.ndarray, nranks: int) -> tuple[list[np.ndarray], np.ndarray]:
+    """Every rank's global rows and its local row ranges per row block
+    ([nranks][n_row_blocks][2]), the interleaving of owned_rows."""
+    rows, ranges = zip(*(owned_rows(row_ptr, nranks, r) for r in range(nranks)))
+    return list(rows), np.ascontiguousarray(np.stack(ranges), dtype=np.int64)
+
+
+def _as_device(t, dev):
+    import torch
+
+    if isinstance(t, torch.Tensor):
+        return t.to(dev, dtype=torch.float64)
+    return torch.from_numpy(np.ascontiguousarray(t, dtype=np.float64)).to(dev)
+
+
+def run_persistent_virtual(a, b, x_star, cfg, row_ptr: np.ndarray, vranks: int, x0=None, z0=None,
+                           device: int = 0) -> dict:
+    """The row-sharded persistent kernel (rebk_shard_stream_kernel) with
+    `vranks` ranks emulated in one cooperative launch on one GPU
+    (rebk_shard_run_virtual): each emulated rank gets its interleaved rows
+    of every row block, its own x copy and its own exchange buffer, and the
+    ranks exchange u and dx partials through those buffers exactly as real
+    ranks do through peer memory.  `cfg` is the single-GPU rebk_cfg (global
+    partitions and sampler arrays).  Returns x (rank 0's copy), every rank's
+    x (bitwise replicated), z in global row order and the trace."""
+    import torch
+
+    from .matrix import DeviceMatrix
+
+    dev = torch.device("cuda", device)
+    a_d, b_d = _as_device(a, dev), _as_device(b, dev)
+    m, n = int(a_d.shape[0]), int(a_d.shape[1])
+    rows, ranges = shard_layout(row_ptr, vranks)
+    perm = torch.from_numpy(np.concatenate(rows)).to(dev)
+    a_st = a_d.index_select(0, perm).contiguous()
+    b_st = b_d.index_select(0, perm).contiguous()
+    z_st = (b_d if z0 is None else _as_device(z0, dev)).index_select(0, perm).contiguous()
+    x_all = (torch.zeros(n, dtype=torch.float64, device=dev) if x0 is None else _as_device(x0, dev)).repeat(vranks, 1)
+    xs_d = None if x_star is None else _as_device(x_star, dev)
+    rows_per = np.asarray([r.size for r in rows], dtype=np.int64)
+    dm = DeviceMatrix.from_device_pointer(a_st.data_ptr(), m, n, n, device)
+    tr = _lib.RebkTrace()
+    errs = None
+    if cfg.record_errors:
+        errs = np.zeros(max(1, cfg.max_iters // max(1, cfg.check_stride) + 2))
+        tr.errors, tr.errors_cap = _lib.dptr(errs), errs.size
+    torch.cuda.synchronize(dev)
+    try:
+        _lib.check(_lib.load().rebk_shard_run_virtual(
+            dm.handle, int(vranks), _lib.i64ptr(rows_per), _lib.i64ptr(ranges), ctypes.byref(cfg),
+            ctypes.c_void_p(b_st.data_ptr()), ctypes.c_void_p(0 if xs_d is None else xs_d.data_ptr()),
+            ctypes.c_void_p(x_all.data_ptr()), ctypes.c_void_p(z_st.data_ptr()),
+            ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream), ctypes.byref(tr)), "rebk_shard_run_virtual")
+    finally:
+        dm.close()
+    z = torch.empty_like(z_st)
+    z[perm] = z_st
+    xs_all = x_all.cpu().numpy()
+    return dict(iters=int(tr.iters), converged=bool(tr.converged), final_error=float(tr.final_error),
+                x=xs_all[0], x_all=xs_all, z=z.cpu().numpy(), loop_ms=float(tr.loop_ms), grid_ctas=int(tr.grid_ctas),
+                kernel_path=int(tr.kernel_path), errors=errs, n_checks=int(tr.n_checks))
+
+
+def exchange_ipc_handles(handle: bytes, all_gather_object) -> bytes:
+    """Every rank's 64-byte CUDA IPC handle, concatenated in rank order
+    (`all_gather_object(list, obj)` is torch.distributed's, or a stand-in)."""
+    got = [None] * _world_size(all_gather_object)
+    all_gather_object(got, bytes(handle))
+    if any(h is None or len(h) != 64 for h in got):
+        raise RuntimeError("IPC handle exchange returned a malformed handle")
+    return b"".join(got)
+
+
+def _world_size(all_gather_object):
+    ws = getattr(all_gather_object, "world_size", None)
+    if ws is not None:
+        return int(ws)
+    import torch.distributed as dist
+
+    return dist.get_world_size()
+
+
+class ShardExchange:
+    """This rank's exchange buffer for rebk_shard_run_device, with every
+    peer's buffer mapped over CUDA IPC (one process per GPU, one node).
+
+    Collective: every rank constructs it with the same nJ_cap / n; the CTAs
+    per rank are agreed as the minimum over ranks (all ranks must split x
+    identically for the CTA-to-CTA dx exchange)."""
+
+    def __init__(self, nranks: int, rank: int, nJ_cap: int, n: int, device: int, all_gather_object,
+                 lib=None):
+        self.lib = lib or _lib.load()
+        g = ctypes.c_int()
+        _lib.check(self.lib.rebk_shard_grid_ctas(device, ctypes.byref(g)), "rebk_shard_grid_ctas")
+        gs = [None] * nranks
+        all_gather_object(gs, int(g.value))
+        self.grid_ctas = int(min(gs))
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.rebk_shard_xchg_create(nranks, rank, int(nJ_cap), int(n), self.grid_ctas, device,
+                                                   ctypes.byref(h)), "rebk_shard_xchg_create")
+        self.handle = h
+        buf = ctypes.create_string_buffer(64)
+        _lib.check(self.lib.rebk_shard_xchg_ipc_handle(h, buf), "rebk_shard_xchg_ipc_handle")
+        allh = exchange_ipc_handles(buf.raw, all_gather_object)
+        _lib.check(self.lib.rebk_shard_xchg_open_peers(h, allh), "rebk_shard_xchg_open_peers")
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    def run(self, dm, cfg, ranges: np.ndarray, b_dev, xs_dev, x_dev, z_dev, stream) -> "_lib.RebkTrace":
+        """One solve of this rank's shard (all device buffers; see rebk.h)."""
+        rng = np.ascontiguousarray(ranges, dtype=np.int64)
+        tr = _lib.RebkTrace()
+        _lib.check(self.lib.rebk_shard_run_device(
+            dm.handle, self.handle, ctypes.byref(cfg), _lib.i64ptr(rng), ctypes.c_void_p(b_dev),
+            ctypes.c_void_p(xs_dev or 0), ctypes.c_void_p(x_dev), ctypes.c_void_p(z_dev or 0), ctypes.c_void_p(stream),
+            ctypes.byref(tr)), "rebk_shard_run_device")
+        return tr
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.rebk_shard_xchg_destroy(self.handle)
+            self.handle = None
