@@ -825,6 +825,7 @@ def run_ours_c3_sharded(args):
     wl = c3_device(device=local)
     m, n = wl.shape
     abytes = wl.algorithmic_bytes_per_iter
+    config = c3_config(wl)
     rows, ranges = owned_rows(wl.row_ptr, ws, rank)
     rows_t = torch.from_numpy(rows).to(dev)
     a_local = wl.a.index_select(0, rows_t).contiguous()
@@ -949,7 +950,7 @@ def run_ours_c3_sharded(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (torch Philox on device)",
-            "config": c3_config(wl),
+            "config": config,
             "details": {"parallelism": f"row-sharded x{ws} (interleaved rows of every row block)",
                         "iters_per_solve": per_solve,
                         "timing": "CUDA events around the steps on each rank's stream, max over ranks",

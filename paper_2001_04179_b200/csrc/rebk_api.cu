@@ -1396,6 +1396,14 @@ int shard_stream_impl(rebk_ctx* ctx, const rebk_cfg* cfg, ShardLaunch& L, const 
   p.res_scale = 1.0;
   p.record = errs_cap > 0;
   p.nonfinite_stop = cfg->nonfinite_stop;
+  const char* prof_env = getenv("REBK_PROF");
+  long long* d_prof = nullptr;
+  const int Gtot = L.vranks * G;
+  if (prof_env && prof_env[0] == '1') {
+    CUDA_TRY(arena.alloc(&d_prof, (size_t)Gtot * 16));
+    CUDA_TRY(cudaMemsetAsync(d_prof, 0, (size_t)Gtot * 16 * 8, stream));
+  }
+  p.prof = d_prof;
   spar.stages = stg.NS;
   spar.stage_doubles = stg.SD;
   spar.cw = stg.cw;
@@ -1464,6 +1472,16 @@ int shard_stream_impl(rebk_ctx* ctx, const rebk_cfg* cfg, ShardLaunch& L, const 
   for (int v = 0; v < L.vranks; ++v)
     if (ctl[v].fault)
       return fail(REBK_ECUDA, "row-sharded run: a cross-rank exchange timed out (a peer rank never arrived)");
+  if (d_prof) {
+    std::vector<long long> h((size_t)Gtot * 16);
+    cudaMemcpy(h.data(), d_prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, ctx->device);
+    const double it = (double)std::max<int64_t>(1, ctl[0].iters);
+    fprintf(stderr, "[rebk prof] path=shard-stream P=%d vranks=%d Gr=%d iters=%lld loop=%.3f ms (%.3f us/iter); "
+            "mark mean max\n", L.P, L.vranks, G, (long long)ctl[0].iters, ms, 1e3 * ms / it);
+    print_prof(h, Gtot, Gtot, khz, it);
+  }
   for (int v = 1; v < L.vranks; ++v)
     if (ctl[v].iters != ctl[0].iters || ctl[v].converged != ctl[0].converged)
       return fail(REBK_ECUDA, "row-sharded run: ranks stopped at different iterations (%lld vs %lld)",

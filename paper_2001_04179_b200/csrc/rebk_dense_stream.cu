@@ -528,8 +528,10 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
             for (int q = 0; q < P; ++q) __stcg(X.inbox_x[q] + ((int64_t)slot * P + rank) * X.n_cap + xq0 + c, 0.0);
         }
       }
+      PROF(11);
       publish(1, slot, g, seq);
       await_all(1, slot, g, seq);
+      PROF(12);
       if (s_abort) {
         finished = true;
         break;
@@ -567,7 +569,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
     }
   }
   if (p.prof && tid == 0)
-    for (int i = 0; i < 16; ++i) p.prof[g * 16 + i] = prof_acc[i];
+    for (int i = 0; i < 16; ++i) p.prof[(int64_t)blockIdx.x * 16 + i] = prof_acc[i];
 #undef PROF
   for (int c = tid; c < nC; c += kStreamThreads) __stcg(gx + xq0 + c, s_x[c]);
   if (p.extended)
