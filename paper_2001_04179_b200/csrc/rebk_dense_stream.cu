@@ -135,6 +135,10 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
     }
     __syncthreads();
     if (tid == 0) {
+      // cumulative over every store this CTA's threads made before the
+      // bar.sync above, including the ones into peer GPUs' inboxes: after
+      // the barrier, CTA 0's system-scope flag release covers them all
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
       asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&ctl->bar) : "memory");
       const unsigned long long t0 = globaltimer_ns();
       unsigned long long v;
@@ -258,10 +262,11 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   auto flag_at = [&](int q, int kind, int slot, int from, int cta) -> unsigned long long* {
     return X.flags[q] + (((int64_t)(kind * 2 + slot) * P + from) * G + cta);
   };
-  // after this CTA's stores into the peers' inboxes: make them visible at
-  // system scope, then (CTA `cta` of this rank) raise the flag on every rank
+  // after this CTA's stores into the peers' inboxes: the bar.sync orders
+  // every thread's stores before the flag stores, and a release at system
+  // scope is cumulative over them (PTX memory model), so the peer that
+  // acquires the flag sees the data
   auto publish = [&](int kind, int slot, int cta, unsigned long long seq) {
-    __threadfence_system();
     __syncthreads();
     if (tid < P) st_release_sys_u64(flag_at(tid, kind, slot, rank, cta), seq);
   };
@@ -439,8 +444,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
         }
       }
       PROF(3);
-      if (SH) __threadfence_system();  // this CTA's inbox stores, before the rank-local barrier
-      gsync();
+      gsync();  // SH: thread 0 fences at system scope after the bar.sync (see gsync)
       if (SH) {
         // the rank's u partial is complete in every inbox: CTA 0 raises the
         // flag, everyone waits for all P ranks', then sums in rank order
