@@ -127,18 +127,22 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   unsigned long long bar_target = 0;
   __shared__ int s_abort;  // SH: a cross-rank wait timed out (here or in another CTA of the rank)
   if (SH && tid == 0) s_abort = 0;
-  auto gsync = [&]() {
+  // SH: the barrier's arrival, the flags and every system-scope fence are
+  // done by warp 1 (thread 0 is the TMA producer: a fence there would wait
+  // for its in-flight bulk copies)
+  const int xt = tid - 32;
+  auto gsync = [&](bool sysfence = false) {
     bar_target += (unsigned long long)G;
     if (!SH) {
       grid_barrier(&ctl->bar, bar_target);
       return;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (xt == 0) {
       // cumulative over every store this CTA's threads made before the
       // bar.sync above, including the ones into peer GPUs' inboxes: after
       // the barrier, CTA 0's system-scope flag release covers them all
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      if (sysfence) asm volatile("fence.acq_rel.sys;" ::: "memory");
       asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&ctl->bar) : "memory");
       const unsigned long long t0 = globaltimer_ns();
       unsigned long long v;
@@ -268,11 +272,11 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   // acquires the flag sees the data
   auto publish = [&](int kind, int slot, int cta, unsigned long long seq) {
     __syncthreads();
-    if (tid < P) st_release_sys_u64(flag_at(tid, kind, slot, rank, cta), seq);
+    if (xt >= 0 && xt < P) st_release_sys_u64(flag_at(xt, kind, slot, rank, cta), seq);
   };
   auto await_all = [&](int kind, int slot, int cta, unsigned long long seq) {
-    if (tid < P) {
-      const unsigned long long* f = flag_at(rank, kind, slot, tid, cta);
+    if (xt >= 0 && xt < P) {
+      const unsigned long long* f = flag_at(rank, kind, slot, xt, cta);
       const unsigned long long t0 = globaltimer_ns();
       while (ld_acquire_sys_u64(f) < seq) {
         if (*((volatile int32_t*)&ctl->fault) || globaltimer_ns() - t0 > kXchgTimeoutNs) {
@@ -444,11 +448,11 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
         }
       }
       PROF(3);
-      gsync();  // SH: thread 0 fences at system scope after the bar.sync (see gsync)
+      gsync(true);  // SH: fence at system scope after the bar.sync (see gsync)
       if (SH) {
         // the rank's u partial is complete in every inbox: CTA 0 raises the
         // flag, everyone waits for all P ranks', then sums in rank order
-        if (g == 0 && tid < P && !s_abort) st_release_sys_u64(flag_at(tid, 0, slot, rank, 0), seq);
+        if (g == 0 && xt >= 0 && xt < P && !s_abort) st_release_sys_u64(flag_at(xt, 0, slot, rank, 0), seq);
         await_all(0, slot, 0, seq);
         if (s_abort) {
           finished = true;
