@@ -85,13 +85,20 @@ def test_device_beta_c1_matches_reference_jacobi():
     assert bmax == pytest.approx(float(g["beta"]), rel=BETA_RTOL)
 
 
-def test_device_beta_c2_matches_golden():
+def test_device_beta_c2_matches_reference_jacobi():
+    """C2 (4000 x 10000, blocks of 200) against the reference's OWN beta:
+    rates.compute_beta_max (one-sided Jacobi SVD of all 70 blocks, 886 s on
+    the build host; tests/golden/gen_golden.py --c2-beta)."""
     from paper_2001_04179_b200 import workloads
 
-    g = load("c2_golden.npz")
-    wl = workloads.build("c2")
-    _, _, bmax = P.device_beta_max(wl.problem.a, wl.row_partition, wl.col_partition)
-    assert bmax == pytest.approx(float(g["beta"]), rel=BETA_RTOL)
+    ref = load("c2_beta_ref.npz")
+    wl = workloads.build("c2", beta_max=1.0)
+    br, bc, bmax = P.device_beta_max(wl.problem.a, wl.row_partition, wl.col_partition)
+    assert br == pytest.approx(float(ref["beta_rows"]), rel=BETA_RTOL)
+    assert bc == pytest.approx(float(ref["beta_cols"]), rel=BETA_RTOL)
+    assert bmax == pytest.approx(float(ref["beta"]), rel=BETA_RTOL)
+    # the C2 golden run's alpha came from the host Gram eigensolver: same beta
+    assert float(load("c2_golden.npz")["beta"]) == pytest.approx(float(ref["beta"]), rel=BETA_RTOL)
 
 
 def test_prepare_resolves_beta_on_device_and_warns_like_host(monkeypatch):

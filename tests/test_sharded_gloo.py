@@ -95,3 +95,70 @@ def test_row_ownership_partitions_every_block():
                 blk = rows[ranges[bi, 0]:ranges[bi, 1]]
                 assert np.all((blk >= row_ptr[bi]) & (blk < row_ptr[bi + 1]))
         assert np.all(seen == 1)
+
+
+class _FakeXchgLib:
+    """Records the C-ABI calls ShardExchange makes (no GPU on this host): the
+    per-rank CTA count it reports, the IPC handle it exports, and the handle
+    table it is asked to open."""
+
+    def __init__(self, rank, ctas):
+        self.rank, self.ctas = rank, ctas
+        self.created = None
+        self.opened = None
+
+    def rebk_shard_grid_ctas(self, device, out):
+        out._obj.value = self.ctas
+        return 0
+
+    def rebk_shard_xchg_create(self, P, rank, nJ, n, G, device, out):
+        self.created = (P, rank, nJ, n, G, device)
+        out._obj.value = 1000 + rank
+        return 0
+
+    def rebk_shard_xchg_ipc_handle(self, h, buf):
+        buf.raw = bytes([self.rank]) * 64
+        return 0
+
+    def rebk_shard_xchg_open_peers(self, h, handles):
+        self.opened = bytes(handles)
+        return 0
+
+    def rebk_shard_xchg_destroy(self, h):
+        return 0
+
+
+def _xchg_rank_main(rank, world, port, out_dir):
+    import torch.distributed as dist
+
+    from paper_2001_04179_b200.sharded import ShardExchange
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lib = _FakeXchgLib(rank, ctas=148 - 3 * rank)  # ranks report different CTA counts
+    x = ShardExchange(world, rank, 500, 10000, rank, dist.all_gather_object, lib=lib)
+    np.savez(os.path.join(out_dir, f"x{rank}.npz"), created=np.asarray(lib.created),
+             opened=np.frombuffer(lib.opened, dtype=np.uint8), grid=x.grid_ctas)
+    x.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_exchange_setup_agrees_across_ranks(world):
+    """The multi-GPU setup of the in-kernel exchange (sharded.ShardExchange)
+    over gloo: every rank agrees on the minimum CTA count (the dx exchange
+    pairs CTA g with CTA g, so the x split must match), creates its buffer
+    with its own rank, and receives every rank's IPC handle in rank order."""
+    import torch.multiprocessing as mp
+
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_xchg_rank_main, args=(world, free_port(), d), nprocs=world, join=True)
+        outs = [np.load(os.path.join(d, f"x{r}.npz")) for r in range(world)]
+    want_g = 148 - 3 * (world - 1)
+    want_handles = b"".join(bytes([r]) * 64 for r in range(world))
+    for r, o in enumerate(outs):
+        assert int(o["grid"]) == want_g
+        assert o["created"].tolist() == [world, r, 500, 10000, want_g, r]
+        assert o["opened"].tobytes() == want_handles
