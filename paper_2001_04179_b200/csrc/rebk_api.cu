@@ -1847,6 +1847,9 @@ int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float*
           trace->n_checks = 0;
           trace->grid_ctas = 0;
           trace->kernel_path = math == 6 ? 8 : (math == 4 ? 5 : 4);
+          trace->nonfinite_at = -1;
+          for (int64_t c = 0; c < R; ++c)
+            if (!(er[c] - er[c] == 0.0)) trace->nonfinite_at = K;  // per-column errors at the stop: NaN/Inf
         }
       }
     }
@@ -2077,12 +2080,14 @@ int rebk_ctx_shape(const rebk_ctx* ctx, int64_t* m, int64_t* n) {
 int rebk_run_device(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* x_star_dev,
                     double* x_io_dev, double* z_io_dev, void* stream, rebk_trace* trace) {
   if (!ctx || !cfg) return fail(REBK_EINVAL, "null ctx/cfg");
+  if (trace) trace->nonfinite_at = -1;
   return run_device_impl(ctx, cfg, b_dev, x_star_dev, x_io_dev, z_io_dev, (cudaStream_t)stream, trace);
 }
 
 int rebk_run(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b, const double* x0, const double* z0,
              const double* x_star, double* x_out, double* z_out, rebk_trace* trace) {
   if (!ctx || !cfg || !b || !x_out) return fail(REBK_EINVAL, "null argument");
+  if (trace) trace->nonfinite_at = -1;
   if (cfg->stop_mode == REBK_STOP_ORACLE_ERROR && !x_star)
     return fail(REBK_EINVAL, "oracle_error stopping needs a problem with x_star");
   const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;

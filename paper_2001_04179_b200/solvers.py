@@ -105,7 +105,11 @@ class RunTrace:
     x: np.ndarray | None = None
     z: np.ndarray | None = None
     grid_ctas: int = 0
-    kernel_path: int = 0  # 0 general kernel, 1/2 clustered fast path (2: cooperative launch)
+    kernel_path: int = 0  # rebk_trace.kernel_path (include/rebk.h)
+    # first check whose error was NaN/Inf (None: none).  The reference has no
+    # finiteness check in run() and keeps iterating to max_iters; so does
+    # this path (rebk_cfg.nonfinite_stop = 0), it only reports where
+    nonfinite_at: int | None = None
 
 
 def _block_beta(a: Matrix, p: Partition) -> float:
@@ -472,6 +476,7 @@ def run(problem: ProblemInstance, config: SolverConfig) -> RunTrace:
         x=x,
         z=z,
         grid_ctas=int(tr.grid_ctas),
+        nonfinite_at=None if int(tr.nonfinite_at) < 0 else int(tr.nonfinite_at),
         kernel_path=int(tr.kernel_path),
     )
 
