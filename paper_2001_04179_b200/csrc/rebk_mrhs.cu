@@ -249,7 +249,8 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
   // outputs (R x |J|, R x |I|), so one GEMM would occupy a handful of SMs;
   // batch them over K chunks and sum the partials in a fixed order.
   const int64_t kc_m = 2048, kc_n = 512;
-  const int64_t nb_m = std::max<int64_t>(1, m / kc_m), nb_n = std::max<int64_t>(1, n / kc_n);
+  // full K chunks (possibly none: a dimension shorter than one chunk is all remainder)
+  const int64_t nb_m = m / kc_m, nb_n = n / kc_n;
   float* P;
   const int64_t plen = std::max<int64_t>((int64_t)nJmax * R * (nb_m + 1), (int64_t)nImax * R * (nb_n + 1));
   MR_TRY(cudaMallocAsync((void**)&P, sizeof(float) * plen, stream));
@@ -267,8 +268,9 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
       const float mcs = (float)(-pl.c_scale);
       // U = Σ_chunks Z_chunkᵀ-rows x A_J chunk (split over m), then the z update
       const int64_t ulen = (int64_t)nJ * R;
-      MB_TRY(cb.sgemm_sb(h, CUBLAS_OP_N, CUBLAS_OP_T, R, nJ, (int)kc_m, &one, w.Z, R, kc_m * R, w.A + pl.c_lo,
-                         (int)lda, kc_m * lda, &zero, P, R, ulen, (int)nb_m));
+      if (nb_m > 0)
+        MB_TRY(cb.sgemm_sb(h, CUBLAS_OP_N, CUBLAS_OP_T, R, nJ, (int)kc_m, &one, w.Z, R, kc_m * R, w.A + pl.c_lo,
+                           (int)lda, kc_m * lda, &zero, P, R, ulen, (int)nb_m));
       const int64_t rem = m - nb_m * kc_m;
       if (rem > 0)
         MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, R, nJ, (int)rem, &one, w.Z + nb_m * kc_m * R, R,
@@ -286,8 +288,9 @@ int run_mrhs(const MrhsRun& w, const SampleParams& sp_template, const SamplePara
     const float mrs = (float)(-pl.r_scale);
     {
       // Rr += Σ_chunks X_chunk x A_I chunk (split over n)
-      MB_TRY(cb.sgemm_sb(h, CUBLAS_OP_N, CUBLAS_OP_N, R, nI, (int)kc_n, &one, w.X, R, kc_n * R, AI, (int)lda, kc_n,
-                         &zero, P, R, cnt, (int)nb_n));
+      if (nb_n > 0)
+        MB_TRY(cb.sgemm_sb(h, CUBLAS_OP_N, CUBLAS_OP_N, R, nI, (int)kc_n, &one, w.X, R, kc_n * R, AI, (int)lda, kc_n,
+                           &zero, P, R, cnt, (int)nb_n));
       const int64_t rem = n - nb_n * kc_n;
       if (rem > 0)
         MB_TRY(cb.sgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, R, nI, (int)rem, &one, w.X + nb_n * kc_n * R, R,
