@@ -1128,6 +1128,8 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
         spar.pad_nR = stg.pad_nR;
         spar.pad_nJ = stg.pad_nJ;
         spar.pad_nI = stg.pad_nI;
+        spar.l2hint = env_int("REBK_STREAM_L2HINT", 1);
+        spar.reverse = env_int("REBK_STREAM_REV", 1);
         err = launch_dense_stream(spar, tm_sc, tm_sr, G, stg.smem_bytes, stream);
       } else {
         err = launch_dense(p, G, geo.smem_bytes, stream);
@@ -1416,6 +1418,8 @@ int shard_stream_impl(rebk_ctx* ctx, const rebk_cfg* cfg, ShardLaunch& L, const 
   spar.pad_nR = stg.pad_nR;
   spar.pad_nJ = stg.pad_nJ;
   spar.pad_nI = stg.pad_nI;
+  spar.l2hint = env_int("REBK_STREAM_L2HINT", 1);
+  spar.reverse = env_int("REBK_STREAM_REV", 1);
   RankXchg& X = spar.x;
   X.P = L.P;
   X.rank = L.rank;

@@ -189,6 +189,15 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
       }
     }
   };
+  // L2 policy per pass: R1 -> evict_last (R2 reads the same 80 MB right
+  // after), the column passes and R2 -> evict_first (each byte is read once
+  // in the pass; keeping it would push R1's lines out before R2)
+  const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
+  const int l2hint = sp.l2hint;
+  // second passes (C2, R2) walk their row chunks last-to-first: the boxes the
+  // first pass read most recently are the ones still in L2 (an LRU cache
+  // re-read in the same order would miss on all of them)
+  const bool rev = sp.reverse != 0;
   auto issue = [&](const Cursor& c, int stage) {  // thread 0
     const Plan& pl = plan_of(c.k);
     fence_proxy_async();
@@ -198,16 +207,25 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
       // C1 walks subtile-major (column sums accumulate down the rows),
       // C2 row-chunk-major (row dots accumulate across the subtiles)
       const int s = c.ph == 0 ? c.i / nrc : c.i % nsc;
-      const int rc = c.ph == 0 ? c.i % nrc : c.i / nsc;
+      int rc = c.ph == 0 ? c.i % nrc : c.i / nsc;
+      if (c.ph == 1 && rev) rc = nrc - 1 - rc;  // C2 from the rows C1 read last (still in L2)
       mbar_arrive_expect_tx(&sbar[stage], (uint32_t)(cw * ch * 8));
-      tma_load_2d(dst, &tm_c, (pl.c_lo & ~1) + s * cw, rbase + zr0 + rc * ch, &sbar[stage]);
+      if (l2hint)
+        tma_load_2d_hint(dst, &tm_c, (pl.c_lo & ~1) + s * cw, rbase + zr0 + rc * ch, &sbar[stage], pol_first);
+      else
+        tma_load_2d(dst, &tm_c, (pl.c_lo & ~1) + s * cw, rbase + zr0 + rc * ch, &sbar[stage]);
     } else {
       const int nsr = cdiv(nC, rw), nrr = cdiv(r_hi(pl) - r_lo(pl), rh);
       // R1 row-chunk-major (row dots), R2 subtile-major (column sums)
       const int s = c.ph == 2 ? c.i % nsr : c.i / nrr;
-      const int rr = c.ph == 2 ? c.i / nsr : c.i % nrr;
+      int rr = c.ph == 2 ? c.i / nsr : c.i % nrr;
+      if (c.ph == 3 && rev) rr = nrr - 1 - rr;  // R2 from the rows R1 read last
       mbar_arrive_expect_tx(&sbar[stage], (uint32_t)(rw * rh * 8));
-      tma_load_2d(dst, &tm_r, xq0 + s * rw, rbase + r_lo(pl) + rr * rh, &sbar[stage]);
+      if (l2hint)
+        tma_load_2d_hint(dst, &tm_r, xq0 + s * rw, rbase + r_lo(pl) + rr * rh, &sbar[stage],
+                         c.ph == 2 ? pol_last : pol_first);
+      else
+        tma_load_2d(dst, &tm_r, xq0 + s * rw, rbase + r_lo(pl) + rr * rh, &sbar[stage]);
     }
   };
   Cursor prod{p.k_begin, 0, 0};
@@ -293,7 +311,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   // for the C columns of subtile s; box rc holds rows [rc*bh, rc*bh + bh).
   // Threads own column pairs (cp) and a row residue (rg); the RG partials are
   // summed in fixed order through s_red.
-  auto colsum_stream = [&](int C, int R, int bw, int bh, const double* v, auto out) {
+  auto colsum_stream = [&](int C, int R, int bw, int bh, const double* v, bool rv, auto out) {
     const int nsub = cdiv(C, bw), nrc = cdiv(R, bh);
     for (int s = 0; s < nsub; ++s) {
       const int Cs = min(bw, C - s * bw);
@@ -302,7 +320,8 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
       if (RG > bh) RG = bh;
       const int cp = tid % CP, rg = tid / CP;
       double2 a0 = make_double2(0.0, 0.0), a1 = a0;
-      for (int rc = 0; rc < nrc; ++rc) {
+      for (int rci = 0; rci < nrc; ++rci) {
+        const int rc = rv ? nrc - 1 - rci : rci;
         const int Rb = min(bh, R - rc * bh);
         const double* vb = v + rc * bh;
         take([&](const double* T) {
@@ -343,10 +362,11 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   // Row dots of a box stream, row chunk by row chunk: out(r, Σ_c T[r][c] v[c])
   // over all subtiles of the row; L lanes per row (bh * L <= threads), the
   // accumulators carry across the subtiles of a row chunk.
-  auto rowdot_stream = [&](int C, int R, int bw, int bh, int L, const double* v, auto out) {
+  auto rowdot_stream = [&](int C, int R, int bw, int bh, int L, const double* v, bool rv, auto out) {
     const int nsub = cdiv(C, bw), nrc = cdiv(R, bh);
     const int sub = tid % L, rsub = tid / L;
-    for (int rc = 0; rc < nrc; ++rc) {
+    for (int rci = 0; rci < nrc; ++rci) {
+      const int rc = rv ? nrc - 1 - rci : rci;
       const int Rb = min(bh, R - rc * bh);
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       for (int s = 0; s < nsub; ++s) {
@@ -418,7 +438,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
     if (p.extended) {
       // C1: partial u over owned rows -> upart[e * G + g]
       if (nR > 0)
-        colsum_stream(W, nR, cw, ch, s_z, [&](int c, double val) {
+        colsum_stream(W, nR, cw, ch, s_z, false, [&](int c, double val) {
           if (c >= co) __stcg(upart + (int64_t)(c - co) * G + g, val);
         });
       else
@@ -476,7 +496,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
       __syncthreads();
       const double cs = pl.c_scale;
       if (nR > 0)
-        rowdot_stream(W, nR, cw, ch, sp.lc, s_u, [&](int r, double acc) {
+        rowdot_stream(W, nR, cw, ch, sp.lc, s_u, rev, [&](int r, double acc) {
           const double zn = s_z[r] - cs * acc;
           s_z[r] = zn;
           __stcg(gz + zr0 + r, zn);
@@ -485,7 +505,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
     }
     // R1: partial r over owned columns -> rpart[e * G + g]
     if (nC > 0)
-      rowdot_stream(nC, nI, rw, rh, sp.lr, s_x, [&](int r, double acc) { __stcg(rpart + (int64_t)r * G + g, acc); });
+      rowdot_stream(nC, nI, rw, rh, sp.lr, s_x, false, [&](int r, double acc) { __stcg(rpart + (int64_t)r * G + g, acc); });
     else
       for (int r = tid; r < nI; r += kStreamThreads) __stcg(rpart + (int64_t)r * G + g, 0.0);
     PROF(6);
@@ -522,13 +542,13 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
     __syncthreads();
     const double rs = pl.r_scale;
     if (!SH) {
-      if (nC > 0) colsum_stream(nC, nI, rw, rh, s_r, [&](int c, double acc) { s_x[c] = s_x[c] - rs * acc; });
+      if (nC > 0) colsum_stream(nC, nI, rw, rh, s_r, rev, [&](int c, double acc) { s_x[c] = s_x[c] - rs * acc; });
     } else {
       // this rank's column partials of A[I_p, xq]ᵀ r_p go to CTA g of every
       // rank (same column slice everywhere); then sum over ranks in order
       if (nC > 0) {
         if (nI > 0) {
-          colsum_stream(nC, nI, rw, rh, s_r, [&](int c, double acc) {
+          colsum_stream(nC, nI, rw, rh, s_r, rev, [&](int c, double acc) {
             for (int q = 0; q < P; ++q) __stcg(X.inbox_x[q] + ((int64_t)slot * P + rank) * X.n_cap + xq0 + c, acc);
           });
         } else {

@@ -163,6 +163,8 @@ struct StreamParams {
   int32_t rw, rh;                 // row-block box: rw columns x rh rows
   int32_t lc, lr;                 // lanes per row in the row dots (ch * lc, rh * lr <= 512)
   int32_t pad_nC, pad_nR, pad_nJ, pad_nI;  // vector areas after the ring (doubles, even)
+  int32_t l2hint;   // 1: L2 eviction-priority hints on the TMA loads (REBK_STREAM_L2HINT, default 1)
+  int32_t reverse;  // 1: second passes walk their row chunks backwards (REBK_STREAM_REV, default 1)
 };
 
 // Sparse (CSR + CSC twin) persistent kernel (rebk_csr.cu).
