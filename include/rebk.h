@@ -59,6 +59,7 @@ extern "C" {
 #define REBK_ALGO_REK 1  /* step_rek   solvers.py:340-342 (singleton rebk) */
 #define REBK_ALGO_RABK 2 /* step_rabk  solvers.py:315-321 (row sweep only) */
 #define REBK_ALGO_RK 3   /* step_rk    solvers.py:306-312 (singleton rabk) */
+#define REBK_ALGO_DSBGS 4 /* step_dsbgs solvers.py:371-381 (joint block sampler, dense A) */
 
 /* stopping modes (solvers.py:50-70, :398-422) */
 #define REBK_STOP_ORACLE_ERROR 0
@@ -102,6 +103,18 @@ typedef struct rebk_cfg {
    * at that check and return REBK_ENONFINITE (outputs hold that state). */
   int32_t nonfinite_stop;
   int32_t reserved0;
+  /* REBK_ALGO_DSBGS only (solvers.py:204-229, _build_dsbgs_tables): the
+   * joint law P(i, j) ~ ||A[I_i, J_j]||_F^2 as the column sampler (col_cum /
+   * col_total above) times, per column block j, a conditional sampler over
+   * the row blocks with a nonzero submatrix: entries [dsbgs_off[j],
+   * dsbgs_off[j+1]) of dsbgs_cum (np.cumsum of those weights) and
+   * dsbgs_alive (their row-block indices), total dsbgs_total[j];
+   * dsbgs_scale[i * n_col_blocks + j] = alpha / ||A[I_i, J_j]||_F^2. */
+  const int64_t* dsbgs_off;
+  const double* dsbgs_cum;
+  const double* dsbgs_total;
+  const int32_t* dsbgs_alive;
+  const double* dsbgs_scale;
 } rebk_cfg;
 
 /* RunTrace (solvers.py:96-112). errors is caller-allocated (capacity

@@ -195,7 +195,8 @@ class Sampler:
 # -- the iteration (solvers.py:283-342) and the run loop (solvers.py:425-474) ----
 
 class OracleSolver:
-    """REBK / REK / RABK / RK on contiguous partitions given by block pointers."""
+    """REBK / REK / RABK / RK / DSBGS on partitions given by block pointers
+    or index blocks."""
 
     def __init__(self, a: np.ndarray, b: np.ndarray, row_blocks, col_blocks=None, alpha: float = 1.0,
                  algorithm: str = "rebk"):
@@ -219,6 +220,7 @@ class OracleSolver:
         self.b = np.asarray(b, dtype=np.float64)
         self.algorithm = algorithm
         self.extended = algorithm in ("rebk", "rek")
+        self.dsbgs = algorithm == "dsbgs"
         if isinstance(row_blocks, np.ndarray) and row_blocks.dtype != object:
             row_blocks = blocks_from_ptr(row_blocks)
         self.row_sel = [_sel(bk) for bk in row_blocks]
@@ -229,7 +231,7 @@ class OracleSolver:
         self.row_sampler = Sampler(block_weights(self.a, row_blocks, "row", self.csr, self.csc))
         self.row_scales = [float(alpha / w) for w in self.row_sampler.weights]
         self.b_blocks = [self.b[s] for s in self.row_sel]
-        if self.extended:
+        if self.extended or self.dsbgs:
             if isinstance(col_blocks, np.ndarray) and col_blocks.dtype != object:
                 col_blocks = blocks_from_ptr(col_blocks)
             self.col_sel = [_sel(bk) for bk in col_blocks]
@@ -239,9 +241,51 @@ class OracleSolver:
                 self.col_blocks = [self.a[:, s] for s in self.col_sel]
             self.col_sampler = Sampler(block_weights(self.a, col_blocks, "col", self.csr, self.csc))
             self.col_scales = [float(alpha / w) for w in self.col_sampler.weights]
+        if self.dsbgs:
+            self._dsbgs_tables(alpha)
+
+    def _dsbgs_tables(self, alpha):
+        """_build_dsbgs_tables (solvers.py:204-229): weight of every
+        submatrix A[I_i, J_j] by the dot of its C-order flattening (sparse:
+        of its CSR values), per column block the conditional sampler over
+        the row blocks whose submatrix is nonzero, scales alpha / w."""
+        s, t = len(self.row_blocks), len(self.col_sel)
+        self.sub = [[None] * t for _ in range(s)]
+        w = np.zeros((s, t))
+        for i in range(s):
+            for j, cs in enumerate(self.col_sel):
+                sub = self.row_blocks[i][:, cs]
+                self.sub[i][j] = sub
+                if self.sparse:
+                    w[i, j] = float(sub.data @ sub.data) if sub.nnz else 0.0
+                else:
+                    flat = np.ravel(sub)
+                    w[i, j] = float(flat @ flat)
+        self.ds_scales = [[float(alpha / v) if v > 0.0 else None for v in row] for row in w]
+        self.ds_cond = []
+        for j in range(t):
+            alive = np.flatnonzero(w[:, j] > 0.0)
+            self.ds_cond.append((Sampler(w[alive, j]), alive))
+
+    def draw(self, rng) -> tuple[int, int]:
+        """The two draws of one iteration (solvers.py:8-12, :373-375)."""
+        if self.dsbgs:
+            j = self.col_sampler.sample(rng)
+            cond, alive = self.ds_cond[j]
+            return j, int(alive[cond.sample(rng)])
+        if self.extended:
+            j = self.col_sampler.sample(rng)
+        else:
+            rng.uniform()
+            j = -1
+        return j, self.row_sampler.sample(rng)
 
     def picks(self, rng, count: int) -> np.ndarray:
         out = np.empty((count, 2), dtype=np.int64)
+        if self.dsbgs:
+            for k in range(count):
+                out[k] = self.draw(rng)
+            return out
         for k in range(count):
             if self.extended:
                 out[k, 0] = self.col_sampler.sample(rng)
@@ -252,6 +296,12 @@ class OracleSolver:
         return out
 
     def step(self, x: np.ndarray, z: np.ndarray | None, j: int, i: int) -> None:
+        if self.dsbgs:                        # step_dsbgs, solvers.py:371-381
+            r = self.row_blocks[i] @ x
+            r -= self.b_blocks[i]
+            u = self.sub[i][j].T @ r
+            x[self.col_sel[j]] -= self.ds_scales[i][j] * u
+            return
         if self.extended:
             blk = self.col_blocks[j]          # _weighted_col_update, solvers.py:283-286
             u = blk.T @ z
@@ -304,12 +354,7 @@ class OracleSolver:
         t0 = time.perf_counter()
         if not conv:
             for k in range(1, max_iters + 1):
-                if self.extended:
-                    j = self.col_sampler.sample(rng)
-                else:
-                    rng.uniform()
-                    j = -1
-                i = self.row_sampler.sample(rng)
+                j, i = self.draw(rng)
                 picks.append((j, i))
                 self.step(x, z, j, i)
                 if k % stride == 0:

@@ -26,7 +26,7 @@ ERRORS = {
     -5: "REBK_ENONFINITE",
 }
 
-ALGO_CODES = {"rebk": 0, "rek": 1, "rabk": 2, "rk": 3}
+ALGO_CODES = {"rebk": 0, "rek": 1, "rabk": 2, "rk": 3, "dsbgs": 4}
 STOP_CODES = {"oracle_error": 0, "residual_proxy": 1, "max_iters_only": 2}
 
 
@@ -55,6 +55,11 @@ class RebkCfg(ctypes.Structure):
         ("residual_scale", c_double),
         ("nonfinite_stop", c_int32),
         ("reserved0", c_int32),
+        ("dsbgs_off", POINTER(c_int64)),
+        ("dsbgs_cum", POINTER(c_double)),
+        ("dsbgs_total", POINTER(c_double)),
+        ("dsbgs_alive", POINTER(c_int32)),
+        ("dsbgs_scale", POINTER(c_double)),
     ]
 
 

@@ -605,6 +605,71 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
   return REBK_OK;
 }
 
+// The sampler arrays of a run (row / column partitions, DSBGS tables,
+// explicit picks) copied to the device and wired into the plan sampler.
+// `cols` = the run uses the column partition (REBK/REK column sweep, or the
+// DSBGS column draw).
+int upload_sampler(DevArena& arena, const rebk_cfg* cfg, bool extended, bool cols, cudaStream_t stream,
+                   SampleParams* sp) {
+  const int64_t s = cfg->n_row_blocks, t = cols ? cfg->n_col_blocks : 0;
+  const bool dsbgs = cfg->algorithm == REBK_ALGO_DSBGS;
+  *sp = SampleParams{};
+  sp->key0 = cfg->philox_key[0];
+  sp->key1 = cfg->philox_key[1];
+  sp->draw_offset = cfg->draw_offset;
+  sp->extended = extended;
+  sp->dsbgs = dsbgs;
+  sp->n_row_blocks = (int32_t)s;
+  sp->n_col_blocks = (int32_t)t;
+  sp->row_total = cfg->row_total;
+  sp->col_total = cfg->col_total;
+  auto up = [&](auto** dst, const auto* src, int64_t count) -> cudaError_t {
+    using T = std::remove_const_t<std::remove_pointer_t<decltype(src)>>;
+    T* d = nullptr;
+    cudaError_t e = arena.alloc(&d, (size_t)std::max<int64_t>(count, 1));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d, src, sizeof(T) * count, cudaMemcpyHostToDevice, stream);
+    *dst = d;
+    return e;
+  };
+  CUDA_TRY(up(&sp->row_ptr, cfg->row_ptr, s + 1));
+  CUDA_TRY(up(&sp->row_cum, cfg->row_cum, s));
+  CUDA_TRY(up(&sp->row_scale, cfg->row_scale, s));
+  if (cols) {
+    CUDA_TRY(up(&sp->col_ptr, cfg->col_ptr, t + 1));
+    CUDA_TRY(up(&sp->col_cum, cfg->col_cum, t));
+    if (cfg->col_scale) CUDA_TRY(up(&sp->col_scale, cfg->col_scale, t));
+  }
+  if (dsbgs) {
+    const int64_t total = cfg->dsbgs_off[t];
+    CUDA_TRY(up(&sp->d_off, cfg->dsbgs_off, t + 1));
+    CUDA_TRY(up(&sp->d_cum, cfg->dsbgs_cum, total));
+    CUDA_TRY(up(&sp->d_total, cfg->dsbgs_total, t));
+    CUDA_TRY(up(&sp->d_alive, cfg->dsbgs_alive, total));
+    CUDA_TRY(up(&sp->d_scale, cfg->dsbgs_scale, s * t));
+  }
+  if (cfg->picks && cfg->max_iters > 0) CUDA_TRY(up(&sp->picks, cfg->picks, 2 * cfg->max_iters));
+  return REBK_OK;
+}
+
+// DSBGS tables: offsets monotone from 0, alive indices in range, every
+// scale finite and positive where the conditional can pick it
+int check_dsbgs(const rebk_cfg* cfg) {
+  const int64_t s = cfg->n_row_blocks, t = cfg->n_col_blocks;
+  if (!cfg->dsbgs_off || !cfg->dsbgs_cum || !cfg->dsbgs_total || !cfg->dsbgs_alive || !cfg->dsbgs_scale)
+    return fail(REBK_EINVAL, "dsbgs needs its joint-sampler tables (rebk_cfg.dsbgs_*)");
+  if (cfg->dsbgs_off[0] != 0) return fail(REBK_EINVAL, "dsbgs_off[0] must be 0");
+  for (int64_t j = 0; j < t; ++j) {
+    if (cfg->dsbgs_off[j + 1] <= cfg->dsbgs_off[j])
+      return fail(REBK_EINVAL, "column block %lld has no nonzero submatrix", (long long)j);
+    for (int64_t e = cfg->dsbgs_off[j]; e < cfg->dsbgs_off[j + 1]; ++e) {
+      const int32_t i = cfg->dsbgs_alive[e];
+      if (i < 0 || i >= s) return fail(REBK_EINVAL, "dsbgs_alive entry out of range");
+      if (!(cfg->dsbgs_scale[i * t + j] > 0.0)) return fail(REBK_EINVAL, "dsbgs scale must be positive");
+    }
+  }
+  return REBK_OK;
+}
+
 int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev, double* x_dev,
                  double* z_dev, cudaStream_t stream, rebk_trace* trace) {
   const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
@@ -620,30 +685,12 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
 
   DevArena arena;
   arena.stream = stream;
-  const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
-  int64_t *d_row_ptr, *d_col_ptr = nullptr;
-  double *d_row_cum, *d_row_scale, *d_col_cum = nullptr, *d_col_scale = nullptr;
-  CUDA_TRY(arena.alloc(&d_row_ptr, s + 1));
-  CUDA_TRY(arena.alloc(&d_row_cum, s));
-  CUDA_TRY(arena.alloc(&d_row_scale, s));
-  CUDA_TRY(cudaMemcpyAsync(d_row_ptr, cfg->row_ptr, (s + 1) * 8, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync(d_row_cum, cfg->row_cum, s * 8, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync(d_row_scale, cfg->row_scale, s * 8, cudaMemcpyHostToDevice, stream));
-  if (extended) {
-    CUDA_TRY(arena.alloc(&d_col_ptr, t + 1));
-    CUDA_TRY(arena.alloc(&d_col_cum, t));
-    CUDA_TRY(arena.alloc(&d_col_scale, t));
-    CUDA_TRY(cudaMemcpyAsync(d_col_ptr, cfg->col_ptr, (t + 1) * 8, cudaMemcpyHostToDevice, stream));
-    CUDA_TRY(cudaMemcpyAsync(d_col_cum, cfg->col_cum, t * 8, cudaMemcpyHostToDevice, stream));
-    CUDA_TRY(cudaMemcpyAsync(d_col_scale, cfg->col_scale, t * 8, cudaMemcpyHostToDevice, stream));
-  }
-  int32_t* d_picks = nullptr;
-  if (cfg->picks && cfg->max_iters > 0) {
-    CUDA_TRY(arena.alloc(&d_picks, 2 * cfg->max_iters));
-    CUDA_TRY(cudaMemcpyAsync(d_picks, cfg->picks, 2 * cfg->max_iters * sizeof(int32_t), cudaMemcpyHostToDevice,
-                             stream));
-  }
-  const int nJ_max = extended ? max_block(t, cfg->col_ptr) : 1;
+  const bool dsbgs = cfg->algorithm == REBK_ALGO_DSBGS;
+  const int64_t s = cfg->n_row_blocks, t = (extended || dsbgs) ? cfg->n_col_blocks : 0;
+  SampleParams smp{};
+  rc = upload_sampler(arena, cfg, extended, extended || dsbgs, stream, &smp);
+  if (rc) return rc;
+  const int nJ_max = t > 0 ? max_block(t, cfg->col_ptr) : 1;
   const int nI_max = max_block(s, cfg->row_ptr);
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(cfg->max_iters, (int64_t)1 << 20));
   Plan* d_plan;
@@ -663,23 +710,6 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
     CUDA_TRY(arena.alloc(&d_prof, (size_t)G * 16));
     CUDA_TRY(cudaMemsetAsync(d_prof, 0, (size_t)G * 16 * 8, stream));
   }
-
-  SampleParams smp{};
-  smp.key0 = cfg->philox_key[0];
-  smp.key1 = cfg->philox_key[1];
-  smp.draw_offset = cfg->draw_offset;
-  smp.extended = extended;
-  smp.n_row_blocks = (int32_t)s;
-  smp.n_col_blocks = (int32_t)t;
-  smp.row_ptr = d_row_ptr;
-  smp.row_cum = d_row_cum;
-  smp.row_total = cfg->row_total;
-  smp.row_scale = d_row_scale;
-  smp.col_ptr = d_col_ptr;
-  smp.col_cum = d_col_cum;
-  smp.col_total = cfg->col_total;
-  smp.col_scale = d_col_scale;
-  smp.picks = d_picks;
 
   CsrParams p{};
   p.m = (int32_t)ctx->m;
@@ -722,6 +752,7 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
   p.res_scale = cfg->residual_scale > 0.0 ? cfg->residual_scale : 1.0;
   p.record = errs_cap > 0;
   p.nonfinite_stop = cfg->nonfinite_stop;
+  p.dsbgs = dsbgs;
   p.prof = d_prof;
 
   cudaEvent_t ev0, ev1;
@@ -807,7 +838,8 @@ constexpr int kRetryGeneral = 100;
 int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const double* xs_dev,
                          double* x_dev, double* z_dev, cudaStream_t stream, rebk_trace* trace, bool force_general) {
   const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
-  if (cfg->algorithm < 0 || cfg->algorithm > 3) return fail(REBK_EINVAL, "unknown algorithm %d", cfg->algorithm);
+  const bool dsbgs = cfg->algorithm == REBK_ALGO_DSBGS;
+  if (cfg->algorithm < 0 || cfg->algorithm > 4) return fail(REBK_EINVAL, "unknown algorithm %d", cfg->algorithm);
   if (cfg->stop_mode < 0 || cfg->stop_mode > 2) return fail(REBK_EINVAL, "unknown stopping mode %d", cfg->stop_mode);
   if (cfg->stop_mode != REBK_STOP_MAX_ITERS_ONLY && !(cfg->tol > 0.0)) return fail(REBK_EINVAL, "tol must be positive");
   if (cfg->check_stride < 1) return fail(REBK_EINVAL, "check_stride must be at least 1");
@@ -817,10 +849,12 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
   if (!b_dev || !x_dev || (extended && !z_dev)) return fail(REBK_EINVAL, "missing b / x / z buffer");
   int rc = check_partition("row", cfg->n_row_blocks, cfg->row_ptr, cfg->row_cum, cfg->row_scale, ctx->m);
   if (rc) return rc;
-  if (extended) {
-    rc = check_partition("col", cfg->n_col_blocks, cfg->col_ptr, cfg->col_cum, cfg->col_scale, ctx->n);
+  if (extended || dsbgs) {
+    rc = check_partition("col", cfg->n_col_blocks, cfg->col_ptr, cfg->col_cum, dsbgs ? cfg->col_cum : cfg->col_scale,
+                         ctx->n);
     if (rc) return rc;
   }
+  if (dsbgs && (rc = check_dsbgs(cfg)) != 0) return rc;
   if (ctx->m > INT32_MAX || ctx->n > INT32_MAX) return fail(REBK_EINVAL, "matrix dimension exceeds 2^31");
   if (ctx->kind == 2) return fail(REBK_EINVAL, "fp32 contexts run through rebk_run_mrhs");
   if (ctx->kind == 1) return run_csr_impl(ctx, cfg, b_dev, xs_dev, x_dev, z_dev, stream, trace);
@@ -850,7 +884,7 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
     // TMA boxes start on 16-byte aligned columns: the clustered kernels need
     // even column-block starts (the streaming kernel handles odd ones)
     const bool even_cols = !extended || blocks_even(cfg->n_col_blocks, cfg->col_ptr);
-    if (!force_general && env_int("REBK_NO_FAST", 0) == 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY && aligned && even_cols && CS >= 1 &&
+    if (!force_general && !dsbgs && env_int("REBK_NO_FAST", 0) == 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY && aligned && even_cols && CS >= 1 &&
         G0 >= CS && encode_fn() != nullptr) {
       int NC = std::max(1, G0 / CS);
       for (int attempt = 0; attempt < 3 && NC >= 1; ++attempt) {
@@ -905,7 +939,7 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
   StreamGeometry stg;
   CUtensorMap tm_sc, tm_sr;
   const int stream_env = env_int("REBK_STREAM", 1);  // 0 off, 1 when the general kernel cannot stage, 2 always
-  if (!use_fast && stream_env != 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY &&
+  if (!use_fast && !dsbgs && stream_env != 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY &&
       (ctx->lda % 2 == 0) && ((uintptr_t)ctx->A % 16 == 0) && encode_fn() != nullptr &&
       (stream_env == 2 || tiles_exceed_smem(geo, extended))) {
     stg = stream_geometry(ctx, cfg, std::min(G0, ctx->sm_count), extended);
@@ -921,31 +955,10 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
 
   DevArena arena;
   arena.stream = stream;
-  const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
-  int64_t *d_row_ptr, *d_col_ptr = nullptr;
-  double *d_row_cum, *d_row_scale, *d_col_cum = nullptr, *d_col_scale = nullptr;
   hm.mark("path selection");
-  CUDA_TRY(arena.alloc(&d_row_ptr, s + 1));
-  CUDA_TRY(arena.alloc(&d_row_cum, s));
-  CUDA_TRY(arena.alloc(&d_row_scale, s));
-  CUDA_TRY(cudaMemcpyAsync(d_row_ptr, cfg->row_ptr, (s + 1) * 8, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync(d_row_cum, cfg->row_cum, s * 8, cudaMemcpyHostToDevice, stream));
-  CUDA_TRY(cudaMemcpyAsync(d_row_scale, cfg->row_scale, s * 8, cudaMemcpyHostToDevice, stream));
-  if (extended) {
-    CUDA_TRY(arena.alloc(&d_col_ptr, t + 1));
-    CUDA_TRY(arena.alloc(&d_col_cum, t));
-    CUDA_TRY(arena.alloc(&d_col_scale, t));
-    CUDA_TRY(cudaMemcpyAsync(d_col_ptr, cfg->col_ptr, (t + 1) * 8, cudaMemcpyHostToDevice, stream));
-    CUDA_TRY(cudaMemcpyAsync(d_col_cum, cfg->col_cum, t * 8, cudaMemcpyHostToDevice, stream));
-    CUDA_TRY(cudaMemcpyAsync(d_col_scale, cfg->col_scale, t * 8, cudaMemcpyHostToDevice, stream));
-  }
-  int32_t* d_picks = nullptr;
-  if (cfg->picks && cfg->max_iters > 0) {
-    CUDA_TRY(arena.alloc(&d_picks, 2 * cfg->max_iters));
-    CUDA_TRY(cudaMemcpyAsync(d_picks, cfg->picks, 2 * cfg->max_iters * sizeof(int32_t),
-                             cudaMemcpyHostToDevice, stream));
-  }
-
+  SampleParams sp{};
+  rc = upload_sampler(arena, cfg, extended, extended || dsbgs, stream, &sp);
+  if (rc) return rc;
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(cfg->max_iters, (int64_t)1 << 20));
   Plan* d_plan;
   double *d_upart, *d_rpart, *d_u, *d_r, *d_errpart, *d_res = nullptr, *d_errs = nullptr;
@@ -996,23 +1009,6 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
   }
   CUDA_TRY(cudaMemsetAsync(d_ctl, 0, sizeof(Control), stream));
 
-  SampleParams sp{};
-  sp.key0 = cfg->philox_key[0];
-  sp.key1 = cfg->philox_key[1];
-  sp.draw_offset = cfg->draw_offset;
-  sp.extended = extended;
-  sp.n_row_blocks = (int32_t)s;
-  sp.n_col_blocks = (int32_t)t;
-  sp.row_ptr = d_row_ptr;
-  sp.row_cum = d_row_cum;
-  sp.row_total = cfg->row_total;
-  sp.row_scale = d_row_scale;
-  sp.col_ptr = d_col_ptr;
-  sp.col_cum = d_col_cum;
-  sp.col_total = cfg->col_total;
-  sp.col_scale = d_col_scale;
-  sp.picks = d_picks;
-
   DenseParams p{};
   p.A = ctx->A;
   p.lda = ctx->lda;
@@ -1041,6 +1037,7 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
   p.res_scale = cfg->residual_scale > 0.0 ? cfg->residual_scale : 1.0;
   p.record = errs_cap > 0;
   p.nonfinite_stop = cfg->nonfinite_stop;
+  p.dsbgs = dsbgs;
   p.nJ_max = geo.nJ_max;
   p.nI_max = geo.nI_max;
   p.nR_max = geo.nR_max;
@@ -2136,7 +2133,12 @@ int rebk_run(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b, const double* 
 int rebk_sample_sequence(const rebk_cfg* cfg, int64_t k0, int64_t count, int32_t* picks_out) {
   if (!cfg || !picks_out || k0 < 1 || count < 0) return fail(REBK_EINVAL, "bad argument");
   const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
+  const bool dsbgs = cfg->algorithm == REBK_ALGO_DSBGS;
   if (count == 0) return REBK_OK;
+  if (dsbgs) {
+    int rc = check_dsbgs(cfg);
+    if (rc) return rc;
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(REBK_ENODEV, "no CUDA device available");
   cudaStream_t stream;
@@ -2145,44 +2147,17 @@ int rebk_sample_sequence(const rebk_cfg* cfg, int64_t k0, int64_t count, int32_t
   {
     DevArena arena;
     arena.stream = stream;
-    const int64_t s = cfg->n_row_blocks, t = extended ? cfg->n_col_blocks : 0;
-    int64_t *d_row_ptr, *d_col_ptr = nullptr;
-    double *d_row_cum, *d_row_scale, *d_col_cum = nullptr, *d_col_scale = nullptr;
-    int32_t* d_out;
-    cudaError_t e = arena.alloc(&d_row_ptr, s + 1);
-    if (!e) e = arena.alloc(&d_row_cum, s);
-    if (!e) e = arena.alloc(&d_row_scale, s);
-    if (!e) e = cudaMemcpyAsync(d_row_ptr, cfg->row_ptr, (s + 1) * 8, cudaMemcpyHostToDevice, stream);
-    if (!e) e = cudaMemcpyAsync(d_row_cum, cfg->row_cum, s * 8, cudaMemcpyHostToDevice, stream);
-    if (!e) e = cudaMemcpyAsync(d_row_scale, cfg->row_scale, s * 8, cudaMemcpyHostToDevice, stream);
-    if (!e && extended) {
-      e = arena.alloc(&d_col_ptr, t + 1);
-      if (!e) e = arena.alloc(&d_col_cum, t);
-      if (!e) e = arena.alloc(&d_col_scale, t);
-      if (!e) e = cudaMemcpyAsync(d_col_ptr, cfg->col_ptr, (t + 1) * 8, cudaMemcpyHostToDevice, stream);
-      if (!e) e = cudaMemcpyAsync(d_col_cum, cfg->col_cum, t * 8, cudaMemcpyHostToDevice, stream);
-      if (!e) e = cudaMemcpyAsync(d_col_scale, cfg->col_scale, t * 8, cudaMemcpyHostToDevice, stream);
-    }
-    if (!e) e = arena.alloc(&d_out, 2 * count);
     SampleParams sp{};
-    sp.key0 = cfg->philox_key[0];
-    sp.key1 = cfg->philox_key[1];
-    sp.draw_offset = cfg->draw_offset;
-    sp.extended = extended;
-    sp.n_row_blocks = (int32_t)s;
-    sp.n_col_blocks = (int32_t)t;
-    sp.row_ptr = d_row_ptr;
-    sp.row_cum = d_row_cum;
-    sp.row_total = cfg->row_total;
-    sp.row_scale = d_row_scale;
-    sp.col_ptr = d_col_ptr;
-    sp.col_cum = d_col_cum;
-    sp.col_total = cfg->col_total;
-    sp.col_scale = d_col_scale;
-    if (!e) e = launch_sample_plan(sp, k0, count, nullptr, d_out, stream);
-    if (!e) e = cudaMemcpyAsync(picks_out, d_out, 2 * count * sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
-    if (!e) e = cudaStreamSynchronize(stream);
-    if (e) rc = fail(REBK_ECUDA, "sampling failed: %s", cudaGetErrorString(e));
+    rebk_cfg c = *cfg;
+    c.picks = nullptr;
+    rc = upload_sampler(arena, &c, extended, extended || dsbgs, stream, &sp);
+    int32_t* d_out = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (!rc) e = arena.alloc(&d_out, 2 * count);
+    if (!rc && !e) e = launch_sample_plan(sp, k0, count, nullptr, d_out, stream);
+    if (!rc && !e) e = cudaMemcpyAsync(picks_out, d_out, 2 * count * sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
+    if (!rc && !e) e = cudaStreamSynchronize(stream);
+    if (!rc && e) rc = fail(REBK_ECUDA, "sampling failed: %s", cudaGetErrorString(e));
   }
   cudaStreamSynchronize(stream);
   cudaStreamDestroy(stream);

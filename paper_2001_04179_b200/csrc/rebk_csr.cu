@@ -274,6 +274,8 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
       const int64_t s1 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g + 1];
       for (int64_t sg = s0 + tid; sg < s1; sg += kCsrThreads) {
         const int j = p.rseg_col[sg];
+        // step_dsbgs: only x[J] moves (solvers.py:378-379)
+        if (p.dsbgs && (j < pl.c_lo || j >= pl.c_hi)) continue;
         const double xj = __ldcg(p.x + j);
         double acc = 0.0;
         const int64_t e1 = p.rseg_ptr[sg + 1];

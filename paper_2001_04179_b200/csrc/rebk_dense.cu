@@ -285,7 +285,11 @@ __global__ void __launch_bounds__(kThreads, 1) rebk_dense_kernel(DenseParams p) 
       const double* rt = p.stage_rt ? s_rt : p.A + (int64_t)rl * p.lda + xq0;
       const int64_t rtld = p.stage_rt ? p.rt_ld : p.lda;
       const double rs = pl.r_scale;
-      auto x_epi = [&](int c, double acc) { s_x[c] = s_x[c] - rs * acc; };
+      // step_dsbgs: only the sampled column block's coordinates move
+      // (x[J] -= s_ij A[I, J]^T r, solvers.py:378-379)
+      auto x_epi = [&](int c, double acc) {
+        if (!p.dsbgs || (xq0 + c >= cl && xq0 + c < cl + nJ)) s_x[c] = s_x[c] - rs * acc;
+      };
       if (p.stage_rt)
         tile_colsum<LdShared, LdShared>(rt, rtld, nI, nC, s_r, s_red, x_epi);
       else
@@ -405,6 +409,16 @@ __global__ void sample_plan_kernel(SampleParams sp, int64_t k0, int64_t count, P
   if (sp.picks) {
     j = sp.picks[2 * (k - 1)];
     i = sp.picks[2 * (k - 1) + 1];
+  } else if (sp.dsbgs) {
+    // step_dsbgs (solvers.py:371-375): column block from the column sampler
+    // (draw 2(k-1)), then the row block from that column's conditional
+    // sampler over its nonzero submatrices (draw 2k-1)
+    const uint64_t dc = sp.draw_offset + 2ull * (uint64_t)(k - 1);
+    const uint64_t wc = philox_word(dc, sp.key0, sp.key1), wr = philox_word(dc + 1, sp.key0, sp.key1);
+    j = sample_block(sp.col_cum, sp.n_col_blocks, sp.col_total, u64_to_unit_double(wc));
+    const int64_t o0 = sp.d_off[j], o1 = sp.d_off[j + 1];
+    const int c = sample_block(sp.d_cum + o0, (int)(o1 - o0), sp.d_total[j], u64_to_unit_double(wr));
+    i = sp.d_alive[o0 + c];
   } else {
     const uint64_t dc = sp.draw_offset + 2ull * (uint64_t)(k - 1);
     const uint64_t dr = dc + 1;
@@ -422,7 +436,11 @@ __global__ void sample_plan_kernel(SampleParams sp, int64_t k0, int64_t count, P
   }
   if (plan) {
     Plan pl;
-    if (sp.extended) {
+    if (sp.dsbgs) {
+      pl.c_lo = (int32_t)sp.col_ptr[j];
+      pl.c_hi = (int32_t)sp.col_ptr[j + 1];
+      pl.c_scale = 0.0;
+    } else if (sp.extended) {
       pl.c_lo = (int32_t)sp.col_ptr[j];
       pl.c_hi = (int32_t)sp.col_ptr[j + 1];
       pl.c_scale = sp.col_scale[j];
@@ -432,7 +450,7 @@ __global__ void sample_plan_kernel(SampleParams sp, int64_t k0, int64_t count, P
     }
     pl.r_lo = (int32_t)sp.row_ptr[i];
     pl.r_hi = (int32_t)sp.row_ptr[i + 1];
-    pl.r_scale = sp.row_scale[i];
+    pl.r_scale = sp.dsbgs ? sp.d_scale[(int64_t)i * sp.n_col_blocks + j] : sp.row_scale[i];
     pl.cb = j;
     pl.rb = i;
     pl.pad0 = pl.pad1 = 0;

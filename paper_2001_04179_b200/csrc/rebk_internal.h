@@ -82,6 +82,7 @@ struct DenseParams {
   double res_scale;
   int32_t record;
   int32_t nonfinite_stop;  // stop the run at a NaN/Inf error (rebk_cfg.nonfinite_stop)
+  int32_t dsbgs;           // step_dsbgs: x update restricted to the plan's column block, no z
   // tile geometry (host-computed)
   int32_t nJ_max, nI_max;  // largest column / row block
   int32_t nR_max, nC_max;  // largest owned z-row / x-column slice
@@ -213,6 +214,7 @@ struct CsrParams {
   double res_scale;
   int32_t record;
   int32_t nonfinite_stop;
+  int32_t dsbgs;  // step_dsbgs: x update restricted to the plan's column block, no z
   long long* prof;  // optional per-CTA phase cycle counters [G][16] (REBK_PROF=1)
 };
 
@@ -253,6 +255,13 @@ struct SampleParams {
   double col_total;
   const double* col_scale;
   const int32_t* picks;  // optional scripted picks, indexed by (k-1)
+  // DSBGS joint sampler (rebk_cfg.dsbgs_*; device copies), dsbgs != 0
+  int32_t dsbgs;
+  const int64_t* d_off;
+  const double* d_cum;
+  const double* d_total;
+  const int32_t* d_alive;
+  const double* d_scale;
 };
 
 // balanced split of [0, len) over G parts; boundaries rounded down to even

@@ -16,9 +16,11 @@ same validation errors.  The iteration itself never runs in Python:
   iteration with those explicit picks.
 
 Algorithms on the device: rebk, rek, rabk, rk (step_rebk/step_rek/
-step_rabk/step_rk, solvers.py:306-342).  rbk, rdbk and dsbgs validate like
-the reference but raise NotImplementedError: they need per-block
-pseudoinverses or a joint sampler, outside this hot path.
+step_rabk/step_rk, solvers.py:306-342) and dsbgs (step_dsbgs,
+solvers.py:371-381: the joint submatrix sampler, with the reference's own
+tables as inputs).  rbk and rdbk validate like the reference but raise
+NotImplementedError: they apply per-block pseudoinverses (a different
+kernel, outside this hot path).
 """
 
 from __future__ import annotations
@@ -43,7 +45,7 @@ _EXTENDED = frozenset({"rek", "rdbk", "rebk"})
 _NEEDS_COL_PARTITION = frozenset({"rdbk", "dsbgs", "rebk"})
 _PROJECTION = frozenset({"rbk", "rdbk"})
 _STEPSIZE_RATE_ALGOS = frozenset({"rk", "rek", "rabk", "rebk"})
-DEVICE_ALGORITHMS = frozenset({"rk", "rek", "rabk", "rebk"})
+DEVICE_ALGORITHMS = frozenset({"rk", "rek", "rabk", "rebk", "dsbgs"})
 
 OutOfRegimeWarning = "stepsize at or beyond 2/beta_max: outside the guaranteed mean-square regime"
 
@@ -222,10 +224,13 @@ class SolverContext:
             self.col_scales = [float(self.alpha / w) for w in self.col_sampler.weights]
             self.col_selectors = [slice(i.start, i.stop) if isinstance(i, range) else i for i in col_p.blocks]
 
+        self.dsbgs_conditionals = None
+        self.dsbgs_scales = None
+        if algo == "dsbgs":
+            self._build_dsbgs_tables()
+
         if algo not in DEVICE_ALGORITHMS:
-            raise NotImplementedError(
-                f"{algo} is not on the B200 hot path (needs block pseudoinverses or a joint sampler)"
-            )
+            raise NotImplementedError(f"{algo} is not on the B200 hot path (it needs per-block pseudoinverses)")
 
         self.warnings: list[str] = []
         self.beta_max = config.beta_max
@@ -245,6 +250,48 @@ class SolverContext:
             self.warnings.append(OutOfRegimeWarning)
 
         self._bind_device()
+
+    def _build_dsbgs_tables(self):
+        """The reference's joint law P(i, j) ~ ||A[I_i, J_j]||_F^2
+        (solvers.py:204-229) with its arithmetic: every submatrix weight is
+        numpy's `flat @ flat` on the C-order submatrix (scipy `data @ data`
+        when sparse), the per-column conditionals are WeightedSamplers over
+        the nonzero weights, and the scales alpha / w; the device samples
+        with exactly these arrays, so the (j, i) sequence is the reference's."""
+        from .sampling import WeightedSampler
+
+        a = self.a
+        s, t = len(self.row_partition), len(self.col_partition)
+        col_sel = [slice(i.start, i.stop) if isinstance(i, range) else i for i in self.col_partition.blocks]
+        weights = np.zeros((s, t))
+        for i, ridx in enumerate(self.row_partition.blocks):
+            rb = a.block_matrix(a.block("row", ridx))
+            for j, csel in enumerate(col_sel):
+                sub = rb[:, csel]
+                if hasattr(sub, "toarray"):
+                    w = float(sub.data @ sub.data) if sub.nnz else 0.0
+                else:
+                    flat = np.ravel(sub)
+                    w = float(flat @ flat)
+                weights[i, j] = w
+        self.dsbgs_scales = [[float(self.alpha / w) if w > 0.0 else None for w in row] for row in weights]
+        conditionals = []
+        for j in range(t):
+            alive = np.flatnonzero(weights[:, j] > 0.0)
+            conditionals.append((WeightedSampler(weights[alive, j]), alive))
+        self.dsbgs_conditionals = conditionals
+        # flat device layout of the same tables (rebk_cfg.dsbgs_*)
+        self._ds_off = np.zeros(t + 1, dtype=np.int64)
+        self._ds_off[1:] = np.cumsum([alive.size for _, alive in conditionals])
+        self._ds_cum = np.ascontiguousarray(np.concatenate([c.cumulative for c, _ in conditionals]), dtype=np.float64)
+        self._ds_total = np.asarray([float(c.total) for c, _ in conditionals], dtype=np.float64)
+        self._ds_alive = np.ascontiguousarray(np.concatenate([alive for _, alive in conditionals]), dtype=np.int32)
+        sc = np.zeros((s, t))
+        for i in range(s):
+            for j in range(t):
+                v = self.dsbgs_scales[i][j]
+                sc[i, j] = 0.0 if v is None else v
+        self._ds_scale = np.ascontiguousarray(sc, dtype=np.float64)
 
     def _resolve_partition(self, p: Partition | None, axis: str, axis_len: int) -> Partition:
         algo = self.algorithm
@@ -282,7 +329,7 @@ class SolverContext:
         self._row_ptr = self.row_partition.pointers()
         self._row_cum = np.ascontiguousarray(self.row_sampler.cumulative, dtype=np.float64)
         self._row_scale = np.asarray(self.row_scales, dtype=np.float64)
-        if self.extended:
+        if self.extended or self.algorithm == "dsbgs":
             self._col_ptr = self.col_partition.pointers()
             self._col_cum = np.ascontiguousarray(self.col_sampler.cumulative, dtype=np.float64)
             self._col_scale = np.asarray(self.col_scales, dtype=np.float64)
@@ -310,12 +357,18 @@ class SolverContext:
         cfg.row_cum = _lib.dptr(self._row_cum)
         cfg.row_total = float(self.row_sampler.total)
         cfg.row_scale = _lib.dptr(self._row_scale)
-        if self.extended:
+        if self.extended or self.algorithm == "dsbgs":
             cfg.n_col_blocks = len(self.col_partition)
             cfg.col_ptr = _lib.i64ptr(self._col_ptr)
             cfg.col_cum = _lib.dptr(self._col_cum)
             cfg.col_total = float(self.col_sampler.total)
             cfg.col_scale = _lib.dptr(self._col_scale)
+        if self.algorithm == "dsbgs":
+            cfg.dsbgs_off = _lib.i64ptr(self._ds_off)
+            cfg.dsbgs_cum = _lib.dptr(self._ds_cum)
+            cfg.dsbgs_total = _lib.dptr(self._ds_total)
+            cfg.dsbgs_alive = self._ds_alive.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            cfg.dsbgs_scale = _lib.dptr(self._ds_scale)
         if picks is not None:
             cfg.picks = picks.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
         cfg.record_errors = int(bool(record))
@@ -407,6 +460,10 @@ class SolverContext:
         """The two draws of one iteration, in the reference's stream layout
         (solvers.py:8-12): column draw first (discarded without a column
         sweep), then the row draw."""
+        if self.algorithm == "dsbgs":  # step_dsbgs, solvers.py:373-375
+            j = self.col_sampler.sample(rng)
+            conditional, alive = self.dsbgs_conditionals[j]
+            return j, int(alive[conditional.sample(rng)])
         if self.extended:
             j = self.col_sampler.sample(rng)
         else:
@@ -507,4 +564,9 @@ def step_rk(state: SolverState, ctx: SolverContext) -> SolverState:
     return ctx.step(state)
 
 
-_STEPPERS = {"rk": step_rk, "rek": step_rek, "rabk": step_rabk, "rebk": step_rebk}
+def step_dsbgs(state: SolverState, ctx: SolverContext) -> SolverState:
+    """Sampled column coordinates updated from the sampled row residuals."""
+    return ctx.step(state)
+
+
+_STEPPERS = {"rk": step_rk, "rek": step_rek, "rabk": step_rabk, "rebk": step_rebk, "dsbgs": step_dsbgs}

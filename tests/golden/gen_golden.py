@@ -35,6 +35,11 @@ def ref_picks(ctx, seed, count):
     rng = K.Rng(seed)
     out = np.empty((count, 2), dtype=np.int32)
     for k in range(count):
+        if ctx.algorithm == "dsbgs":  # solvers.py:373-375
+            out[k, 0] = ctx.col_sampler.sample(rng)
+            cond, alive = ctx.dsbgs_conditionals[out[k, 0]]
+            out[k, 1] = alive[cond.sample(rng)]
+            continue
         if ctx.col_sampler is not None and ctx.algorithm in ("rebk", "rek"):
             out[k, 0] = ctx.col_sampler.sample(rng)
         else:
@@ -116,6 +121,8 @@ def small_case(name, a, b, algo, alpha, seed, row_p=None, col_p=None, max_iters=
         warnings=np.asarray(tr.warnings), picks=ref_picks(ctx, seed, npk), ks=np.asarray(ks),
         row_cum=ctx.row_sampler.cumulative, row_scales=np.asarray(ctx.row_scales),
     )
+    if ctx.algorithm == "dsbgs":
+        out["dsbgs_scales"] = np.asarray([[np.nan if v is None else v for v in row] for row in ctx.dsbgs_scales])
     if ctx.col_partition is not None:
         out["col_blocks"] = np.asarray([np.asarray(bk, dtype=np.int64) for bk in ctx.col_partition.blocks],
                                        dtype=object)
@@ -193,6 +200,45 @@ def small_cases():
     beta = compute_beta_max(p.a, rp, cp)[2]
     small_case("t1_30x50_rebk", None, None, "rebk", 1.75 / beta, 13, rp, cp, max_iters=20000, tol=1e-9,
                problem=p, stride=5)
+
+
+def dsbgs_cases():
+    """step_dsbgs (solvers.py:204-229, :371-381): the joint sampler and the
+    column-restricted x update; dense ragged, dense with a zero submatrix
+    (a row block with an all-zero column block, so that column's conditional
+    skips it), non-contiguous, and sparse."""
+    import scipy.sparse as sparse
+
+    a = K.gen_type2(37, 23, seed=60)
+    p = K.make_rhs(a, seed=61)
+    rp, cp = K.contiguous_partition(37, 5, "row"), K.contiguous_partition(23, 4, "col")
+    small_case("t2_37x23_dsbgs", None, None, "dsbgs", 1.2, 5, rp, cp, max_iters=3000, tol=1e-9, problem=p,
+               stride=3)
+    d = K.gen_type2(30, 20, seed=62).to_dense().copy()
+    d[0:6, 0:5] = 0.0
+    p = K.make_rhs(K.Matrix.from_dense(d), seed=63)
+    small_case("t2_30x20_dsbgs_zero_sub", None, None, "dsbgs", 1.0, 8, K.contiguous_partition(30, 6, "row"),
+               K.contiguous_partition(20, 5, "col"), max_iters=400, mode="max_iters_only", problem=p,
+               ks=(1, 10, 100, 400))
+    a = K.gen_type2(20, 12, seed=64)
+    p = K.make_rhs(a, seed=65)
+    rng = np.random.default_rng(6)
+    rperm, cperm = rng.permutation(20), rng.permutation(12)
+    rp = K.Partition("row", 20, tuple(np.sort(rperm[i:i + 4]) for i in range(0, 20, 4)))
+    cp = K.Partition("col", 12, tuple(np.sort(cperm[i:i + 3]) for i in range(0, 12, 3)))
+    small_case("t2_20x12_dsbgs_noncontig", None, None, "dsbgs", 1.0, 12, rp, cp, max_iters=2000, tol=1e-9,
+               problem=p)
+    g = np.random.default_rng(66)
+    s = sparse.random(80, 40, density=0.15, format="csr", random_state=g, data_rvs=g.standard_normal)
+    for r in range(80):
+        if s.indptr[r] == s.indptr[r + 1]:
+            s[r, r % 40] = 1.0
+    s = sparse.csr_matrix(s)
+    mat = K.Matrix.from_sparse(s)
+    prob = K.make_rhs(mat, seed=67)
+    small_case("sp_80x40_dsbgs", None, None, "dsbgs", 1.0, 14, K.contiguous_partition(80, 10, "row"),
+               K.contiguous_partition(40, 8, "col"), max_iters=300, mode="max_iters_only", problem=prob,
+               ks=(1, 10, 100, 300))
 
 
 def sparse_cases():
@@ -416,6 +462,10 @@ if __name__ == "__main__":
     philox_fixture()
     small_cases()
     sparse_cases()
+    if "--dsbgs-only" in sys.argv:
+        dsbgs_cases()
+        sys.exit(0)
+    dsbgs_cases()
     if "--small-only" in sys.argv:
         sys.exit(0)
     if "--c5-only" in sys.argv:

@@ -40,7 +40,7 @@ def test_struct_layout_matches_header():
     assert _lib.load().rebk_abi_struct_sizes(*[ctypes.byref(s) for s in sizes]) == 0
     assert [s.value for s in sizes] == [ctypes.sizeof(_lib.RebkCfg), ctypes.sizeof(_lib.RebkTrace),
                                         ctypes.sizeof(_lib.RebkShardRunArgs)]
-    assert ctypes.sizeof(_lib.RebkCfg) == 4 + 4 + 8 + 8 + 8 + 16 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 4 + 4 + 8 + 4 + 4
+    assert ctypes.sizeof(_lib.RebkCfg) == 4 + 4 + 8 + 8 + 8 + 16 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 8 + 4 + 4 + 8 + 4 + 4 + 5 * 8
     assert ctypes.sizeof(_lib.RebkTrace) == 8 + 4 + 4 + 8 + 8 + 8 + 8 + 8 + 4 + 4 + 8
 
 
