@@ -301,6 +301,30 @@ int rebk_block_frobenius_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* 
 int rebk_block_sigma1_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* ptr, int max_steps,
                          double* sigma1_sq_out, int32_t* steps_out);
 
+/* ---- MatrixMarket -> CSR / dense host arrays (rebk_mmio.cpp) -------------
+ * Native reader with the acceptance rules and error texts of the reference's
+ * read_matrix_market (matrix_io.py:67-157): coordinate (real / integer /
+ * pattern, general / symmetric) and array formats, duplicates summed,
+ * symmetric storage mirrored, Python int()/float() token grammar, the
+ * density threshold that decides dense vs CSR.  The output arrays (CSR with
+ * sorted columns and no explicit zeros: the reference Matrix's normalised
+ * form, ready for rebk_ctx_create_csr) are malloc'ed by the library and
+ * released with rebk_mm_free.  On a parse error: REBK_EINVAL, the message
+ * (without the "path:line: " prefix) in rebk_last_error, the 1-based line in
+ * out->err_line.  Parses on up to nthreads host threads. */
+typedef struct rebk_mm_matrix {
+  int64_t rows, cols;
+  int32_t dense;       /* 1: values = rows x cols row-major; 0: CSR */
+  int32_t reserved;
+  int64_t nnz;
+  int64_t* indptr;     /* [rows + 1] (CSR) */
+  int32_t* indices;    /* [nnz] */
+  double* values;      /* [nnz] or [rows * cols] */
+  int64_t err_line;
+} rebk_mm_matrix;
+int rebk_mm_read(const char* path, double dense_threshold, int nthreads, rebk_mm_matrix* out);
+void rebk_mm_free(rebk_mm_matrix* m);
+
 /* ---- host-side helpers (no GPU needed) ---------------------------------- */
 /* numpy SeedSequence(entropy, spawn_key).generate_state(2, uint64): the
  * Philox key of Rng(seed, spawn_key) (sampling.py:33-37). entropy / spawn

@@ -87,6 +87,20 @@ class RebkShardRunArgs(ctypes.Structure):
     ]
 
 
+class RebkMmMatrix(ctypes.Structure):
+    _fields_ = [
+        ("rows", c_int64),
+        ("cols", c_int64),
+        ("dense", c_int32),
+        ("reserved", c_int32),
+        ("nnz", c_int64),
+        ("indptr", POINTER(c_int64)),
+        ("indices", POINTER(c_int32)),
+        ("values", POINTER(c_double)),
+        ("err_line", c_int64),
+    ]
+
+
 class RebkTrace(ctypes.Structure):
     _fields_ = [
         ("iters", c_int64),
@@ -148,6 +162,8 @@ SIGNATURES = {
     "rebk_shard_run": (c_int, [c_void_p, c_void_p, POINTER(RebkShardRunArgs), _P_I64, POINTER(c_int32), _P_D]),
     "rebk_philox_key": (c_int, [POINTER(c_uint32), c_int64, POINTER(c_uint32), c_int64, POINTER(c_uint64)]),
     "rebk_philox_uniforms_host": (c_int, [POINTER(c_uint64), c_uint64, c_int64, _P_D]),
+    "rebk_mm_read": (c_int, [c_char_p, c_double, c_int, POINTER(RebkMmMatrix)]),
+    "rebk_mm_free": (None, [POINTER(RebkMmMatrix)]),
     "rebk_host_gather_col_blocks": (c_int, [_P_D, c_int64, c_int64, c_int64, c_int64, _P_I64, _P_D, c_int]),
 }
 
