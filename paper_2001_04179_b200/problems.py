@@ -1,10 +1,10 @@
 """Problem containers (problems.py:26-59 of the reference).
 
-Only the data types the solver entry point consumes are mirrored here; the
-reference's generators and its Jacobi-SVD oracle are test-time machinery and
-out of this package's scope.  ``ensure_oracle`` is kept so a
-ProblemInstance built without ground truth can still be completed, using
-LAPACK's SVD on the host.
+The data types the solver entry point consumes.  The generators and the
+oracle at scale live in :mod:`paper_2001_04179_b200.generators` (device QR /
+SVD instead of the reference's Python Jacobi SVD).  ``ensure_oracle``
+completes a ProblemInstance built without ground truth: device SVD when a
+CUDA device is present, LAPACK's on the host otherwise.
 """
 
 from __future__ import annotations
@@ -62,7 +62,18 @@ class ProblemInstance:
 
     def ensure_oracle(self) -> Svd:
         if self.oracle is None:
-            self.oracle = thin_svd(self.a)
+            try:
+                import torch
+
+                cuda = torch.cuda.is_available()
+            except Exception:  # pragma: no cover
+                cuda = False
+            if cuda:
+                from .generators import device_svd
+
+                self.oracle = device_svd(self.a)
+            else:
+                self.oracle = thin_svd(self.a)
         f = self.oracle
         if self.x_star is None:
             self.x_star = f.v @ ((f.u.T @ self.b) / f.sigma)
