@@ -104,7 +104,11 @@ def device_svd(a, device=None, keep_on_device: bool = False) -> Svd:
     wide = m < n
     w = t.T if wide else t
     q, rr = torch.linalg.qr(w, mode="reduced")
-    ur, s, vh = torch.linalg.svd(rr, full_matrices=False)
+    # cuSOLVER gesvd (QR iteration) on the device: the default driver
+    # selection may pick the approximate Jacobi variant, whose vectors are
+    # orthonormal only to its stopping tolerance
+    kw = {"driver": "gesvd"} if rr.is_cuda else {}
+    ur, s, vh = torch.linalg.svd(rr, full_matrices=False, **kw)
     left = q @ ur          # left singular vectors of w
     right = vh.T
     tol = max(m, n) * _EPS * float(s[0])

@@ -92,4 +92,6 @@ def test_oracle_at_scale_on_device():
     assert float(torch.linalg.norm(r - bp) / torch.linalg.norm(b)) <= 1e-10      # A x* = b - b_perp
     assert float(torch.linalg.norm(A.T @ bp) / torch.linalg.norm(b)) <= 1e-10    # b_perp in null(Aᵀ)
     v = torch.from_numpy(p.oracle.v).cuda()
-    assert float(torch.linalg.norm(xs - v @ (v.T @ xs)) / torch.linalg.norm(xs)) <= 1e-12  # x* in range(Aᵀ)
+    proj = float(torch.linalg.norm(xs - v @ (v.T @ xs)) / torch.linalg.norm(xs))
+    orth = float(torch.linalg.norm(v.T @ v - torch.eye(v.shape[1], dtype=v.dtype, device=v.device)))
+    assert proj <= 1e-12 and orth <= 1e-11, (proj, orth)  # x* in range(Aᵀ), V orthonormal
