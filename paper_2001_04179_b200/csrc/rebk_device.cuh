@@ -231,21 +231,31 @@ __device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uin
                "l"(__double_as_longlong(v)), "r"(remote_mbar)
                : "memory");
 }
-// {value, seq} published as one 16-byte store; consumers poll the same word
+// {value, seq} published as one 16-byte store; consumers poll the same word.
+// Tear-proof layout (the LL idea): each 8-byte half carries the sequence in
+// its high 32 bits and one half of the value in its low 32 bits.  The PTX
+// memory model guarantees single-copy atomicity for aligned accesses up to 8
+// bytes only (a wider access may be observed as its 8-byte pieces), so the
+// reader accepts the word only when BOTH halves show the expected sequence:
+// a torn read (one half old, one half new) is retried, never consumed.
 __device__ __forceinline__ void st_ll(LLWord* w, double v, unsigned long long seq) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long s32 = (seq & 0xffffffffull) << 32;
+  const unsigned long long h0 = s32 | (bits & 0xffffffffull), h1 = s32 | (bits >> 32);
   asm volatile("{\n\t.reg .b128 t;\n\tmov.b128 t, {%1, %2};\n\tst.relaxed.gpu.global.b128 [%0], t;\n\t}" ::"l"(w),
-               "l"(__double_as_longlong(v)), "l"(seq)
+               "l"(h0), "l"(h1)
                : "memory");
 }
 __device__ __forceinline__ double poll_ll(const LLWord* w, unsigned long long seq) {
-  unsigned long long v, s;
+  const unsigned long long s32 = seq & 0xffffffffull;
+  unsigned long long h0, h1;
   do {
     asm volatile("{\n\t.reg .b128 t;\n\tld.relaxed.gpu.global.b128 t, [%2];\n\tmov.b128 {%0, %1}, t;\n\t}"
-                 : "=l"(v), "=l"(s)
+                 : "=l"(h0), "=l"(h1)
                  : "l"(w)
                  : "memory");
-  } while (s != seq);
-  return __longlong_as_double(v);
+  } while ((h0 >> 32) != s32 || (h1 >> 32) != s32);
+  return __longlong_as_double((long long)((h1 << 32) | (h0 & 0xffffffffull)));
 }
 
 // ---- shared-memory tile products of the fast path ---------------------------

@@ -47,10 +47,11 @@ struct SplitShared {
   unsigned long long stop;          // 0 running; K+1 = the run stopped with state K
 };
 
-// 16-byte {value, sequence} word of the fast path's cross-cluster exchange
+// 16-byte {value, sequence} word of the fast path's cross-cluster exchange;
+// written and read only through st_ll / poll_ll (rebk_device.cuh), which
+// pack the sequence into both 8-byte halves so a torn access is detected
 struct __align__(16) LLWord {
-  double v;
-  unsigned long long seq;
+  unsigned long long half[2];  // {seq32 << 32 | lo32(v), seq32 << 32 | hi32(v)}
 };
 
 struct DenseParams {
