@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-SOURCES = ["rebk_dense.cu", "rebk_dense_fast.cu", "rebk_dense_split.cu", "rebk_dense_stream.cu", "rebk_csr.cu", "rebk_mrhs.cu", "rebk_mrhs_tc.cu", "rebk_shard.cu", "rebk_beta.cu", "rebk_nccl.cu", "rebk_api.cu", "rebk_mmio.cpp"]
+SOURCES = ["rebk_dense.cu", "rebk_dense_fast.cu", "rebk_dense_split.cu", "rebk_dense_stream.cu", "rebk_csr.cu", "rebk_csr_build.cu", "rebk_mrhs.cu", "rebk_mrhs_tc.cu", "rebk_shard.cu", "rebk_beta.cu", "rebk_nccl.cu", "rebk_api.cu", "rebk_mmio.cpp"]
 HEADERS = ["rebk_internal.h", "philox.h", "rebk_device.cuh", "umma.cuh"]
 OUT = os.path.join(HERE, "librebk.so")
 NVCC_FLAGS = [

@@ -49,9 +49,6 @@ struct rebk_ctx {
   int64_t *csr_ptr = nullptr, *csc_ptr = nullptr;
   int32_t *csr_col = nullptr, *csc_row = nullptr;
   double *csr_val = nullptr, *csc_val = nullptr;
-  std::vector<int64_t> h_csr_ptr, h_csc_ptr;
-  std::vector<int32_t> h_csr_col, h_csc_row;
-  std::vector<double> h_csr_val, h_csc_val;
   std::vector<CsrSegPlan*> seg_cache;  // guarded by mu
   float* A32 = nullptr;  // dense fp32 A (multi-RHS contexts, kind 2)
   float* A32t = nullptr;  // its transpose (n x ldat), built at the first tensor-core run (under mu)
@@ -455,101 +452,6 @@ void free_seg_plan(CsrSegPlan* sp) {
   delete sp;
 }
 
-// Segment lists of one orientation of a sparse matrix stored by major lines
-// (CSR: rows, CSC: columns).  The blocks partition the minor axis
-// (bptr[nb+1]); for every block: the major lines with nonzeros in it, in
-// major order, their [lo, hi) entry range, a compact copy of those entries
-// (minor index relative to the block start) and each of the G CTAs' first
-// segment (major axis split by split_rows).  T host threads own contiguous
-// major ranges; per-(thread, block) counts give every thread its write
-// offsets, so the lists are identical to a sequential pass.
-struct SegLists {
-  std::vector<int64_t> off, lo, hi, ptr, cta;
-  std::vector<int32_t> major_id, minor_local;
-  std::vector<double> val;
-};
-
-template <class F>
-void parallel_for_threads(int T, F&& f) {
-  std::vector<std::thread> pool;
-  pool.reserve(T - 1);
-  for (int th = 1; th < T; ++th) pool.emplace_back(f, th);
-  f(0);
-  for (auto& t : pool) t.join();
-}
-
-void seg_lists(int64_t nmajor, const int64_t* mptr, const int32_t* minor, const double* vals, int64_t nminor,
-               int64_t nb, const int64_t* bptr, int G, int T, SegLists& L) {
-  T = (int)std::max<int64_t>(1, std::min<int64_t>(T, nmajor / 4096));
-  std::vector<int32_t> blk(nminor);
-  for (int64_t q = 0; q < nb; ++q)
-    for (int64_t j = bptr[q]; j < bptr[q + 1]; ++j) blk[j] = (int32_t)q;
-  auto lo_of = [&](int th) { return nmajor * th / T; };
-  std::vector<int64_t> cnt((size_t)T * nb, 0);
-  parallel_for_threads(T, [&](int th) {
-    int64_t* c = cnt.data() + (size_t)th * nb;
-    for (int64_t i = lo_of(th); i < lo_of(th + 1); ++i) {
-      int32_t prev = -1;
-      for (int64_t e = mptr[i]; e < mptr[i + 1]; ++e) {
-        const int32_t q = blk[minor[e]];
-        if (q != prev) ++c[q];
-        prev = q;
-      }
-    }
-  });
-  L.off.assign(nb + 1, 0);
-  std::vector<int64_t> fill((size_t)T * nb);
-  for (int64_t q = 0; q < nb; ++q) {
-    int64_t acc = L.off[q];
-    for (int th = 0; th < T; ++th) {
-      fill[(size_t)th * nb + q] = acc;
-      acc += cnt[(size_t)th * nb + q];
-    }
-    L.off[q + 1] = acc;
-  }
-  const int64_t ns = L.off[nb];
-  L.lo.resize(ns); L.hi.resize(ns); L.major_id.resize(ns);
-  parallel_for_threads(T, [&](int th) {
-    int64_t* f = fill.data() + (size_t)th * nb;
-    for (int64_t i = lo_of(th); i < lo_of(th + 1); ++i) {
-      int32_t prev = -1;
-      int64_t cur = -1;
-      for (int64_t e = mptr[i]; e < mptr[i + 1]; ++e) {
-        const int32_t q = blk[minor[e]];
-        if (q != prev) {
-          cur = f[q]++;
-          L.major_id[cur] = (int32_t)i;
-          L.lo[cur] = e;
-        }
-        L.hi[cur] = e + 1;
-        prev = q;
-      }
-    }
-  });
-  L.ptr.resize(ns + 1);
-  L.ptr[0] = 0;
-  for (int64_t k = 0; k < ns; ++k) L.ptr[k + 1] = L.ptr[k] + (L.hi[k] - L.lo[k]);
-  L.val.resize(L.ptr[ns]);
-  L.minor_local.resize(L.ptr[ns]);
-  parallel_for_threads(T, [&](int th) {
-    for (int64_t q = th; q < nb; q += T)
-      for (int64_t k = L.off[q]; k < L.off[q + 1]; ++k)
-        for (int64_t e = L.lo[k]; e < L.hi[k]; ++e) {
-          const int64_t o = L.ptr[k] + (e - L.lo[k]);
-          L.val[o] = vals[e];
-          L.minor_local[o] = minor[e] - (int32_t)bptr[q];
-        }
-  });
-  L.cta.resize(nb * (G + 1));
-  for (int64_t q = 0; q < nb; ++q)
-    for (int g = 0; g <= G; ++g) {
-      const int32_t r0 = split_rows(nmajor, G, g);
-      L.cta[q * (G + 1) + g] =
-          std::lower_bound(L.major_id.begin() + L.off[q], L.major_id.begin() + L.off[q + 1], r0) -
-          L.major_id.begin();
-    }
-}
-
 // Segment lists of one partition: for every column block, the rows with
 // nonzeros in it and their [lo, hi) range in the CSR arrays (sorted by row);
 // for every row block, the columns with nonzeros in it and their range in the
@@ -571,34 +473,37 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
   sp->G = G;
   sp->row_ptr.assign(cfg->row_ptr, cfg->row_ptr + s + 1);
   if (extended) sp->col_ptr.assign(cfg->col_ptr, cfg->col_ptr + t + 1);
-  const int T = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  SegLists C, R;
-  C.off.assign(1, 0);
-  C.ptr.assign(1, 0);
-  // column blocks -> row segments into CSR
-  if (extended)
-    seg_lists(m, ctx->h_csr_ptr.data(), ctx->h_csr_col.data(), ctx->h_csr_val.data(), n, t, cfg->col_ptr, G, T, C);
-  // row blocks -> column segments into CSC
-  seg_lists(n, ctx->h_csc_ptr.data(), ctx->h_csc_row.data(), ctx->h_csc_val.data(), m, s, cfg->row_ptr, G, T, R);
-  const auto &coff = C.off, &cptr = C.ptr, &ccta = C.cta, &roff = R.off, &rptr = R.ptr, &rcta = R.cta;
-  const auto &crow = C.major_id, &ccolv = C.minor_local, &rcol = R.major_id, &rrowv = R.minor_local;
-  const auto &cval = C.val, &rval = R.val;
+  // built on the device from the resident CSR / CSC (rebk_csr_build.cu)
+  cudaStream_t st;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DevSegLists C, R;
   cudaError_t e = cudaSuccess;
-  if (!e) e = upload_vec(&sp->cseg_off, coff);
-  if (!e) e = upload_vec(&sp->cseg_ptr, cptr);
-  if (!e) e = upload_vec(&sp->cval, cval);
-  if (!e) e = upload_vec(&sp->ccol, ccolv);
-  if (!e) e = upload_vec(&sp->cseg_row, crow);
-  if (!e) e = upload_vec(&sp->cseg_cta, ccta);
-  if (!e) e = upload_vec(&sp->rseg_off, roff);
-  if (!e) e = upload_vec(&sp->rseg_ptr, rptr);
-  if (!e) e = upload_vec(&sp->rval, rval);
-  if (!e) e = upload_vec(&sp->rrow, rrowv);
-  if (!e) e = upload_vec(&sp->rseg_col, rcol);
-  if (!e) e = upload_vec(&sp->rseg_cta, rcta);
+  // column blocks -> row segments into CSR
+  if (extended) e = seg_lists_device(m, ctx->csr_ptr, ctx->csr_col, ctx->csr_val, ctx->nnz, n, t, cfg->col_ptr, G, &C, st);
+  // row blocks -> column segments into CSC
+  if (!e) e = seg_lists_device(n, ctx->csc_ptr, ctx->csc_row, ctx->csc_val, ctx->nnz, m, s, cfg->row_ptr, G, &R, st);
+  if (!e && !extended) {  // RABK / RK / DSBGS: an empty column plan (off = ptr = {0})
+    e = cudaMalloc(&C.off, sizeof(int64_t));
+    if (!e) e = cudaMalloc(&C.ptr, sizeof(int64_t));
+    if (!e) e = cudaMemset(C.off, 0, sizeof(int64_t));
+    if (!e) e = cudaMemset(C.ptr, 0, sizeof(int64_t));
+  }
+  cudaStreamDestroy(st);
+  sp->cseg_off = C.off;
+  sp->cseg_ptr = C.ptr;
+  sp->cval = C.val;
+  sp->ccol = C.minor_local;
+  sp->cseg_row = C.major_id;
+  sp->cseg_cta = C.cta;
+  sp->rseg_off = R.off;
+  sp->rseg_ptr = R.ptr;
+  sp->rval = R.val;
+  sp->rrow = R.minor_local;
+  sp->rseg_col = R.major_id;
+  sp->rseg_cta = R.cta;
   if (e) {
     free_seg_plan(sp);
-    return fail(REBK_ENOMEM, "segment lists upload failed: %s", cudaGetErrorString(e));
+    return fail(REBK_ENOMEM, "segment lists (device build) failed: %s", cudaGetErrorString(e));
   }
   ctx->seg_cache.push_back(sp);
   *out = sp;
@@ -1636,51 +1541,24 @@ int rebk_ctx_create_csr(const int64_t* indptr, const int32_t* indices, const dou
   c->n = n;
   c->lda = n;
   c->nnz = nnz;
-  c->h_csr_ptr.assign(indptr, indptr + m + 1);
-  c->h_csr_col.assign(indices, indices + nnz);
-  // CSC twin (counting sort by column: rows stay ascending within a column).
-  // T host threads own contiguous row ranges; per-(thread, column) counts give
-  // each thread its write offsets, so the twin equals a sequential sort.
-  const int T = (int)std::max<int64_t>(
-      1, std::min<int64_t>({16, (int64_t)std::thread::hardware_concurrency(), nnz / (8 * (n + 1)), m / 4096}));
-  auto lo_of = [&](int th) { return m * th / T; };
-  std::vector<int64_t> cnt((size_t)T * n, 0);
-  parallel_for_threads(T, [&](int th) {
-    int64_t* cc = cnt.data() + (size_t)th * n;
-    for (int64_t e = indptr[lo_of(th)]; e < indptr[lo_of(th + 1)]; ++e) cc[indices[e]]++;
-  });
-  c->h_csc_ptr.assign(n + 1, 0);
-  for (int64_t j = 0; j < n; ++j) {
-    int64_t acc = c->h_csc_ptr[j];
-    for (int th = 0; th < T; ++th) {
-      const int64_t k = cnt[(size_t)th * n + j];
-      cnt[(size_t)th * n + j] = acc;
-      acc += k;
-    }
-    c->h_csc_ptr[j + 1] = acc;
-  }
-  c->h_csc_row.resize(nnz);
-  std::vector<double> csc_val(nnz);
-  parallel_for_threads(T, [&](int th) {
-    int64_t* fill = cnt.data() + (size_t)th * n;
-    for (int64_t i = lo_of(th); i < lo_of(th + 1); ++i)
-      for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
-        const int64_t q = fill[indices[e]]++;
-        c->h_csc_row[q] = (int32_t)i;
-        csc_val[q] = data[e];
-      }
-  });
-  c->h_csr_val.assign(data, data + nnz);
-  c->h_csc_val = std::move(csc_val);
-  cudaError_t e = upload_vec(&c->csr_ptr, c->h_csr_ptr);
-  if (!e) e = upload_vec(&c->csr_col, c->h_csr_col);
-  if (!e) e = upload_vec(&c->csr_val, c->h_csr_val);
-  if (!e) e = upload_vec(&c->csc_ptr, c->h_csc_ptr);
-  if (!e) e = upload_vec(&c->csc_row, c->h_csc_row);
-  if (!e) e = upload_vec(&c->csc_val, c->h_csc_val);
+  // upload the CSR (the caller's buffers; pinned ones copy at full PCIe
+  // rate), then build the CSC twin on the device (rebk_csr_build.cu)
+  cudaError_t e = cudaMalloc(&c->csr_ptr, sizeof(int64_t) * (m + 1));
+  if (!e) e = cudaMalloc(&c->csr_col, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  if (!e) e = cudaMalloc(&c->csr_val, sizeof(double) * std::max<int64_t>(nnz, 1));
+  if (!e) e = cudaMalloc(&c->csc_ptr, sizeof(int64_t) * (n + 1));
+  if (!e) e = cudaMalloc(&c->csc_row, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
+  if (!e) e = cudaMalloc(&c->csc_val, sizeof(double) * std::max<int64_t>(nnz, 1));
+  cudaStream_t st = nullptr;
+  if (!e) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (!e) e = cudaMemcpyAsync(c->csr_ptr, indptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, st);
+  if (!e && nnz) e = cudaMemcpyAsync(c->csr_col, indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st);
+  if (!e && nnz) e = cudaMemcpyAsync(c->csr_val, data, sizeof(double) * nnz, cudaMemcpyHostToDevice, st);
+  if (!e) e = csr_to_csc_device(m, n, nnz, c->csr_ptr, c->csr_col, c->csr_val, c->csc_ptr, c->csc_row, c->csc_val, st);
+  if (st) cudaStreamDestroy(st);
   if (e) {
     rebk_ctx_destroy(c);
-    return fail(REBK_ENOMEM, "CSR upload failed: %s", cudaGetErrorString(e));
+    return fail(REBK_ENOMEM, "CSR upload / CSC twin failed: %s", cudaGetErrorString(e));
   }
   *out = c;
   return REBK_OK;

@@ -294,6 +294,19 @@ cudaError_t stream_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
 cudaError_t launch_shard_stream(const StreamParams& sp, const CUtensorMap& tm_c, const CUtensorMap& tm_r,
                                 size_t smem_bytes, cudaStream_t stream);
 cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream);
+// rebk_csr_build.cu: the sparse context's derived arrays built on the device
+struct DevSegLists {
+  int64_t nseg = 0;
+  int64_t *off = nullptr, *ptr = nullptr, *cta = nullptr;
+  int32_t *major_id = nullptr, *minor_local = nullptr;
+  double* val = nullptr;
+};
+cudaError_t csr_to_csc_device(int64_t m, int64_t n, int64_t nnz, const int64_t* csr_ptr, const int32_t* csr_col,
+                              const double* csr_val, int64_t* csc_ptr, int32_t* csc_row, double* csc_val,
+                              cudaStream_t st);
+cudaError_t seg_lists_device(int64_t nmajor, const int64_t* mptr, const int32_t* minor, const double* vals,
+                             int64_t nnz, int64_t nminor, int64_t nb, const int64_t* bptr_host, int G, DevSegLists* out,
+                             cudaStream_t st);
 cudaError_t csr_kernel_occupancy(int* blocks_per_sm);
 struct MrhsRun {
   const float* A;
