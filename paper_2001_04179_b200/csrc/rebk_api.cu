@@ -445,10 +445,10 @@ cudaError_t upload_vec(T** dst, const std::vector<T>& v) {
 
 void free_seg_plan(CsrSegPlan* sp) {
   if (!sp) return;
-  cudaFree(sp->cseg_off); cudaFree(sp->cseg_ptr); cudaFree(sp->cseg_cta); cudaFree(sp->cseg_row);
-  cudaFree(sp->ccol); cudaFree(sp->cval);
-  cudaFree(sp->rseg_off); cudaFree(sp->rseg_ptr); cudaFree(sp->rseg_cta); cudaFree(sp->rseg_col);
-  cudaFree(sp->rrow); cudaFree(sp->rval);
+  for (void* p : {(void*)sp->cseg_off, (void*)sp->cseg_ptr, (void*)sp->cseg_cta, (void*)sp->cseg_row, (void*)sp->ccol,
+                  (void*)sp->cval, (void*)sp->rseg_off, (void*)sp->rseg_ptr, (void*)sp->rseg_cta, (void*)sp->rseg_col,
+                  (void*)sp->rrow, (void*)sp->rval})
+    pool_free(p);
   delete sp;
 }
 
@@ -483,8 +483,8 @@ int build_seg_plan(rebk_ctx* ctx, const rebk_cfg* cfg, bool extended, int G, Csr
   // row blocks -> column segments into CSC
   if (!e) e = seg_lists_device(n, ctx->csc_ptr, ctx->csc_row, ctx->csc_val, ctx->nnz, m, s, cfg->row_ptr, G, &R, st);
   if (!e && !extended) {  // RABK / RK / DSBGS: an empty column plan (off = ptr = {0})
-    e = cudaMalloc(&C.off, sizeof(int64_t));
-    if (!e) e = cudaMalloc(&C.ptr, sizeof(int64_t));
+    e = pool_malloc(&C.off, 1);
+    if (!e) e = pool_malloc(&C.ptr, 1);
     if (!e) e = cudaMemset(C.off, 0, sizeof(int64_t));
     if (!e) e = cudaMemset(C.ptr, 0, sizeof(int64_t));
   }
@@ -1413,6 +1413,14 @@ int shard_stream_impl(rebk_ctx* ctx, const rebk_cfg* cfg, ShardLaunch& L, const 
 
 namespace rebk {
 int set_error_msg(int code, const char* msg) { return fail(code, "%s", msg); }
+cudaError_t pool_malloc_bytes(void** p, size_t bytes) {
+  cudaError_t e = cudaMallocAsync(p, bytes, cudaStreamPerThread);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamPerThread);
+  return e;
+}
+void pool_free(void* p) {
+  if (p) cudaFreeAsync(p, cudaStreamPerThread);
+}
 bool ctx_dense_view(const rebk_ctx* ctx, const double** A, int64_t* m, int64_t* n, int64_t* lda, int* device) {
   if (!ctx || ctx->kind != 0) return false;
   *A = ctx->A;
@@ -1455,6 +1463,14 @@ static int ctx_common(rebk_ctx* c, int device) {
   if (e != cudaSuccess || ndev == 0) return fail(REBK_ENODEV, "no CUDA device available");
   if (device < 0 || device >= ndev) return fail(REBK_EINVAL, "device %d out of range", device);
   CUDA_TRY(cudaSetDevice(device));
+  {
+    // keep freed pool memory mapped (pool_malloc): see rebk_internal.h
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   CUDA_TRY(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
   c->device = device;
   return REBK_OK;
@@ -1474,7 +1490,7 @@ int rebk_ctx_create_dense(const double* a_host, int64_t m, int64_t n, int64_t ld
   // store with an even leading dimension so every row is 16-byte aligned
   const int64_t ld = (n + 1) & ~(int64_t)1;
   double* dA = nullptr;
-  cudaError_t e = cudaMalloc(&dA, (size_t)m * ld * sizeof(double));
+  cudaError_t e = pool_malloc(&dA, (size_t)m * ld);
   if (e != cudaSuccess) {
     delete c;
     return fail(REBK_ENOMEM, "cudaMalloc(A, %lld bytes): %s", (long long)(m * ld * 8), cudaGetErrorString(e));
@@ -1522,12 +1538,32 @@ int rebk_ctx_create_csr(const int64_t* indptr, const int32_t* indices, const dou
   if (m < 1 || n < 1) return fail(REBK_EINVAL, "matrix must be 2-D and nonempty");
   if (m > INT32_MAX || n > INT32_MAX) return fail(REBK_EINVAL, "matrix dimension exceeds 2^31");
   if (indptr[0] != 0 || indptr[m] != nnz) return fail(REBK_EINVAL, "indptr does not describe nnz entries");
-  for (int64_t i = 0; i < m; ++i) {
-    if (indptr[i + 1] < indptr[i]) return fail(REBK_EINVAL, "indptr must be nondecreasing");
-    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
-      if (indices[e] < 0 || indices[e] >= n) return fail(REBK_EINVAL, "column index out of range");
-      if (e > indptr[i] && indices[e] <= indices[e - 1])
-        return fail(REBK_EINVAL, "column indices must be sorted and unique within a row");
+  {
+    // the reference Matrix's invariants (matrix.py:46-58), checked on up to
+    // 16 host threads over row ranges; the first bad row in row order wins
+    const int T = (int)std::max<int64_t>(1, std::min<int64_t>({16, (int64_t)std::thread::hardware_concurrency(),
+                                                               m / 4096 + 1}));
+    std::vector<int64_t> bad_row(T, INT64_MAX);
+    std::vector<int> bad_kind(T, 0);
+    parallel_for_threads(T, [&](int th) {
+      for (int64_t i = m * th / T; i < m * (th + 1) / T; ++i) {
+        int kind = 0;
+        if (indptr[i + 1] < indptr[i]) kind = 1;
+        for (int64_t e = indptr[i]; !kind && e < indptr[i + 1]; ++e) {
+          if (indices[e] < 0 || indices[e] >= n) kind = 2;
+          else if (e > indptr[i] && indices[e] <= indices[e - 1]) kind = 3;
+        }
+        if (kind) {
+          bad_row[th] = i;
+          bad_kind[th] = kind;
+          return;
+        }
+      }
+    });
+    for (int th = 0; th < T; ++th) {
+      if (bad_kind[th] == 1) return fail(REBK_EINVAL, "indptr must be nondecreasing");
+      if (bad_kind[th] == 2) return fail(REBK_EINVAL, "column index out of range");
+      if (bad_kind[th] == 3) return fail(REBK_EINVAL, "column indices must be sorted and unique within a row");
     }
   }
   rebk_ctx* c = new rebk_ctx{};
@@ -1543,12 +1579,12 @@ int rebk_ctx_create_csr(const int64_t* indptr, const int32_t* indices, const dou
   c->nnz = nnz;
   // upload the CSR (the caller's buffers; pinned ones copy at full PCIe
   // rate), then build the CSC twin on the device (rebk_csr_build.cu)
-  cudaError_t e = cudaMalloc(&c->csr_ptr, sizeof(int64_t) * (m + 1));
-  if (!e) e = cudaMalloc(&c->csr_col, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
-  if (!e) e = cudaMalloc(&c->csr_val, sizeof(double) * std::max<int64_t>(nnz, 1));
-  if (!e) e = cudaMalloc(&c->csc_ptr, sizeof(int64_t) * (n + 1));
-  if (!e) e = cudaMalloc(&c->csc_row, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
-  if (!e) e = cudaMalloc(&c->csc_val, sizeof(double) * std::max<int64_t>(nnz, 1));
+  cudaError_t e = pool_malloc(&c->csr_ptr, m + 1);
+  if (!e) e = pool_malloc(&c->csr_col, nnz);
+  if (!e) e = pool_malloc(&c->csr_val, nnz);
+  if (!e) e = pool_malloc(&c->csc_ptr, n + 1);
+  if (!e) e = pool_malloc(&c->csc_row, nnz);
+  if (!e) e = pool_malloc(&c->csc_val, nnz);
   cudaStream_t st = nullptr;
   if (!e) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   if (!e) e = cudaMemcpyAsync(c->csr_ptr, indptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice, st);
@@ -1576,7 +1612,7 @@ int rebk_ctx_create_dense_f32(const float* a_host, int64_t m, int64_t n, int64_t
     return rc;
   }
   float* dA = nullptr;
-  cudaError_t e = cudaMalloc(&dA, (size_t)m * n * sizeof(float));
+  cudaError_t e = pool_malloc(&dA, (size_t)m * n);
   if (e == cudaSuccess)
     e = cudaMemcpy2D(dA, n * sizeof(float), a_host, lda * sizeof(float), n * sizeof(float), m, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -1676,7 +1712,7 @@ int rebk_run_mrhs(rebk_ctx* ctx, const rebk_cfg* cfg, int64_t nrhs, const float*
         std::lock_guard<std::mutex> lock(ctx->mu);
         if (!ctx->A32t) {
           float* t32 = nullptr;
-          if (cudaMalloc(&t32, sizeof(float) * n * m) == cudaSuccess) {
+          if (pool_malloc(&t32, (size_t)n * m) == cudaSuccess) {
             if (mrhs_transpose_a(ctx->A32, m, n, ctx->lda, t32, m, stream) == cudaSuccess &&
                 cudaStreamSynchronize(stream) == cudaSuccess) {
               ctx->ldat = m;
@@ -1931,20 +1967,13 @@ int rebk_ctx_destroy(rebk_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaFree(ctx->shard_scratch);
   }
-  if (ctx->A32t) cudaFree(ctx->A32t);
-  if (ctx->A32) {
-    cudaSetDevice(ctx->device);
-    cudaFree(ctx->A32);
-  }
   cudaSetDevice(ctx->device);
-  if (ctx->A_owned) cudaFree(ctx->A_owned);
-  cudaFree(ctx->csr_ptr);
-  cudaFree(ctx->csr_col);
-  cudaFree(ctx->csr_val);
-  cudaFree(ctx->csc_ptr);
-  cudaFree(ctx->csc_row);
-  cudaFree(ctx->csc_val);
+  // pool memory (pool_malloc): returned to the device pool, stays mapped
+  for (void* p : {(void*)ctx->A32t, (void*)ctx->A32, (void*)ctx->A_owned, (void*)ctx->csr_ptr, (void*)ctx->csr_col,
+                  (void*)ctx->csr_val, (void*)ctx->csc_ptr, (void*)ctx->csc_row, (void*)ctx->csc_val})
+    pool_free(p);
   for (CsrSegPlan* sp : ctx->seg_cache) free_seg_plan(sp);
+  cudaStreamSynchronize(cudaStreamPerThread);
   delete ctx;
   return REBK_OK;
 }

@@ -269,10 +269,10 @@ cudaError_t seg_lists_device(int64_t nmajor, const int64_t* mptr, const int32_t*
     B_TRY(cub::DeviceRadixSort::SortPairs(tmp2, tb2, key, skey, sidx, order, nseg, 0, bits_for(nb), st));
   }
   // outputs (owned by the plan; cudaFree in free_seg_plan)
-  B_TRY(cudaMalloc(&out->off, sizeof(int64_t) * (nb + 1)));
-  B_TRY(cudaMalloc(&out->major_id, sizeof(int32_t) * std::max<int64_t>(nseg, 1)));
-  B_TRY(cudaMalloc(&out->ptr, sizeof(int64_t) * (nseg + 1)));
-  B_TRY(cudaMalloc(&out->cta, sizeof(int64_t) * nb * (G + 1)));
+  B_TRY(pool_malloc(&out->off, nb + 1));
+  B_TRY(pool_malloc(&out->major_id, nseg));
+  B_TRY(pool_malloc(&out->ptr, nseg + 1));
+  B_TRY(pool_malloc(&out->cta, nb * (G + 1)));
   int64_t* len;
   B_TRY(S.get(&len, nseg));
   if (nseg > 0) {
@@ -292,8 +292,8 @@ cudaError_t seg_lists_device(int64_t nmajor, const int64_t* mptr, const int32_t*
   int64_t nent = 0;
   B_TRY(cudaMemcpyAsync(&nent, out->ptr + nseg, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   B_TRY(cudaStreamSynchronize(st));
-  B_TRY(cudaMalloc(&out->val, sizeof(double) * std::max<int64_t>(nent, 1)));
-  B_TRY(cudaMalloc(&out->minor_local, sizeof(int32_t) * std::max<int64_t>(nent, 1)));
+  B_TRY(pool_malloc(&out->val, nent));
+  B_TRY(pool_malloc(&out->minor_local, nent));
   if (nseg > 0) {
     k_seg_copy<<<(unsigned)((nseg + kTB / 32 - 1) / (kTB / 32)), kTB, 0, st>>>(
         nseg, order, start, out->ptr, skey, bptr, minor, vals, out->val, out->minor_local);

@@ -294,6 +294,16 @@ cudaError_t stream_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
 cudaError_t launch_shard_stream(const StreamParams& sp, const CUtensorMap& tm_c, const CUtensorMap& tm_r,
                                 size_t smem_bytes, cudaStream_t stream);
 cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream);
+// Device memory that outlives one call (context arrays, cached plans): taken
+// from the device's default memory pool, whose release threshold is raised
+// when the first context is created, so a context created and destroyed per
+// solve reuses mapped memory instead of paying cudaMalloc/cudaFree each time
+cudaError_t pool_malloc_bytes(void** p, size_t bytes);
+void pool_free(void* p);
+template <class T>
+inline cudaError_t pool_malloc(T** p, size_t count) {
+  return pool_malloc_bytes(reinterpret_cast<void**>(p), (count > 0 ? count : 1) * sizeof(T));
+}
 // rebk_csr_build.cu: the sparse context's derived arrays built on the device
 struct DevSegLists {
   int64_t nseg = 0;
