@@ -452,6 +452,14 @@ void free_seg_plan(CsrSegPlan* sp) {
   delete sp;
 }
 
+template <class F>
+void parallel_for_threads(int T, F&& f) {
+  std::vector<std::thread> pool;
+  for (int th = 1; th < T; ++th) pool.emplace_back(f, th);
+  f(0);
+  for (auto& t : pool) t.join();
+}
+
 // Segment lists of one partition: for every column block, the rows with
 // nonzeros in it and their [lo, hi) range in the CSR arrays (sorted by row);
 // for every row block, the columns with nonzeros in it and their range in the
