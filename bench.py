@@ -838,6 +838,31 @@ def run_ours_c3_sharded(args):
     stream = torch.cuda.Stream(device=dev)
     x_d = torch.zeros(n, dtype=torch.float64, device=dev)
     z_d = torch.empty_like(b_local)
+    fallback_reason = None
+    xchg = dm = comm = None
+    if not host_driver:
+        # the in-kernel exchange; if its setup or first solve fails on any
+        # rank (e.g. CUDA IPC refused), every rank falls back to the
+        # host-driven NCCL loop and the line says so
+        ok = 1
+        try:
+            c = wl.cfg("oracle_error", tol, args.max_iters)
+            xchg = ShardExchange(ws, rank, int(np.diff(wl.col_ptr).max()), n, local, dist.all_gather_object)
+            dm = DeviceMatrix.from_device_pointer(a_local.data_ptr(), a_local.shape[0], n, n, local)
+            with torch.cuda.stream(stream):
+                x_d.zero_()
+                z_d.copy_(b_local)
+            xchg.run(dm, c, ranges, b_local.data_ptr(), wl.x_star.data_ptr(), x_d.data_ptr(), z_d.data_ptr(),
+                     stream.cuda_stream)
+        except Exception as exc:  # pragma: no cover - exercised only on a failing multi-GPU box
+            ok = 0
+            fallback_reason = f"rank {rank}: {type(exc).__name__}: {exc}"
+            log(f"[bench] in-kernel exchange unavailable, falling back to the NCCL driver: {fallback_reason}")
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            host_driver = True
+            fallback_reason = fallback_reason or "another rank's in-kernel exchange failed"
     if host_driver:
         c = wl.cfg("max_iters_only", 1.0, args.max_iters)
         picks = np.empty((args.max_iters, 2), dtype=np.int32)
@@ -848,10 +873,6 @@ def run_ours_c3_sharded(args):
         uid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = NcclComm(uid[0], ws, rank, local)
-    else:
-        c = wl.cfg("oracle_error", tol, args.max_iters)
-        xchg = ShardExchange(ws, rank, int(np.diff(wl.col_ptr).max()), n, local, dist.all_gather_object)
-        dm = DeviceMatrix.from_device_pointer(a_local.data_ptr(), a_local.shape[0], n, n, local)
 
     def solve():
         if host_driver:
@@ -958,7 +979,8 @@ def run_ours_c3_sharded(args):
                                    "rebk_shard_run (C++ issue loop, ncclAllReduce per iteration)" if host_driver else
                                    "rebk_shard_stream_kernel: one persistent kernel per rank per solve, u and dx "
                                    "exchanged in-kernel through peer memory (CUDA IPC) with release flags"),
-                        "grid_ctas_per_rank": int(getattr(xchg, "grid_ctas", 0)) if not host_driver else None},
+                        "grid_ctas_per_rank": int(getattr(xchg, "grid_ctas", 0)) if not host_driver else None,
+                        "fallback_reason": fallback_reason},
             "time_to_tol_s": secs / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * ws, "unit": "GB/s",
                          "frac": achieved / (peak * ws), "traffic": None,
@@ -971,11 +993,9 @@ def run_ours_c3_sharded(args):
         }
         os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.barrier()
-    if host_driver:
-        comm.close()
-    else:
-        dm.close()
-        xchg.close()
+    for obj in (comm, dm, xchg):
+        if obj is not None:
+            obj.close()
     dist.destroy_process_group()
     return 0
 
