@@ -137,6 +137,29 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def measured_read_peaks():
+    """L2 and HBM read bandwidth measured on this pool's B200 by
+    tools/l2_bw.cu (profiles/r02_l2_bw.json): {buffer MB: GB/s}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_l2_bw.json")) as fh:
+            pts = json.load(fh)["points"]
+        return {int(p["buffer_mb"]): float(p["read_gbs"]) for p in pts}
+    except Exception:
+        return {}
+
+
+def l2_roofline(a_bytes):
+    """(peak GB/s, source) of the L2 read bandwidth for an A of a_bytes, or
+    None when A does not fit the 126 MB L2."""
+    pts = measured_read_peaks()
+    if a_bytes > 96e6 or not pts:
+        return None
+    mb = min((k for k in pts if k < 1000 and k * 2**20 >= a_bytes), default=None)
+    if mb is None:
+        return None
+    return pts[mb], f"measured L2 read bandwidth, {mb} MB buffer (tools/l2_bw.cu, profiles/r02_l2_bw.json)"
+
+
 def profiled_traffic(workload):
     """dram bytes per launch from the committed ncu --set full summary, if any."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -429,6 +452,12 @@ def run_ours(args):
     kernel_ms = loop_ms_total / args.steps
     achieved = bytes_per_iter * per_solve_iters / (kernel_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
+    bound = "hbm"
+    a_bytes = (prob.a.nnz * 12 * 2) if prob.a.is_sparse else m * n * 8
+    l2 = l2_roofline(a_bytes)
+    if l2 is not None:  # A stays in L2 between iterations (C1): the L2 roofline applies
+        peak, peak_src = l2
+        bound = "l2"
     tr_info = profiled_traffic(args.workload)
     traffic = None
     if isinstance(tr_info, dict) and tr_info.get("bytes_per_iter"):
@@ -510,7 +539,7 @@ def run_ours(args):
                                         "rebk_dense_stream_kernel (TMA ring)"][int(tr.kernel_path)]},
             "time_to_tol_s": ms_max / args.steps / 1e3,
             "achieved_gbps": achieved,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_note": (tr_info or {}).get("note") if isinstance(tr_info, dict) else None,
                          "kernel": ["rebk_dense_kernel", "rebk_dense_fast_kernel", "rebk_dense_fast_kernel",
@@ -767,7 +796,10 @@ def run_ours_c3(args):
                      "iters_per_launch": per_solve, "kernel_ms_per_launch": kernel_ms,
                      "two_pass_cap": two_pass_cap(wl),
                      "note": "the 800 MB column block cannot stay on chip between the u sum and the z update, so it "
-                             "is read twice per iteration: frac <= two_pass_cap by construction"},
+                             "is read twice per iteration: frac <= two_pass_cap by construction",
+                     "read_peak_gbs": measured_read_peaks().get(4096),
+                     "read_peak_note": "pure-read HBM bandwidth measured by tools/l2_bw.cu (4 GB buffer); this kernel "
+                                       "only reads A, so this is the tighter ceiling for it"},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 2 * args.steps, "clocks": clk,
     }
     print(json.dumps(line), flush=True)
