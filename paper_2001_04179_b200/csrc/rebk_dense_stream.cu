@@ -198,10 +198,14 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   // first pass read most recently are the ones still in L2 (an LRU cache
   // re-read in the same order would miss on all of them)
   const bool rev = sp.reverse != 0;
-  auto issue = [&](const Cursor& c, int stage) {  // thread 0
+  // the box of cursor c: tensor map, coordinates (x0 = column, y0 = row), bytes
+  struct Box {
+    const CUtensorMap* map;
+    int x0, y0;
+    uint32_t bytes;
+  };
+  auto box_of = [&](const Cursor& c) -> Box {
     const Plan& pl = plan_of(c.k);
-    fence_proxy_async();
-    double* dst = sm + (size_t)stage * SD;
     if (c.ph < 2) {
       const int nsc = cdiv(span_c(pl), cw), nrc = cdiv(nR, ch);
       // C1 walks subtile-major (column sums accumulate down the rows),
@@ -209,27 +213,33 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
       const int s = c.ph == 0 ? c.i / nrc : c.i % nsc;
       int rc = c.ph == 0 ? c.i % nrc : c.i / nsc;
       if (c.ph == 1 && rev) rc = nrc - 1 - rc;  // C2 from the rows C1 read last (still in L2)
-      mbar_arrive_expect_tx(&sbar[stage], (uint32_t)(cw * ch * 8));
-      if (l2hint)
-        tma_load_2d_hint(dst, &tm_c, (pl.c_lo & ~1) + s * cw, rbase + zr0 + rc * ch, &sbar[stage], pol_first);
-      else
-        tma_load_2d(dst, &tm_c, (pl.c_lo & ~1) + s * cw, rbase + zr0 + rc * ch, &sbar[stage]);
-    } else {
-      const int nsr = cdiv(nC, rw), nrr = cdiv(r_hi(pl) - r_lo(pl), rh);
-      // R1 row-chunk-major (row dots), R2 subtile-major (column sums)
-      const int s = c.ph == 2 ? c.i % nsr : c.i / nrr;
-      int rr = c.ph == 2 ? c.i / nsr : c.i % nrr;
-      if (c.ph == 3 && rev) rr = nrr - 1 - rr;  // R2 from the rows R1 read last
-      mbar_arrive_expect_tx(&sbar[stage], (uint32_t)(rw * rh * 8));
-      if (l2hint)
-        tma_load_2d_hint(dst, &tm_r, xq0 + s * rw, rbase + r_lo(pl) + rr * rh, &sbar[stage],
-                         c.ph == 2 ? pol_last : pol_first);
-      else
-        tma_load_2d(dst, &tm_r, xq0 + s * rw, rbase + r_lo(pl) + rr * rh, &sbar[stage]);
+      return Box{&tm_c, (pl.c_lo & ~1) + s * cw, rbase + zr0 + rc * ch, (uint32_t)(cw * ch * 8)};
     }
+    const int nsr = cdiv(nC, rw), nrr = cdiv(r_hi(pl) - r_lo(pl), rh);
+    // R1 row-chunk-major (row dots), R2 subtile-major (column sums)
+    const int s = c.ph == 2 ? c.i % nsr : c.i / nrr;
+    int rr = c.ph == 2 ? c.i / nsr : c.i % nrr;
+    if (c.ph == 3 && rev) rr = nrr - 1 - rr;  // R2 from the rows R1 read last
+    return Box{&tm_r, xq0 + s * rw, rbase + r_lo(pl) + rr * rh, (uint32_t)(rw * rh * 8)};
+  };
+  auto issue = [&](const Cursor& c, int stage) {  // thread 0
+    fence_proxy_async();
+    double* dst = sm + (size_t)stage * SD;
+    const Box bx = box_of(c);
+    mbar_arrive_expect_tx(&sbar[stage], bx.bytes);
+    if (l2hint)
+      tma_load_2d_hint(dst, bx.map, bx.x0, bx.y0, &sbar[stage], (c.ph == 2) ? pol_last : pol_first);
+    else
+      tma_load_2d(dst, bx.map, bx.x0, bx.y0, &sbar[stage]);
   };
   Cursor prod{p.k_begin, 0, 0};
   int64_t produced = 0, consumed = 0;
+  // L2 prefetch runs PF boxes ahead of the loads: HBM keeps streaming the
+  // next boxes into L2 while the CTA waits at a grid barrier (the ring alone
+  // only covers NS boxes, ~4 us of HBM time for the whole grid)
+  const int PF = sp.prefetch;
+  Cursor pfc{p.k_begin, 0, 0};
+  int64_t prefetched = 0;
   auto refill = [&]() {  // thread 0: keep NS boxes in flight
     if (tid != 0) return;
     settle(prod);
@@ -238,6 +248,20 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
       ++produced;
       ++prod.i;
       settle(prod);
+    }
+    if (PF > 0) {
+      if (prefetched < produced) {  // never prefetch what is already loading
+        pfc = prod;
+        prefetched = produced;
+      }
+      settle(pfc);
+      while (pfc.k <= p.k_end && prefetched < produced + PF) {
+        const Box bx = box_of(pfc);
+        tma_prefetch_l2_2d(bx.map, bx.x0, bx.y0);
+        ++prefetched;
+        ++pfc.i;
+        settle(pfc);
+      }
     }
   };
   // consumer: wait for the next box, hand it to f, release its stage

@@ -167,6 +167,8 @@ struct StreamParams {
   int32_t pad_nC, pad_nR, pad_nJ, pad_nI;  // vector areas after the ring (doubles, even)
   int32_t l2hint;   // 1: L2 eviction-priority hints on the TMA loads (REBK_STREAM_L2HINT, default 1)
   int32_t reverse;  // 1: second passes walk their row chunks backwards (REBK_STREAM_REV, default 1)
+  int32_t prefetch; // boxes of L2 prefetch ahead of the TMA loads (REBK_STREAM_PF)
+  int32_t pad1;
 };
 
 // Sparse (CSR + CSC twin) persistent kernel (rebk_csr.cu).
