@@ -234,9 +234,10 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   };
   Cursor prod{p.k_begin, 0, 0};
   int64_t produced = 0, consumed = 0;
-  // L2 prefetch runs PF boxes ahead of the loads: HBM keeps streaming the
-  // next boxes into L2 while the CTA waits at a grid barrier (the ring alone
-  // only covers NS boxes, ~4 us of HBM time for the whole grid)
+  // optional L2 prefetch PF boxes ahead of the loads (REBK_STREAM_PF; off by
+  // default: measured on C3, PF = 4 / 8 boxes ahead cost 295 -> 354 / 496
+  // us per iteration, the prefetched lines are evicted before their loads
+  // and the traffic doubles; profiles/r02_pf_ab.txt)
   const int PF = sp.prefetch;
   Cursor pfc{p.k_begin, 0, 0};
   int64_t prefetched = 0;
