@@ -788,6 +788,12 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
   // fast path: clustered kernel (oracle_error / max_iters_only, TMA-able tiles,
   // at least one full cluster).  The choice depends only on the problem shape,
   // partitions and stopping mode, so repeated runs take the same path.
+  // residual_proxy on the fast kernels: they iterate in chunks of
+  // check_stride in max_iters_only mode, and stand-alone residual-check
+  // kernels run between the chunks (launch_residual_check); worth it once a
+  // check covers enough iterations (REBK_RES_MIN_STRIDE, default 8)
+  const bool res_mode = cfg->stop_mode == REBK_STOP_RESIDUAL_PROXY;
+  const bool res_chunks_ok = res_mode && cfg->check_stride >= env_int("REBK_RES_MIN_STRIDE", 8);
   FastGeometry fg;
   bool use_fast = false;
   CUtensorMap tm_ct, tm_rt;
@@ -797,7 +803,7 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
     // TMA boxes start on 16-byte aligned columns: the clustered kernels need
     // even column-block starts (the streaming kernel handles odd ones)
     const bool even_cols = !extended || blocks_even(cfg->n_col_blocks, cfg->col_ptr);
-    if (!force_general && !dsbgs && env_int("REBK_NO_FAST", 0) == 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY && aligned && even_cols && CS >= 1 &&
+    if (!force_general && !dsbgs && env_int("REBK_NO_FAST", 0) == 0 && (!res_mode || res_chunks_ok) && aligned && even_cols && CS >= 1 &&
         G0 >= CS && encode_fn() != nullptr) {
       int NC = std::max(1, G0 / CS);
       for (int attempt = 0; attempt < 3 && NC >= 1; ++attempt) {
@@ -852,7 +858,7 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
   StreamGeometry stg;
   CUtensorMap tm_sc, tm_sr;
   const int stream_env = env_int("REBK_STREAM", 1);  // 0 off, 1 when the general kernel cannot stage, 2 always
-  if (!use_fast && !dsbgs && stream_env != 0 && cfg->stop_mode != REBK_STOP_RESIDUAL_PROXY &&
+  if (!use_fast && !dsbgs && stream_env != 0 && (!res_mode || res_chunks_ok) &&
       (ctx->lda % 2 == 0) && ((uintptr_t)ctx->A % 16 == 0) && encode_fn() != nullptr &&
       (stream_env == 2 || tiles_exceed_smem(geo, extended))) {
     stg = stream_geometry(ctx, cfg, std::min(G0, ctx->sm_count), extended);
@@ -872,7 +878,9 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
   SampleParams sp{};
   rc = upload_sampler(arena, cfg, extended, extended || dsbgs, stream, &sp);
   if (rc) return rc;
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(cfg->max_iters, (int64_t)1 << 20));
+  const bool res_fast = res_mode && (use_fast || use_split || use_stream);
+  const int64_t chunk = res_fast ? cfg->check_stride
+                                 : std::max<int64_t>(1, std::min<int64_t>(cfg->max_iters, (int64_t)1 << 20));
   Plan* d_plan;
   double *d_upart, *d_rpart, *d_u, *d_r, *d_errpart, *d_res = nullptr, *d_errs = nullptr;
   Control* d_ctl;
@@ -902,6 +910,11 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
     CUDA_TRY(cudaMemsetAsync(d_cpr, 0, 2 * (size_t)fg.NC * (2 * fg.nI_max + 1) * sizeof(LLWord), stream));
   }
   if (cfg->stop_mode == REBK_STOP_RESIDUAL_PROXY) CUDA_TRY(arena.alloc(&d_res, ctx->m));
+  double *d_rpart_chk = nullptr, *d_colsq = nullptr;
+  if (res_fast) {
+    CUDA_TRY(arena.alloc(&d_rpart_chk, residual_check_part_len((int)ctx->m, (int)ctx->n)));
+    CUDA_TRY(arena.alloc(&d_colsq, ctx->n));
+  }
   const int64_t errs_cap = (cfg->record_errors && trace && trace->errors) ? trace->errors_cap : 0;
   if (errs_cap > 0) CUDA_TRY(arena.alloc(&d_errs, errs_cap));
   CUDA_TRY(arena.alloc(&d_ctl, 1));
@@ -951,6 +964,10 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
   p.record = errs_cap > 0;
   p.nonfinite_stop = cfg->nonfinite_stop;
   p.dsbgs = dsbgs;
+  if (res_fast) {  // the kernels iterate; the checks are separate launches
+    p.stop_mode = REBK_STOP_MAX_ITERS_ONLY;
+    p.max_iters = INT64_MAX;
+  }
   p.nJ_max = geo.nJ_max;
   p.nI_max = geo.nI_max;
   p.nR_max = geo.nR_max;
@@ -993,7 +1010,14 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
   CUDA_TRY(cudaEventCreate(&ev1));
   cudaError_t err = cudaEventRecord(ev0, stream);
   hm.mark("workspace + uploads");
+  auto res_check = [&](int64_t kc) -> cudaError_t {
+    return launch_residual_check(ctx->A, ctx->lda, (int)ctx->m, (int)ctx->n, x_dev, b_dev, extended ? z_dev : nullptr,
+                                 d_res, d_rpart_chk, d_colsq, cfg->residual_scale > 0.0 ? cfg->residual_scale : 1.0,
+                                 cfg->tol, cfg->nonfinite_stop, errs_cap > 0, d_errs, errs_cap, kc, d_ctl, stream);
+  };
+  if (res_fast && err == cudaSuccess) err = res_check(0);  // check(0), solvers.py:444
   int64_t k = 1;
+  int chunks_since_sync = 0;
   do {
     const int64_t count = std::min(chunk, cfg->max_iters - k + 1);
     if (err == cudaSuccess) err = launch_sample_plan(sp, k, count, d_plan, nullptr, stream);
@@ -1056,7 +1080,15 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
       }
     }
     k += std::max<int64_t>(count, 1);
-    if (err == cudaSuccess && k <= cfg->max_iters) {
+    if (res_fast && err == cudaSuccess) {
+      const int64_t ke = k - 1;  // state of iteration ke: a check on stride, and the for-else final check
+      if (ke % cfg->check_stride == 0 || ke == cfg->max_iters) err = res_check(ke);
+    }
+    // converged runs stop early: the host looks at the device flag after every
+    // chunk (every 32 chunks in residual-check mode, whose launches are short
+    // and return at once once the flag is set)
+    if (err == cudaSuccess && k <= cfg->max_iters && (!res_fast || ++chunks_since_sync >= 32)) {
+      chunks_since_sync = 0;
       int32_t done = 0;
       err = cudaMemcpyAsync(&done, &d_ctl->done, sizeof done, cudaMemcpyDeviceToHost, stream);
       if (err == cudaSuccess) err = cudaStreamSynchronize(stream);
@@ -1107,6 +1139,9 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
             (long long)ctl.iters, ms, 1e3 * ms / it);
     print_prof(h, G, use_split ? split_ncc * fg.CS : G, khz, it);
   }
+  // residual checks between chunks: a run that never stopped ends at max_iters
+  // (the for-else of run(), solvers.py:459-464)
+  if (res_fast && !ctl.converged && !(ctl.nonfinite_at && cfg->nonfinite_stop)) ctl.iters = cfg->max_iters;
   if (trace) {
     trace->iters = ctl.iters;
     trace->converged = ctl.converged;

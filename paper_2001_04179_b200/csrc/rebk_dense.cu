@@ -511,3 +511,83 @@ cudaError_t launch_block_norms(const double* A, int64_t lda, int64_t m, int64_t 
 }
 
 }  // namespace rebk
+
+namespace rebk {
+// ---------------------------------------------------------- residual check
+// The residual_proxy stopping rule of run() (solvers.py:410-421) as stand-
+// alone kernels, for the clustered / split / streaming dense kernels, which
+// run the iterations in chunks of check_stride between these checks:
+//   res = A x - b (+ z),  g = Aᵀ res,  err = ||g|| / (||A||_F ||b||).
+// Fixed-order reductions (warp per row; per-column partials over row chunks
+// summed in chunk order), so a run replays bit for bit.
+namespace {
+constexpr int kResChunk = 256;  // rows per partial of Aᵀ res
+
+__global__ void __launch_bounds__(256) k_res_rows(const double* __restrict__ A, int64_t lda, int m, int n,
+                                                  const double* __restrict__ x, const double* __restrict__ b,
+                                                  const double* __restrict__ z, const Control* ctl,
+                                                  double* __restrict__ res) {
+  if (*((volatile const int32_t*)&ctl->done)) return;
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= m) return;
+  const double* row = A + (int64_t)r * lda;
+  double acc = 0.0;
+  for (int c = lane; c < n; c += 32) acc = fma(__ldg(row + c), __ldcg(x + c), acc);
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) res[r] = acc - __ldg(b + r) + (z ? __ldcg(z + r) : 0.0);
+}
+
+__global__ void __launch_bounds__(256) k_res_cols(const double* __restrict__ A, int64_t lda, int m, int n,
+                                                  const double* __restrict__ res, const Control* ctl,
+                                                  double* __restrict__ part) {
+  if (*((volatile const int32_t*)&ctl->done)) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x, chunk = blockIdx.y;
+  if (c >= n) return;
+  const int r0 = chunk * kResChunk, r1 = min(m, r0 + kResChunk);
+  double acc = 0.0;
+  for (int r = r0; r < r1; ++r) acc = fma(__ldg(A + (int64_t)r * lda + c), __ldcg(res + r), acc);
+  part[(int64_t)chunk * n + c] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_res_norm(int n, int nchunks, const double* __restrict__ part, Control* ctl,
+                                                  double* __restrict__ colsq) {
+  if (*((volatile const int32_t*)&ctl->done)) return;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double g = 0.0;
+  for (int q = 0; q < nchunks; ++q) g += part[(int64_t)q * n + c];
+  colsq[c] = g * g;
+}
+
+__global__ void __launch_bounds__(1024) k_res_decide(int n, const double* __restrict__ colsq, double scale, double tol,
+                                                     int32_t nonfinite_stop, int32_t record, double* errs,
+                                                     int64_t errs_cap, int64_t k, Control* ctl) {
+  __shared__ double red[32];
+  if (*((volatile const int32_t*)&ctl->done)) return;
+  double acc = 0.0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) acc += colsq[c];
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    record_check(ctl, errs, errs_cap, record, sqrt(s) / scale, tol, nonfinite_stop, k);
+  }
+}
+}  // namespace
+
+cudaError_t launch_residual_check(const double* A, int64_t lda, int m, int n, const double* x, const double* b,
+                                  const double* z, double* res, double* part, double* colsq, double scale,
+                                  double tol, int32_t nonfinite_stop, int32_t record, double* errs, int64_t errs_cap,
+                                  int64_t k, Control* ctl, cudaStream_t st) {
+  k_res_rows<<<(unsigned)((m + 7) / 8), 256, 0, st>>>(A, lda, m, n, x, b, z, ctl, res);
+  const int nchunks = (m + kResChunk - 1) / kResChunk;
+  k_res_cols<<<dim3((unsigned)((n + 255) / 256), (unsigned)nchunks), 256, 0, st>>>(A, lda, m, n, res, ctl, part);
+  k_res_norm<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, nchunks, part, ctl, colsq);
+  k_res_decide<<<1, 1024, 0, st>>>(n, colsq, scale, tol, nonfinite_stop, record, errs, errs_cap, k, ctl);
+  return cudaGetLastError();
+}
+
+size_t residual_check_part_len(int m, int n) { return (size_t)((m + kResChunk - 1) / kResChunk) * n; }
+}  // namespace rebk

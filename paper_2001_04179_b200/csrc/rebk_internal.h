@@ -283,6 +283,12 @@ __host__ __device__ inline int32_t split_rows(int64_t len, int32_t G, int32_t g)
 cudaError_t launch_sample_plan(const SampleParams& sp, int64_t k0, int64_t count, Plan* plan,
                                int32_t* picks_out, cudaStream_t stream);
 cudaError_t launch_dense(const DenseParams& p, int G, size_t smem_bytes, cudaStream_t stream);
+// residual_proxy check between chunks of the fast dense kernels (rebk_dense.cu)
+cudaError_t launch_residual_check(const double* A, int64_t lda, int m, int n, const double* x, const double* b,
+                                  const double* z, double* res, double* part, double* colsq, double scale,
+                                  double tol, int32_t nonfinite_stop, int32_t record, double* errs, int64_t errs_cap,
+                                  int64_t k, Control* ctl, cudaStream_t st);
+size_t residual_check_part_len(int m, int n);
 cudaError_t dense_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
 cudaError_t launch_dense_fast(const FastParams& fp, const CUtensorMap& tm_ct, const CUtensorMap& tm_rt, int G,
                               int cluster_size, size_t smem_bytes, cudaStream_t stream);

@@ -6,6 +6,7 @@ makes the C-ABI stop with REBK_ENONFINITE), and the explicit report of the
 multi-RHS library path."""
 
 import ctypes
+import os
 import threading
 import warnings
 
@@ -163,3 +164,36 @@ def test_multi_rhs_library_path_is_reported():
         tr = run_multi(a32, b32, cfg)
     assert tr.kernel_path in (4, 5)
     assert any("cuBLAS" in str(x.message) for x in w)
+
+
+@pytest.mark.parametrize("path_env,expect_path", [({}, 6), ({"REBK_SPLIT": "0"}, 2),
+                                                  ({"REBK_NO_FAST": "1", "REBK_STREAM": "2"}, 7),
+                                                  ({"REBK_RES_MIN_STRIDE": "1000"}, 0)])
+def test_residual_proxy_on_the_fast_kernels(monkeypatch, path_env, expect_path):
+    """residual_proxy stopping (solvers.py:410-421) on the split / fused /
+    streaming kernels: they iterate in chunks of check_stride and stand-alone
+    residual-check kernels decide between the chunks; same ITER, checkpoints,
+    errors and iterates as the oracle (and as the general kernel)."""
+    from oracle.rebk_oracle import OracleSolver
+    from paper_2001_04179_b200.workloads import c1_matrix
+
+    for k, v in path_env.items():
+        monkeypatch.setenv(k, v)
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c1_golden.npz"))
+    a = c1_matrix()
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=g["b"], x_star=g["x_star"], b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    rp, cp = P.contiguous_partition(2000, 100, "row"), P.contiguous_partition(500, 100, "col")
+    tol, stride = 3e-4, 10
+    cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=17, max_iters=3000, row_partition=rp,
+                         col_partition=cp, stop=P.StoppingRule(mode="residual_proxy", tol=tol, check_stride=stride),
+                         record_errors=True, beta_max=float(g["beta"]))
+    tr = P.run(prob, cfg)
+    assert tr.kernel_path == expect_path
+    orc = OracleSolver(a, g["b"], rp.pointers(), cp.pointers(), float(g["alpha"]), "rebk")
+    ref = orc.run(17, 3000, tol, None, stride, "residual_proxy", record=True)
+    assert tr.iters == ref["iters"] and tr.converged == ref["converged"] and ref["converged"]
+    np.testing.assert_array_equal(tr.checkpoints, ref["checkpoints"])
+    np.testing.assert_allclose(tr.errors, ref["errors"], rtol=1e-9)
+    rel = lambda u, v: np.linalg.norm(u - v) / np.linalg.norm(v)
+    assert rel(tr.x, ref["x"]) <= 1e-10 and rel(tr.z, ref["z"]) <= 1e-10
