@@ -184,9 +184,9 @@ def test_residual_proxy_on_the_fast_kernels(monkeypatch, path_env, expect_path):
     prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=g["b"], x_star=g["x_star"], b_perp=None,
                              meta=P.ProblemMeta(0, None, False, 0, 0.0))
     rp, cp = P.contiguous_partition(2000, 100, "row"), P.contiguous_partition(500, 100, "col")
-    tol, stride = 2.3e-3, 10  # first crossing at k = 1820 (the proxy plateaus near 2.3e-3 with z0 = 0)
-    # z0 = 0 (with the default z0 = b the proxy is exactly 0 at k = 0)
-    z0 = np.zeros(2000)
+    tol, stride = 1e-6, 10  # first crossing at k = 390
+    # z0 = b + A v (with the default z0 = b the proxy is exactly 0 at k = 0)
+    z0 = g["b"] + a @ (0.1 * np.random.default_rng(1).standard_normal(500))
     cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=17, max_iters=3000, row_partition=rp,
                          col_partition=cp, stop=P.StoppingRule(mode="residual_proxy", tol=tol, check_stride=stride),
                          record_errors=True, beta_max=float(g["beta"]), z0=z0)
@@ -194,7 +194,7 @@ def test_residual_proxy_on_the_fast_kernels(monkeypatch, path_env, expect_path):
     assert tr.kernel_path == expect_path
     orc = OracleSolver(a, g["b"], rp.pointers(), cp.pointers(), float(g["alpha"]), "rebk")
     ref = orc.run(17, 3000, tol, None, stride, "residual_proxy", z0=z0, record=True)
-    assert ref["iters"] > 100
+    assert ref["iters"] == 390
     assert tr.iters == ref["iters"] and tr.converged == ref["converged"] and ref["converged"]
     np.testing.assert_array_equal(tr.checkpoints, ref["checkpoints"])
     np.testing.assert_allclose(tr.errors, ref["errors"], rtol=1e-9)
