@@ -167,6 +167,10 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     }
   };
 
+  // phase counters only in profiling builds (-DREBK_KERNEL_PROF): at 1024
+  // threads the kernel has 64 registers per thread, and keeping 8 live
+  // 64-bit counters for a runtime flag made it spill
+#ifdef REBK_KERNEL_PROF
   long long prof_acc[8];
   for (int i = 0; i < 8; ++i) prof_acc[i] = 0;
   long long prof_last = clock64();
@@ -176,6 +180,9 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     prof_acc[i] += _t - prof_last;   \
     prof_last = _t;                  \
   }
+#else
+#define PROF(i)
+#endif
   bool finished = false;
   if (p.k_begin == 1 && checking) {
     if (oracle) {
@@ -328,8 +335,10 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
       }
     }
   }
+#ifdef REBK_KERNEL_PROF
   if (p.prof && tid == 0)
     for (int i = 0; i < 8; ++i) p.prof[g * 16 + i] = prof_acc[i];
+#endif
 #undef PROF
 }
 
