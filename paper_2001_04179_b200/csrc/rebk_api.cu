@@ -1065,6 +1065,7 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
         spar.l2hint = env_int("REBK_STREAM_L2HINT", 1);
         spar.reverse = env_int("REBK_STREAM_REV", 1);
         spar.prefetch = env_int("REBK_STREAM_PF", 0);
+        spar.pfence = env_int("REBK_STREAM_PFENCE", 0);
         err = launch_dense_stream(spar, tm_sc, tm_sr, G, stg.smem_bytes, stream);
       } else {
         err = launch_dense(p, G, geo.smem_bytes, stream);
@@ -1367,6 +1368,7 @@ int shard_stream_impl(rebk_ctx* ctx, const rebk_cfg* cfg, ShardLaunch& L, const 
   spar.l2hint = env_int("REBK_STREAM_L2HINT", 1);
   spar.reverse = env_int("REBK_STREAM_REV", 1);
   spar.prefetch = env_int("REBK_STREAM_PF", 0);
+  spar.pfence = env_int("REBK_STREAM_PFENCE", 0);
   RankXchg& X = spar.x;
   X.P = L.P;
   X.rank = L.rank;

@@ -223,7 +223,10 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
     return Box{&tm_r, xq0 + s * rw, rbase + r_lo(pl) + rr * rh, (uint32_t)(rw * rh * 8)};
   };
   auto issue = [&](const Cursor& c, int stage) {  // thread 0
-    fence_proxy_async();
+    // the stage was only READ by the generic proxy (ordered before this by the
+    // take() barrier); a proxy fence is needed only for generic writes that
+    // the async proxy must see, so none here (REBK_STREAM_PFENCE=1 restores it)
+    if (sp.pfence) fence_proxy_async();
     double* dst = sm + (size_t)stage * SD;
     const Box bx = box_of(c);
     mbar_arrive_expect_tx(&sbar[stage], bx.bytes);

@@ -168,7 +168,7 @@ struct StreamParams {
   int32_t l2hint;   // 1: L2 eviction-priority hints on the TMA loads (REBK_STREAM_L2HINT, default 1)
   int32_t reverse;  // 1: second passes walk their row chunks backwards (REBK_STREAM_REV, default 1)
   int32_t prefetch; // boxes of L2 prefetch ahead of the TMA loads (REBK_STREAM_PF)
-  int32_t pad1;
+  int32_t pfence;   // fence.proxy.async before every TMA issue (REBK_STREAM_PFENCE, default 0)
 };
 
 // Sparse (CSR + CSC twin) persistent kernel (rebk_csr.cu).
