@@ -81,6 +81,9 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int P = SH ? X.P : 1;
+  // a single rank has nothing to exchange: the sharded kernel then takes the
+  // single-GPU code paths (same bits, no flags or system-scope fences)
+  const bool XCH = SH && P > 1;
   const int rank = SH ? (X.vranks > 1 ? vr : X.rank) : 0;
   const int m_loc = SH ? X.m[vr] : p.m;
   const int rbase = SH ? X.row_base[vr] : 0;
@@ -488,7 +491,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
       for (int e = g * kStreamWarps + warp; e < nJ; e += G * kStreamWarps) {
         const double s = warp_sum_cg(upart + (int64_t)e * G, G);
         if (lane == 0) {
-          if (SH) {
+          if (XCH) {
             for (int q = 0; q < P; ++q) __stcg(X.inbox_u[q] + ((int64_t)slot * P + rank) * X.nJ_cap + e, s);
           } else {
             __stcg(gu + e, s);
@@ -496,8 +499,8 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
         }
       }
       PROF(3);
-      gsync(true);  // SH: fence at system scope after the bar.sync (see gsync)
-      if (SH) {
+      gsync(XCH);  // exchanging: fence at system scope after the bar.sync (see gsync)
+      if (XCH) {
         // the rank's u partial is complete in every inbox: CTA 0 raises the
         // flag, everyone waits for all P ranks', then sums in rank order
         if (g == 0 && xt >= 0 && xt < P && !s_abort) st_release_sys_u64(flag_at(xt, 0, slot, rank, 0), seq);
@@ -512,7 +515,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
       for (int c = tid; c < W; c += kStreamThreads) {
         double uc = 0.0;
         if (c >= co) {
-          if (SH) {
+          if (XCH) {
             const double* ib = X.inbox_u[rank] + (int64_t)slot * P * X.nJ_cap + (c - co);
             for (int q = 0; q < P; ++q) uc += __ldcg(ib + (int64_t)q * X.nJ_cap);
           } else {
@@ -569,7 +572,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
     for (int c = tid; c < nI; c += kStreamThreads) s_r[c] = __ldcg(gr + c);
     __syncthreads();
     const double rs = pl.r_scale;
-    if (!SH) {
+    if (!XCH) {
       if (nC > 0) colsum_stream(nC, nI, rw, rh, s_r, rev, [&](int c, double acc) { s_x[c] = s_x[c] - rs * acc; });
     } else {
       // this rank's column partials of A[I_p, xq]ᵀ r_p go to CTA g of every
