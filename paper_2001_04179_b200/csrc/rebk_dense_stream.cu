@@ -147,15 +147,19 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
       // the barrier, CTA 0's system-scope flag release covers them all
       if (sysfence) asm volatile("fence.acq_rel.sys;" ::: "memory");
       asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&ctl->bar) : "memory");
-      const unsigned long long t0 = globaltimer_ns();
-      unsigned long long v;
-      while (true) {
+      unsigned long long t0 = 0, v;
+      // the abort checks (another CTA's fault flag, the timeout) run on every
+      // 256th poll only: they add L2 traffic and latency to the spin
+      for (unsigned spins = 0;; ++spins) {
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&ctl->bar) : "memory");
         if (v >= bar_target) break;
-        if (*((volatile int32_t*)&ctl->fault) || globaltimer_ns() - t0 > kXchgTimeoutNs) {
-          atomicExch(&ctl->fault, 2);
-          s_abort = 1;
-          break;
+        if ((spins & 255u) == 255u) {
+          if (t0 == 0) t0 = globaltimer_ns();
+          if (*((volatile int32_t*)&ctl->fault) || globaltimer_ns() - t0 > kXchgTimeoutNs) {
+            atomicExch(&ctl->fault, 2);
+            s_abort = 1;
+            break;
+          }
         }
       }
     }
@@ -326,12 +330,15 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   auto await_all = [&](int kind, int slot, int cta, unsigned long long seq) {
     if (xt >= 0 && xt < P) {
       const unsigned long long* f = flag_at(rank, kind, slot, xt, cta);
-      const unsigned long long t0 = globaltimer_ns();
-      while (ld_acquire_sys_u64(f) < seq) {
-        if (*((volatile int32_t*)&ctl->fault) || globaltimer_ns() - t0 > kXchgTimeoutNs) {
-          atomicExch(&ctl->fault, 2);
-          s_abort = 1;
-          break;
+      unsigned long long t0 = 0;
+      for (unsigned spins = 0; ld_acquire_sys_u64(f) < seq; ++spins) {
+        if ((spins & 255u) == 255u) {
+          if (t0 == 0) t0 = globaltimer_ns();
+          if (*((volatile int32_t*)&ctl->fault) || globaltimer_ns() - t0 > kXchgTimeoutNs) {
+            atomicExch(&ctl->fault, 2);
+            s_abort = 1;
+            break;
+          }
         }
       }
     }
