@@ -910,6 +910,9 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
     CUDA_TRY(cudaMemsetAsync(d_cpr, 0, 2 * (size_t)fg.NC * (2 * fg.nI_max + 1) * sizeof(LLWord), stream));
   }
   if (cfg->stop_mode == REBK_STOP_RESIDUAL_PROXY) CUDA_TRY(arena.alloc(&d_res, ctx->m));
+  // streaming kernel: z before the latest column sweep (its column sweep runs one step ahead of the row sweep)
+  double* d_zprev = nullptr;
+  if (use_stream && extended) CUDA_TRY(arena.alloc(&d_zprev, ctx->m));
   double *d_rpart_chk = nullptr, *d_colsq = nullptr;
   if (res_fast) {
     CUDA_TRY(arena.alloc(&d_rpart_chk, residual_check_part_len((int)ctx->m, (int)ctx->n)));
@@ -1066,6 +1069,10 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
         spar.reverse = env_int("REBK_STREAM_REV", 1);
         spar.prefetch = env_int("REBK_STREAM_PF", 0);
         spar.pfence = env_int("REBK_STREAM_PFENCE", 0);
+        spar.dbg = env_int("REBK_STREAM_DBG", 0);
+        spar.order = env_int("REBK_STREAM_ORDER", 0);
+  spar.tail = env_int("REBK_STREAM_TAIL", 0);
+        spar.zprev = d_zprev;
         err = launch_dense_stream(spar, tm_sc, tm_sr, G, stg.smem_bytes, stream);
       } else {
         err = launch_dense(p, G, geo.smem_bytes, stream);
@@ -1369,6 +1376,12 @@ int shard_stream_impl(rebk_ctx* ctx, const rebk_cfg* cfg, ShardLaunch& L, const 
   spar.reverse = env_int("REBK_STREAM_REV", 1);
   spar.prefetch = env_int("REBK_STREAM_PF", 0);
   spar.pfence = env_int("REBK_STREAM_PFENCE", 0);
+  spar.dbg = env_int("REBK_STREAM_DBG", 0);
+  spar.order = env_int("REBK_STREAM_ORDER", 0);
+  spar.tail = env_int("REBK_STREAM_TAIL", 0);
+  double* d_zprev = nullptr;
+  if (extended) CUDA_TRY(arena.alloc(&d_zprev, ctx->m));
+  spar.zprev = d_zprev;
   RankXchg& X = spar.x;
   X.P = L.P;
   X.rank = L.rank;
@@ -1450,7 +1463,9 @@ int shard_stream_impl(rebk_ctx* ctx, const rebk_cfg* cfg, ShardLaunch& L, const 
     trace->kernel_path = 9;
     trace->nonfinite_at = ctl[0].nonfinite_at - 1;
   }
-  L.seq_base += (unsigned long long)ctl[0].iters;  // exchanges this solve completed
+  // sequence numbers this solve used: the column sweep runs one step ahead of
+  // the row sweep, so a run stopped at iteration K has exchanged u up to K + 1
+  L.seq_base += (unsigned long long)ctl[0].iters + 2;
   if (ctl[0].nonfinite_at && cfg->nonfinite_stop)
     return fail(REBK_ENONFINITE, "non-finite error at the check of iteration %lld", (long long)(ctl[0].nonfinite_at - 1));
   return REBK_OK;

@@ -3,10 +3,23 @@
 // a CTA's slice of the column block is ~1350 rows x 500 = 5.4 MB).
 //
 // Same iteration, ownership and reductions as rebk_dense.cu (step_rebk,
-// solvers.py:324-337; P1..P5 with 4 grid barriers; partial sums stored
-// transposed and summed in fixed order, so runs replay bit for bit).  What
-// changes is the data movement: every pass over a block is a stream of TMA
-// boxes through a ring of NS shared-memory stages, each on its own mbarrier.
+// solvers.py:324-337; partial sums stored transposed and summed in fixed
+// order, so runs replay bit for bit).  What changes is the data movement:
+// every pass over a block is a stream of TMA boxes through a ring of NS
+// shared-memory stages, each on its own mbarrier.
+//
+// Schedule: in step_rebk the z sequence never depends on x, and the row sweep
+// of iteration k needs only z_k[I_k].  So the two sweeps are software-
+// pipelined one iteration apart and share their grid barriers: step s runs
+//   X:  C1(s)  u partials          +  R1(s-1)  r partials     -> barrier, both sums
+//   Y:  R2(s-1) x update           +  C2(s)    z update       (after a 2nd barrier)
+// i.e. two grid barriers per iteration instead of four, and the row sweep's
+// 160 MB ride in the column sweep's HBM stream instead of being two short
+// phases of their own.  No barrier is needed between Y and the next X: C1 and
+// R1 read only the CTA's own z rows / x columns, and the partial buffers they
+// write were last read before the second barrier.  A stop decided for
+// x_{s-2} (after the first barrier of step s) needs z_{s-2}, one column sweep
+// back: C2 also stores the z it replaces (StreamParams.zprev).
 // The chunk sequence of a whole run is known in advance (the block plan), so
 // thread 0 keeps NS boxes in flight across phases and grid barriers: while a
 // CTA waits at a barrier, the first boxes of the next pass are already
@@ -38,14 +51,6 @@ namespace rebk {
 
 constexpr int kStreamThreads = 512;
 constexpr int kStreamWarps = kStreamThreads / 32;
-
-// position in the run's box sequence: iteration k, phase (0 C1, 1 C2, 2 R1,
-// 3 R2), box index i within the phase
-struct Cursor {
-  int64_t k;
-  int ph;
-  int i;
-};
 
 __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -90,6 +95,7 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   const int64_t wso = SH ? (int64_t)vr * X.ws_stride : 0;
   const double* gb = p.b + rbase;
   double* gz = p.z ? p.z + rbase : nullptr;
+  double* gzp = sp.zprev ? sp.zprev + rbase : nullptr;  // z before the latest column sweep (exact stop state)
   double* gx = p.x + (SH ? (int64_t)vr * X.x_stride : 0);
   double* upart = p.upart + wso;
   double* rpart = p.rpart + wso;
@@ -177,111 +183,157 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
   // odd column is loaded from the even column before it (span = nJ + 1, the
   // extra leading column is weighted by zero / dropped)
   auto span_c = [](const Plan& pl) { return pl.c_hi - pl.c_lo + (pl.c_lo & 1); };
-  auto boxes = [&](int64_t k, int ph) -> int {
-    const Plan& pl = plan_of(k);
-    if (ph < 2) {
-      if (!p.extended || nR <= 0) return 0;
-      return cdiv(span_c(pl), cw) * cdiv(nR, ch);
-    }
-    if (nC <= 0) return 0;
-    return cdiv(r_hi(pl) - r_lo(pl), rh) * cdiv(nC, rw);
-  };
-  // skip empty phases; k > k_end means the walk is over
-  auto settle = [&](Cursor& c) {
-    while (c.k <= p.k_end && c.i >= boxes(c.k, c.ph)) {
-      c.i = 0;
-      if (++c.ph == 4) {
-        c.ph = 0;
-        ++c.k;
-      }
-    }
-  };
+  // the row sweep runs `skew` steps behind the column sweep
+  const int skew = p.extended ? 1 : 0;
+  const int64_t s_end = p.k_end + skew;  // last step of this launch
+  auto col_active = [&](int64_t s) { return p.extended && s <= p.k_end; };
+  auto row_active = [&](int64_t s) { return s - skew >= p.k_begin; };
+  // pass order within the two phases of a step (sp.order): 0 = C1 R1 | R2 C2
+  // (R2 right behind R1: its 80 MB are still in L2), 1 = R1 C1 | C2 R2 (C2
+  // right behind C1; R1's lines are loaded evict_last to survive the column
+  // passes).  kind: 0 C1, 1 R1, 2 R2, 3 C2
+  const int order = sp.order ? 1 : 0;
+  auto kind_of = [&](int ph) -> int { return order ? (ph ^ 1) : ph; };
   // L2 policy per pass: R1 -> evict_last (R2 reads the same 80 MB right
-  // after), the column passes and R2 -> evict_first (each byte is read once
-  // in the pass; keeping it would push R1's lines out before R2)
+  // after, across the two barriers), the column passes and R2 -> evict_first
+  // (each byte is read once in the pass; keeping it would push R1's lines out
+  // before R2)
   const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
   const int l2hint = sp.l2hint;
   // second passes (C2, R2) walk their row chunks last-to-first: the boxes the
   // first pass read most recently are the ones still in L2 (an LRU cache
   // re-read in the same order would miss on all of them)
   const bool rev = sp.reverse != 0;
-  // the box of cursor c: tensor map, coordinates (x0 = column, y0 = row), bytes
-  struct Box {
+  // C1's last `tail` row chunks are the first ones C2 (walking backwards)
+  // reads again: they are loaded evict_last so they are still in L2 then
+  const int tail = rev ? sp.tail : 0;
+
+  // ---- producer (thread 0): the walk over the run's boxes as an incremental
+  // state machine.  A pass is a nest of two counters (in: fastest); box
+  // coordinates advance by per-pass steps, so issuing a box costs a handful
+  // of instructions (no divisions, no plan lookups) on the consumers' critical
+  // path; the per-pass setup runs four times per step.
+  //   C1 (kind 0): subtile-major   (out = column subtile, in = row chunk; column sums run down the rows)
+  //   C2 (kind 3): row-chunk-major (out = row chunk, in = subtile; row dots run across the subtiles)
+  //   R1 (kind 1): row-chunk-major, R2 (kind 2): subtile-major
+  struct Walk {
+    int64_t k;   // step
+    int ph;      // phase position 0..3 within the step
+    int in, out, n_in, n_out;
+    int x, y;              // coordinates of the next box
+    int xb, yb;            // coordinates at (in, out) = (0, 0)
+    int x_in, y_in, x_out, y_out;  // steps
+    int keep_from;         // in >= keep_from: load evict_last (kind 0); INT_MAX: never; -1: always
     const CUtensorMap* map;
-    int x0, y0;
     uint32_t bytes;
   };
-  auto box_of = [&](const Cursor& c) -> Box {
-    const Plan& pl = plan_of(c.k);
-    if (c.ph < 2) {
+  Walk pw;
+  pw.k = p.k_begin;
+  pw.ph = -1;
+  pw.n_in = pw.n_out = 0;
+  pw.in = pw.out = 0;
+  // set up the pass (k, ph); false if it has no boxes
+  auto walk_setup = [&](Walk& w) -> bool {
+    const int kd = kind_of(w.ph);
+    w.in = w.out = 0;
+    if (kd == 0 || kd == 3) {
+      if (!col_active(w.k) || nR <= 0) return false;
+      const Plan& pl = plan_of(w.k);
       const int nsc = cdiv(span_c(pl), cw), nrc = cdiv(nR, ch);
-      // C1 walks subtile-major (column sums accumulate down the rows),
-      // C2 row-chunk-major (row dots accumulate across the subtiles)
-      const int s = c.ph == 0 ? c.i / nrc : c.i % nsc;
-      int rc = c.ph == 0 ? c.i % nrc : c.i / nsc;
-      if (c.ph == 1 && rev) rc = nrc - 1 - rc;  // C2 from the rows C1 read last (still in L2)
-      return Box{&tm_c, (pl.c_lo & ~1) + s * cw, rbase + zr0 + rc * ch, (uint32_t)(cw * ch * 8)};
+      const int x0 = (pl.c_lo & ~1), y0 = rbase + zr0;
+      w.map = &tm_c;
+      w.bytes = (uint32_t)(cw * ch * 8);
+      if (kd == 0) {
+        w.n_in = nrc, w.n_out = nsc;
+        w.xb = x0, w.yb = y0;
+        w.x_in = 0, w.y_in = ch, w.x_out = cw, w.y_out = 0;
+        w.keep_from = tail > 0 ? nrc - tail : 0x7fffffff;
+      } else {
+        w.n_in = nsc, w.n_out = nrc;
+        w.xb = x0, w.yb = rev ? y0 + (nrc - 1) * ch : y0;
+        w.x_in = cw, w.y_in = 0, w.x_out = 0, w.y_out = rev ? -ch : ch;
+        w.keep_from = 0x7fffffff;
+      }
+    } else {
+      if (!row_active(w.k) || nC <= 0) return false;
+      const Plan& pl = plan_of(w.k - skew);
+      const int nsr = cdiv(nC, rw), nrr = cdiv(r_hi(pl) - r_lo(pl), rh);
+      if (nrr <= 0) return false;
+      const int x0 = xq0, y0 = rbase + r_lo(pl);
+      w.map = &tm_r;
+      w.bytes = (uint32_t)(rw * rh * 8);
+      if (kd == 1) {
+        w.n_in = nsr, w.n_out = nrr;
+        w.xb = x0, w.yb = y0;
+        w.x_in = rw, w.y_in = 0, w.x_out = 0, w.y_out = rh;
+        w.keep_from = -1;
+      } else {
+        w.n_in = nrr, w.n_out = nsr;
+        w.xb = x0, w.yb = rev ? y0 + (nrr - 1) * rh : y0;
+        w.x_in = 0, w.y_in = rev ? -rh : rh, w.x_out = rw, w.y_out = 0;
+        w.keep_from = 0x7fffffff;
+      }
     }
-    const int nsr = cdiv(nC, rw), nrr = cdiv(r_hi(pl) - r_lo(pl), rh);
-    // R1 row-chunk-major (row dots), R2 subtile-major (column sums)
-    const int s = c.ph == 2 ? c.i % nsr : c.i / nrr;
-    int rr = c.ph == 2 ? c.i / nsr : c.i % nrr;
-    if (c.ph == 3 && rev) rr = nrr - 1 - rr;  // R2 from the rows R1 read last
-    return Box{&tm_r, xq0 + s * rw, rbase + r_lo(pl) + rr * rh, (uint32_t)(rw * rh * 8)};
+    w.x = w.xb;
+    w.y = w.yb;
+    return w.n_in > 0 && w.n_out > 0;
   };
-  auto issue = [&](const Cursor& c, int stage) {  // thread 0
-    // the stage was only READ by the generic proxy (ordered before this by the
-    // take() barrier); a proxy fence is needed only for generic writes that
-    // the async proxy must see, so none here (REBK_STREAM_PFENCE=1 restores it)
-    if (sp.pfence) fence_proxy_async();
-    double* dst = sm + (size_t)stage * SD;
-    const Box bx = box_of(c);
-    mbar_arrive_expect_tx(&sbar[stage], bx.bytes);
-    if (l2hint)
-      tma_load_2d_hint(dst, bx.map, bx.x0, bx.y0, &sbar[stage], (c.ph == 2) ? pol_last : pol_first);
-    else
-      tma_load_2d(dst, bx.map, bx.x0, bx.y0, &sbar[stage]);
+  // move to the next non-empty pass; k > s_end means the walk is over
+  auto walk_next_pass = [&](Walk& w) {
+    for (;;) {
+      if (++w.ph == 4) {
+        w.ph = 0;
+        ++w.k;
+      }
+      if (w.k > s_end || walk_setup(w)) return;
+    }
   };
-  Cursor prod{p.k_begin, 0, 0};
-  int64_t produced = 0, consumed = 0;
-  // optional L2 prefetch PF boxes ahead of the loads (REBK_STREAM_PF; off by
-  // default: measured on C3, PF = 4 / 8 boxes ahead cost 295 -> 354 / 496
-  // us per iteration, the prefetched lines are evicted before their loads
-  // and the traffic doubles; profiles/r02_pf_ab.txt)
-  const int PF = sp.prefetch;
-  Cursor pfc{p.k_begin, 0, 0};
-  int64_t prefetched = 0;
-  auto refill = [&]() {  // thread 0: keep NS boxes in flight
+  auto walk_advance = [&](Walk& w) {
+    if (++w.in < w.n_in) {
+      w.x += w.x_in;
+      w.y += w.y_in;
+      return;
+    }
+    w.in = 0;
+    if (++w.out < w.n_out) {
+      w.x = w.xb + w.out * w.x_out;
+      w.y = w.yb + w.out * w.y_out;
+      return;
+    }
+    walk_next_pass(w);
+  };
+  int pstage = 0;          // stage of the next issue
+  int in_flight = 0;       // issued, not yet consumed
+  auto refill = [&]() {    // thread 0: keep NS boxes in flight
     if (tid != 0) return;
-    settle(prod);
-    while (prod.k <= p.k_end && produced < consumed + NS) {
-      issue(prod, (int)(produced % NS));
-      ++produced;
-      ++prod.i;
-      settle(prod);
-    }
-    if (PF > 0) {
-      if (prefetched < produced) {  // never prefetch what is already loading
-        pfc = prod;
-        prefetched = produced;
-      }
-      settle(pfc);
-      while (pfc.k <= p.k_end && prefetched < produced + PF) {
-        const Box bx = box_of(pfc);
-        tma_prefetch_l2_2d(bx.map, bx.x0, bx.y0);
-        ++prefetched;
-        ++pfc.i;
-        settle(pfc);
-      }
+    while (pw.k <= s_end && in_flight < NS) {
+      // the stage was only READ by the generic proxy (ordered before this by
+      // the take() barrier); a proxy fence is needed only for generic writes
+      // the async proxy must see, so none here (REBK_STREAM_PFENCE=1 restores it)
+      if (sp.pfence) fence_proxy_async();
+      double* dst = sm + (size_t)pstage * SD;
+      mbar_arrive_expect_tx(&sbar[pstage], pw.bytes);
+      if (l2hint)
+        tma_load_2d_hint(dst, pw.map, pw.x, pw.y, &sbar[pstage], pw.in >= pw.keep_from ? pol_last : pol_first);
+      else
+        tma_load_2d(dst, pw.map, pw.x, pw.y, &sbar[pstage]);
+      if (++pstage == NS) pstage = 0;
+      ++in_flight;
+      walk_advance(pw);
     }
   };
   // consumer: wait for the next box, hand it to f, release its stage
+  int cstage = 0;
+  uint32_t cphase = 0;
   auto take = [&](auto f) {
-    const int stage = (int)(consumed % NS);
-    mbar_wait(&sbar[stage], (uint32_t)((consumed / NS) & 1));
-    f(sm + (size_t)stage * SD);
+    mbar_wait(&sbar[cstage], cphase);
+    if (!(sp.dbg & 2)) f(sm + (size_t)cstage * SD);  // dbg 2: stream only (timing experiments)
     __syncthreads();  // every reader of this stage is done
-    ++consumed;
+    if (++cstage == NS) {
+      cstage = 0;
+      cphase ^= 1u;
+    }
+    --in_flight;
     refill();
   };
 
@@ -456,74 +508,151 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
     if (SH && s_abort) finished = true;
     else if (decide(0)) finished = true;
   }
-  if (!finished) refill();
+  if (!finished) {
+    if (tid == 0) walk_next_pass(pw);  // the first non-empty pass
+    refill();
+  }
 
   bool pending = false;
   int64_t pending_k = 0;
-  int64_t k = p.k_begin;
-  for (; !finished && k <= p.k_end; ++k) {
-    const Plan pl = plan_of(k);
-    const int rl = r_lo(pl);
-    const int nJ = pl.c_hi - pl.c_lo, nI = r_hi(pl) - rl;
-    const int co = pl.c_lo & 1, W = nJ + co;  // column span of the boxes
-    // exchange sequence number: continues across solves (seq_base = the
+  bool stop_in_loop = false;  // stopped by a decision inside the loop: z is one column sweep ahead of x
+  for (int64_t s = p.k_begin; !finished && s <= s_end; ++s) {
+    const bool colact = col_active(s), rowact = row_active(s);
+    const int64_t kr = s - skew;  // the row sweep's iteration
+    const Plan plc = plan_of(colact ? s : kr);
+    const Plan plr = plan_of(rowact ? kr : s);
+    const int rl = r_lo(plr);
+    const int nJ = plc.c_hi - plc.c_lo, nI = r_hi(plr) - rl;
+    const int co = plc.c_lo & 1, W = nJ + co;  // column span of the boxes
+    // exchange sequence numbers continue across solves (seq_base = the
     // exchanges of earlier solves), so a rank that starts the next solve
     // early writes the other slot than the one a slow peer may still read
-    const unsigned long long seq = seq_base + (unsigned long long)k;
-    const int slot = (int)(seq & 1);
-    const bool check_k = checking && (k % p.stride == 0);
+    const unsigned long long seq_u = seq_base + (unsigned long long)s;
+    const unsigned long long seq_x = seq_base + (unsigned long long)kr;
+    const int slot_u = (int)(seq_u & 1), slot_x = (int)(seq_x & 1);
+    const bool check_k = rowact && checking && (kr % p.stride == 0);
     PROF(0);
-    if (p.extended) {
-      // C1: partial u over owned rows -> upart[e * G + g]
+    // ---- X: C1(s) partial u over owned rows -> upart[e * G + g]
+    auto pass_c1 = [&]() {
+      if (!colact) return;
       if (nR > 0)
         colsum_stream(W, nR, cw, ch, s_z, false, [&](int c, double val) {
           if (c >= co) __stcg(upart + (int64_t)(c - co) * G + g, val);
         });
       else
         for (int c = tid; c < nJ; c += kStreamThreads) __stcg(upart + (int64_t)c * G + g, 0.0);
+    };
+    // R1(kr): partial r over owned columns -> rpart[e * G + g]
+    auto pass_r1 = [&]() {
+      if (!rowact) return;
+      if (nC > 0)
+        rowdot_stream(nC, nI, rw, rh, sp.lr, s_x, false,
+                      [&](int r, double acc) { __stcg(rpart + (int64_t)r * G + g, acc); });
+      else
+        for (int r = tid; r < nI; r += kStreamThreads) __stcg(rpart + (int64_t)r * G + g, 0.0);
+    };
+    if (order == 0) {
+      pass_c1();
       PROF(1);
-      gsync();
-      PROF(2);
-      if (SH && s_abort) {
+      pass_r1();
+    } else {
+      pass_r1();
+      PROF(1);
+      pass_c1();
+    }
+    PROF(6);
+    gsync();
+    PROF(2);
+    if (SH && s_abort) {
+      finished = true;
+      break;
+    }
+    if (pending) {
+      pending = false;
+      if (decide(pending_k)) {
         finished = true;
+        stop_in_loop = true;
         break;
       }
-      if (pending) {
-        pending = false;
-        if (decide(pending_k)) {
-          finished = true;
-          break;
-        }
-      }
+    }
+    if (colact) {
       for (int e = g * kStreamWarps + warp; e < nJ; e += G * kStreamWarps) {
-        const double s = warp_sum_cg(upart + (int64_t)e * G, G);
+        const double sum = warp_sum_cg(upart + (int64_t)e * G, G);
         if (lane == 0) {
           if (XCH) {
-            for (int q = 0; q < P; ++q) __stcg(X.inbox_u[q] + ((int64_t)slot * P + rank) * X.nJ_cap + e, s);
+            for (int q = 0; q < P; ++q) __stcg(X.inbox_u[q] + ((int64_t)slot_u * P + rank) * X.nJ_cap + e, sum);
           } else {
-            __stcg(gu + e, s);
+            __stcg(gu + e, sum);
           }
         }
       }
-      PROF(3);
-      gsync(XCH);  // exchanging: fence at system scope after the bar.sync (see gsync)
-      if (XCH) {
-        // the rank's u partial is complete in every inbox: CTA 0 raises the
-        // flag, everyone waits for all P ranks', then sums in rank order
-        if (g == 0 && xt >= 0 && xt < P && !s_abort) st_release_sys_u64(flag_at(xt, 0, slot, rank, 0), seq);
-        await_all(0, slot, 0, seq);
-        if (s_abort) {
-          finished = true;
-          break;
+    }
+    PROF(3);
+    if (rowact) {
+      // r = (Σ partials - b_I) + z_kr[I]: gz holds z after column sweep kr
+      // (C2 of this step starts only after the next barrier)
+      for (int e = g * kStreamWarps + warp; e < nI; e += G * kStreamWarps) {
+        const double sum = warp_sum_cg(rpart + (int64_t)e * G, G);
+        if (lane == 0) {
+          double rv = sum - __ldg(gb + rl + e);
+          if (p.extended) rv += __ldcg(gz + rl + e);
+          __stcg(gr + e, rv);
         }
       }
-      PROF(4);
-      // C2: z[zr] -= s_J · A[zr, J] u
+    }
+    PROF(8);
+    gsync(XCH && colact);  // exchanging: fence at system scope after the bar.sync (see gsync)
+    if (SH && s_abort) {
+      finished = true;
+      break;
+    }
+    if (XCH && colact) {
+      // the rank's u partial is complete in every inbox: CTA 0 raises the
+      // flag, everyone waits for all P ranks', then sums in rank order
+      if (g == 0 && xt >= 0 && xt < P) st_release_sys_u64(flag_at(xt, 0, slot_u, rank, 0), seq_u);
+      await_all(0, slot_u, 0, seq_u);
+      if (s_abort) {
+        finished = true;
+        break;
+      }
+    }
+    PROF(4);
+    // ---- Y: R2(kr)  x[xq] -= s_I · A[I, xq]ᵀ r
+    const double rs = plr.r_scale;
+    auto pass_r2 = [&]() {
+      if (!rowact) return;
+      for (int c = tid; c < nI; c += kStreamThreads) s_r[c] = __ldcg(gr + c);
+      __syncthreads();
+      if (!XCH) {
+        if (nC > 0) colsum_stream(nC, nI, rw, rh, s_r, rev, [&](int c, double acc) { s_x[c] = s_x[c] - rs * acc; });
+      } else {
+        // this rank's column partials of A[I_p, xq]ᵀ r_p go to CTA g of every
+        // rank (same column slice everywhere); the flags go up now, the sum
+        // over ranks (finish_x) can wait until after C2: the exchange then
+        // hides behind the z pass
+        if (nC > 0) {
+          if (nI > 0) {
+            colsum_stream(nC, nI, rw, rh, s_r, rev, [&](int c, double acc) {
+              for (int q = 0; q < P; ++q) __stcg(X.inbox_x[q] + ((int64_t)slot_x * P + rank) * X.n_cap + xq0 + c, acc);
+            });
+          } else {
+            for (int c = tid; c < nC; c += kStreamThreads)
+              for (int q = 0; q < P; ++q)
+                __stcg(X.inbox_x[q] + ((int64_t)slot_x * P + rank) * X.n_cap + xq0 + c, 0.0);
+          }
+        }
+        publish(1, slot_x, g, seq_x);
+      }
+      __syncthreads();
+    };
+    // C2(s): z[zr] -= s_J · A[zr, J] u
+    auto pass_c2 = [&]() {
+      if (!colact) return;
       for (int c = tid; c < W; c += kStreamThreads) {
         double uc = 0.0;
         if (c >= co) {
           if (XCH) {
-            const double* ib = X.inbox_u[rank] + (int64_t)slot * P * X.nJ_cap + (c - co);
+            const double* ib = X.inbox_u[rank] + (int64_t)slot_u * P * X.nJ_cap + (c - co);
             for (int q = 0; q < P; ++q) uc += __ldcg(ib + (int64_t)q * X.nJ_cap);
           } else {
             uc = __ldcg(gu + c - co);
@@ -532,89 +661,49 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
         s_u[c] = uc;
       }
       __syncthreads();
-      const double cs = pl.c_scale;
+      const double cs = plc.c_scale;
       if (nR > 0)
         rowdot_stream(W, nR, cw, ch, sp.lc, s_u, rev, [&](int r, double acc) {
-          const double zn = s_z[r] - cs * acc;
+          const double zo = s_z[r];
+          const double zn = zo - cs * acc;
           s_z[r] = zn;
           __stcg(gz + zr0 + r, zn);
+          if (checking) __stcg(gzp + zr0 + r, zo);
         });
-      PROF(5);
-    }
-    // R1: partial r over owned columns -> rpart[e * G + g]
-    if (nC > 0)
-      rowdot_stream(nC, nI, rw, rh, sp.lr, s_x, false, [&](int r, double acc) { __stcg(rpart + (int64_t)r * G + g, acc); });
-    else
-      for (int r = tid; r < nI; r += kStreamThreads) __stcg(rpart + (int64_t)r * G + g, 0.0);
-    PROF(6);
-    gsync();
-    PROF(7);
-    if (SH && s_abort) {
-      finished = true;
-      break;
-    }
-    if (!p.extended && pending) {
-      pending = false;
-      if (decide(pending_k)) {
-        finished = true;
-        break;
-      }
-    }
-    for (int e = g * kStreamWarps + warp; e < nI; e += G * kStreamWarps) {
-      const double s = warp_sum_cg(rpart + (int64_t)e * G, G);
-      if (lane == 0) {
-        double rv = s - __ldg(gb + rl + e);
-        if (p.extended) rv += __ldcg(gz + rl + e);
-        __stcg(gr + e, rv);
-      }
-    }
-    PROF(8);
-    gsync();
-    PROF(9);
-    if (SH && s_abort) {
-      finished = true;
-      break;
-    }
-    // R2: x[xq] -= s_I · A[I, xq]ᵀ r
-    for (int c = tid; c < nI; c += kStreamThreads) s_r[c] = __ldcg(gr + c);
-    __syncthreads();
-    const double rs = pl.r_scale;
-    if (!XCH) {
-      if (nC > 0) colsum_stream(nC, nI, rw, rh, s_r, rev, [&](int c, double acc) { s_x[c] = s_x[c] - rs * acc; });
+      // the last row chunk's s_z writes before the next step's C1 reads them
+      // (within the pass, the next take()'s barrier orders them)
+      __syncthreads();
+    };
+    if (order == 0) {
+      pass_r2();
+      PROF(10);
+      pass_c2();
     } else {
-      // this rank's column partials of A[I_p, xq]ᵀ r_p go to CTA g of every
-      // rank (same column slice everywhere); then sum over ranks in order
-      if (nC > 0) {
-        if (nI > 0) {
-          colsum_stream(nC, nI, rw, rh, s_r, rev, [&](int c, double acc) {
-            for (int q = 0; q < P; ++q) __stcg(X.inbox_x[q] + ((int64_t)slot * P + rank) * X.n_cap + xq0 + c, acc);
-          });
-        } else {
-          for (int c = tid; c < nC; c += kStreamThreads)
-            for (int q = 0; q < P; ++q) __stcg(X.inbox_x[q] + ((int64_t)slot * P + rank) * X.n_cap + xq0 + c, 0.0);
-        }
-      }
-      PROF(11);
-      publish(1, slot, g, seq);
-      await_all(1, slot, g, seq);
-      PROF(12);
+      pass_c2();
+      PROF(10);
+      pass_r2();
+    }
+    PROF(5);
+    if (rowact && XCH) {
+      await_all(1, slot_x, g, seq_x);
       if (s_abort) {
         finished = true;
         break;
       }
-      const double* ib = X.inbox_x[rank] + (int64_t)slot * P * X.n_cap + xq0;
+      const double* ib = X.inbox_x[rank] + (int64_t)slot_x * P * X.n_cap + xq0;
       for (int c = tid; c < nC; c += kStreamThreads) {
         double acc = 0.0;
         for (int q = 0; q < P; ++q) acc += __ldcg(ib + (int64_t)q * X.n_cap + c);
         s_x[c] = s_x[c] - rs * acc;
       }
+      __syncthreads();
     }
-    __syncthreads();
-    PROF(10);
+    PROF(12);
+    if (sp.dbg & 1) gsync();
     if (check_k) {
       oracle_partial();
       pending = true;
-      pending_k = k;
+      pending_k = kr;
     }
   }
   if (!finished) {
@@ -638,13 +727,22 @@ __device__ __forceinline__ void stream_body(const StreamParams& sp, const CUtens
     for (int i = 0; i < 16; ++i) p.prof[(int64_t)blockIdx.x * 16 + i] = prof_acc[i];
 #undef PROF
   for (int c = tid; c < nC; c += kStreamThreads) __stcg(gx + xq0 + c, s_x[c]);
-  if (p.extended)
-    for (int r = tid; r < nR; r += kStreamThreads) __stcg(gz + zr0 + r, s_z[r]);
-  // boxes issued for iterations past a stop are still landing: drain them
-  while (consumed < produced) {
-    mbar_wait(&sbar[consumed % NS], (uint32_t)((consumed / NS) & 1));
-    ++consumed;
+  if (p.extended) {
+    // a stop decided inside the loop is for x before the latest column sweep
+    for (int r = tid; r < nR; r += kStreamThreads)
+      __stcg(gz + zr0 + r, stop_in_loop ? __ldcg(gzp + zr0 + r) : s_z[r]);
   }
+  // boxes issued for iterations past a stop are still landing: drain them
+  // (in_flight is tracked by thread 0, the only issuer)
+  if (tid == 0)
+    while (in_flight > 0) {
+      mbar_wait(&sbar[cstage], cphase);
+      if (++cstage == NS) {
+        cstage = 0;
+        cphase ^= 1u;
+      }
+      --in_flight;
+    }
   __syncthreads();
 }
 

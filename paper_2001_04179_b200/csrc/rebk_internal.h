@@ -169,6 +169,10 @@ struct StreamParams {
   int32_t reverse;  // 1: second passes walk their row chunks backwards (REBK_STREAM_REV, default 1)
   int32_t prefetch; // boxes of L2 prefetch ahead of the TMA loads (REBK_STREAM_PF)
   int32_t pfence;   // fence.proxy.async before every TMA issue (REBK_STREAM_PFENCE, default 0)
+  double* zprev;    // [m] z before the latest column sweep (written when a stop can be decided in the loop)
+  int32_t tail;     // C1 row chunks (from the end) loaded evict_last for C2's backward walk (REBK_STREAM_TAIL)
+  int32_t order;    // pass order within a step (REBK_STREAM_ORDER): 0 = C1 R1 | R2 C2, 1 = R1 C1 | C2 R2
+  int32_t dbg;      // REBK_STREAM_DBG experiments (1: a third grid barrier at the end of every step)
 };
 
 // Sparse (CSR + CSC twin) persistent kernel (rebk_csr.cu).

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--col-block", type=int, default=500)
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--solve", action="store_true")
+    ap.add_argument("--ab", default="", help="';'-separated env settings (A=1,B=2;...) timed one after the other")
     args = ap.parse_args()
     m, n = args.m, args.n
     dev = torch.device("cuda", 0)
@@ -108,6 +109,15 @@ def main():
         us = 1e3 * tr.loop_ms / tr.iters
         print(f"[c3] {tr.iters} iterations: {tr.loop_ms:.2f} ms, {us:.1f} us/iter, "
               f"{alg / (us * 1e-6) / 1e9:.0f} GB/s algorithmic, grid {tr.grid_ctas}, path {tr.kernel_path}", flush=True)
+    import os
+    for setting in [v for v in args.ab.split(";") if v or args.ab]:
+        kv = dict(e.split("=") for e in setting.split(",") if e)
+        os.environ.update(kv)
+        run(c)
+        best = min(run(c).loop_ms for _ in range(3))
+        print(f"[c3 ab] {setting or 'default':40s} {1e3 * best / args.iters:8.2f} us/iter", flush=True)
+        for k in kv:
+            del os.environ[k]
     if args.solve:
         tol = 1e-6 * x_star.norm().item()
         tr = run(cfg("oracle_error", tol, 5000))
