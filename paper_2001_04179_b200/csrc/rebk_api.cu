@@ -587,8 +587,16 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
                  double* z_dev, cudaStream_t stream, rebk_trace* trace) {
   const bool extended = cfg->algorithm == REBK_ALGO_REBK || cfg->algorithm == REBK_ALGO_REK;
   CUDA_TRY(cudaSetDevice(ctx->device));
+  // u and r staged in shared memory when the largest blocks fit (REBK_CSR_STAGE=0: gathers from L2)
+  const bool dsbgs_alg = cfg->algorithm == REBK_ALGO_DSBGS;
+  int su_cap = extended ? ((max_block(cfg->n_col_blocks, cfg->col_ptr) + 1) & ~1) : 0;
+  int sr_cap = (max_block(cfg->n_row_blocks, cfg->row_ptr) + 1) & ~1;
+  if (env_int("REBK_CSR_STAGE", 1) == 0) su_cap = sr_cap = 0;
+  if ((size_t)su_cap * 8 > kCsrStageBytesMax / 2) su_cap = 0;
+  if ((size_t)(su_cap + sr_cap) * 8 > kCsrStageBytesMax) sr_cap = 0;
+  (void)dsbgs_alg;
   int occ = 0;
-  CUDA_TRY(csr_kernel_occupancy(&occ));
+  CUDA_TRY(csr_kernel_occupancy((size_t)(su_cap + sr_cap) * 8, &occ));
   int G = cfg->grid_ctas > 0 ? cfg->grid_ctas : grid_override();
   if (G <= 0) G = (int)std::min<int64_t>(std::max<int64_t>(1, (ctx->nnz + 8191) / 8192), (int64_t)ctx->sm_count);
   G = std::max(1, std::min(G, occ * ctx->sm_count));
@@ -666,6 +674,9 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
   p.record = errs_cap > 0;
   p.nonfinite_stop = cfg->nonfinite_stop;
   p.dsbgs = dsbgs;
+  p.l2_prefetch = env_int("REBK_CSR_PF", 1);
+  p.su_cap = su_cap;
+  p.sr_cap = sr_cap;
   p.prof = d_prof;
 
   cudaEvent_t ev0, ev1;

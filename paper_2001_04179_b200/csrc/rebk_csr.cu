@@ -94,6 +94,14 @@ __device__ __forceinline__ double warp_ordered_dot(const double* __restrict__ va
 }
 
 __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
+  // u and r staged per CTA: gathered straight from L2, the few dozen lines
+  // of these short vectors are hammered by every thread of every SM (the z /
+  // x updates are one gather per stored entry), which serialises on their L2
+  // slices; one coalesced copy per CTA and gathers from shared memory instead
+  extern __shared__ __align__(16) double s_vec[];
+  double* s_u = s_vec;
+  double* s_r = s_vec + p.su_cap;
+  const bool st_u = p.su_cap > 0, st_r = p.sr_cap > 0;
   __shared__ double s_red[kCsrWarps];
   __shared__ double s_bcast[2];
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
@@ -167,6 +175,62 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     }
   };
 
+  // ---- L2 prefetch of the block data the coming phases read.  The phases
+  // are chains of dependent loads (segment -> entries -> gathered vector); a
+  // randomly sampled block comes from HBM (A and its copies are several times
+  // L2), so every link of the chain costs a DRAM latency.  The block sequence
+  // is known, and a block's data is a handful of contiguous ranges: while the
+  // row sweep runs (most warps have no row of I), lane 0 of the last four
+  // warps pulls the ranges of the phases that follow into L2 with bulk
+  // prefetches; the chains then run on L2 hits.
+  auto prefetch_range = [&](const void* base, int64_t lo_bytes, int64_t hi_bytes) {
+    const int64_t a = lo_bytes & ~(int64_t)15, b = hi_bytes & ~(int64_t)15;  // stay inside the array
+    const char* q = static_cast<const char*>(base) + a;
+    for (int64_t left = b - a; left > 0; left -= (int64_t)1 << 20, q += (int64_t)1 << 20)
+      bulk_prefetch_l2(q, (uint32_t)(left < ((int64_t)1 << 20) ? left : ((int64_t)1 << 20)));
+  };
+  // this CTA's even share of entries [lo, hi)
+  auto share = [&](int64_t lo, int64_t hi, int64_t& a, int64_t& b) {
+    a = lo + (hi - lo) * g / G;
+    b = lo + (hi - lo) * (g + 1) / G;
+  };
+  // which: 0 = the x update of `cur` (row block copy); 1 = u of `nxt` (CSC
+  // columns of its column block); 2 = the z update of `nxt` (column block
+  // copy); 3 = the row sweep of `nxt` (CSR rows of its row block)
+  auto prefetch_phase_data = [&](int which, const Plan& cur, const Plan* nxt) {
+    if (which == 0) {
+      const int64_t s0 = p.rseg_cta[(int64_t)cur.rb * (G + 1) + g], s1 = p.rseg_cta[(int64_t)cur.rb * (G + 1) + g + 1];
+      if (s1 <= s0) return;
+      prefetch_range(p.rseg_col, s0 * 4, s1 * 4);
+      prefetch_range(p.rseg_ptr, s0 * 8, (s1 + 1) * 8);
+      const int64_t e0 = p.rseg_ptr[s0], e1 = p.rseg_ptr[s1];
+      prefetch_range(p.rval, e0 * 8, e1 * 8);
+      prefetch_range(p.rrow, e0 * 4, e1 * 4);
+    } else if (!nxt) {
+      return;
+    } else if (which == 1) {
+      if (!p.extended) return;
+      int64_t a, b;
+      share(p.csc_ptr[nxt->c_lo], p.csc_ptr[nxt->c_hi], a, b);
+      prefetch_range(p.csc_val, a * 8, b * 8);
+      prefetch_range(p.csc_row, a * 4, b * 4);
+    } else if (which == 2) {
+      if (!p.extended) return;
+      const int64_t s0 = p.cseg_cta[(int64_t)nxt->cb * (G + 1) + g], s1 = p.cseg_cta[(int64_t)nxt->cb * (G + 1) + g + 1];
+      if (s1 <= s0) return;
+      prefetch_range(p.cseg_row, s0 * 4, s1 * 4);
+      prefetch_range(p.cseg_ptr, s0 * 8, (s1 + 1) * 8);
+      const int64_t e0 = p.cseg_ptr[s0], e1 = p.cseg_ptr[s1];
+      prefetch_range(p.cval, e0 * 8, e1 * 8);
+      prefetch_range(p.ccol, e0 * 4, e1 * 4);
+    } else {
+      int64_t a, b;
+      share(p.csr_ptr[nxt->r_lo], p.csr_ptr[nxt->r_hi], a, b);
+      prefetch_range(p.csr_val, a * 8, b * 8);
+      prefetch_range(p.csr_col, a * 4, b * 4);
+    }
+  };
+
   // phase counters only in profiling builds (-DREBK_KERNEL_PROF): at 1024
   // threads the kernel has 64 registers per thread, and keeping 8 live
   // 64-bit counters for a runtime flag made it spill
@@ -205,6 +269,10 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     const Plan pl = p.plan[k - p.k_begin];
     const bool check_k = checking && (k % p.stride == 0);
     // ---- P(k)
+    // u_k (complete since the last barrier) into shared memory; the loads fly
+    // while warp 0 sums the error partials of the pending check
+    if (p.extended && st_u)
+      for (int c = tid; c < pl.c_hi - pl.c_lo; c += kCsrThreads) s_u[c] = __ldcg(p.u + c);
     if (pending) {
       pending = false;
       if (decide(pending_k)) {
@@ -213,6 +281,7 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
       }
     }
     const double cs = pl.c_scale, rs = pl.r_scale;
+    if (p.extended && st_u) __syncthreads();
     PROF(0);
     if (p.extended) {
       const int64_t s0 = p.cseg_cta[(int64_t)pl.cb * (G + 1) + g];
@@ -223,7 +292,10 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
         const double zi = __ldcg(p.z + i);  // issued with the entry loads, not after the sum
         double acc = 0.0;
         const int64_t e1 = p.cseg_ptr[sg + 1];
-        for (int64_t e = p.cseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.cval[e], __ldcg(p.u + p.ccol[e]));
+        if (st_u)
+          for (int64_t e = p.cseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.cval[e], s_u[p.ccol[e]]);
+        else
+          for (int64_t e = p.cseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.cval[e], __ldcg(p.u + p.ccol[e]));
         __stcg(p.z + i, __dsub_rn(zi, __dmul_rn(cs, acc)));
       }
     }
@@ -247,7 +319,8 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
             const int col = p.csr_col[e];
             const double a = p.csr_val[e];
             px[c] = __dmul_rn(a, __ldcg(p.x + col));
-            if (p.extended && col >= pl.c_lo && col < pl.c_hi) pu[c] = __dmul_rn(a, __ldcg(p.u + (col - pl.c_lo)));
+            if (p.extended && col >= pl.c_lo && col < pl.c_hi)
+              pu[c] = __dmul_rn(a, st_u ? s_u[col - pl.c_lo] : __ldcg(p.u + (col - pl.c_lo)));
           }
         }
 #pragma unroll
@@ -272,6 +345,8 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
         __stcg(p.r + (i - pl.r_lo), rv);
       }
     }
+    if (p.l2_prefetch && lane == 0 && warp >= kCsrWarps - 4)
+      prefetch_phase_data(warp - (kCsrWarps - 4), pl, k < p.k_end ? &p.plan[k + 1 - p.k_begin] : nullptr);
     PROF(2);
     gsync();
     PROF(3);
@@ -279,6 +354,10 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     {
       const int64_t s0 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g];
       const int64_t s1 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g + 1];
+      if (st_r) {
+        for (int c = tid; c < pl.r_hi - pl.r_lo; c += kCsrThreads) s_r[c] = __ldcg(p.r + c);
+        __syncthreads();
+      }
       for (int64_t sg = s0 + tid; sg < s1; sg += kCsrThreads) {
         const int j = p.rseg_col[sg];
         // step_dsbgs: only x[J] moves (solvers.py:378-379)
@@ -286,7 +365,10 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
         const double xj = __ldcg(p.x + j);
         double acc = 0.0;
         const int64_t e1 = p.rseg_ptr[sg + 1];
-        for (int64_t e = p.rseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.rval[e], __ldcg(p.r + p.rrow[e]));
+        if (st_r)
+          for (int64_t e = p.rseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.rval[e], s_r[p.rrow[e]]);
+        else
+          for (int64_t e = p.rseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.rval[e], __ldcg(p.r + p.rrow[e]));
         __stcg(p.x + j, __dsub_rn(xj, __dmul_rn(rs, acc)));
       }
     }
@@ -342,14 +424,29 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
 #undef PROF
 }
 
-cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream) {
-  CsrParams pc = p;
-  void* args[] = {&pc};
-  return cudaLaunchCooperativeKernel((const void*)rebk_csr_kernel, dim3(G), dim3(kCsrThreads), args, 0, stream);
+static cudaError_t set_csr_attrs() {
+  static int configured_device = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess || configured_device == dev) return e;
+  e = cudaFuncSetAttribute(rebk_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCsrStageBytesMax);
+  if (e == cudaSuccess) configured_device = dev;
+  return e;
 }
 
-cudaError_t csr_kernel_occupancy(int* blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, rebk_csr_kernel, kCsrThreads, 0);
+cudaError_t launch_csr(const CsrParams& p, int G, cudaStream_t stream) {
+  cudaError_t e = set_csr_attrs();
+  if (e != cudaSuccess) return e;
+  CsrParams pc = p;
+  void* args[] = {&pc};
+  const size_t smem = sizeof(double) * ((size_t)p.su_cap + (size_t)p.sr_cap);
+  return cudaLaunchCooperativeKernel((const void*)rebk_csr_kernel, dim3(G), dim3(kCsrThreads), args, smem, stream);
+}
+
+cudaError_t csr_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm) {
+  cudaError_t e = set_csr_attrs();
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, rebk_csr_kernel, kCsrThreads, smem_bytes);
 }
 
 }  // namespace rebk

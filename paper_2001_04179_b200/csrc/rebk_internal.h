@@ -222,6 +222,8 @@ struct CsrParams {
   int32_t record;
   int32_t nonfinite_stop;
   int32_t dsbgs;  // step_dsbgs: x update restricted to the plan's column block, no z
+  int32_t su_cap, sr_cap;  // u / r staged in shared memory (capacities in doubles, even; 0 = gathered from L2)
+  int32_t l2_prefetch;  // bulk L2 prefetch of the next phases' block data (REBK_CSR_PF, default 1)
   long long* prof;  // optional per-CTA phase cycle counters [G][16] (REBK_PROF=1)
 };
 
@@ -329,7 +331,8 @@ cudaError_t csr_to_csc_device(int64_t m, int64_t n, int64_t nnz, const int64_t* 
 cudaError_t seg_lists_device(int64_t nmajor, const int64_t* mptr, const int32_t* minor, const double* vals,
                              int64_t nnz, int64_t nminor, int64_t nb, const int64_t* bptr_host, int G, DevSegLists* out,
                              cudaStream_t st);
-cudaError_t csr_kernel_occupancy(int* blocks_per_sm);
+cudaError_t csr_kernel_occupancy(size_t smem_bytes, int* blocks_per_sm);
+constexpr size_t kCsrStageBytesMax = 160 * 1024;  // shared memory the CSR kernel may use for the staged u and r
 struct MrhsRun {
   const float* A;
   int64_t m, n, lda;
