@@ -675,6 +675,7 @@ int run_csr_impl(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev, const 
   p.nonfinite_stop = cfg->nonfinite_stop;
   p.dsbgs = dsbgs;
   p.l2_prefetch = env_int("REBK_CSR_PF", 1);
+  p.specialize = env_int("REBK_CSR_SPEC", 1);
   p.su_cap = su_cap;
   p.sr_cap = sr_cap;
   p.prof = d_prof;

@@ -121,14 +121,27 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
   const bool checking = p.stop_mode != 2;
   const bool oracle = p.stop_mode == 0;
 
-  auto oracle_partial = [&]() {
+  // Σ (x_j - x*_j)^2 over this CTA's columns by the warps [w0, 32) (fixed
+  // order: per-thread strided sums, warp butterflies, the warp sums in warp
+  // order); a named barrier of just those warps, so the others can be busy
+  // with something else
+  auto oracle_partial = [&](int w0) {
+    const int T = (kCsrWarps - w0) * 32, t = tid - w0 * 32;
+    if (t < 0) return;
+    named_bar_sync(1, T);  // the group's own x updates are visible
     double acc = 0.0;
-    for (int j = xq0 + tid; j < xq1; j += kCsrThreads) {
+    for (int j = xq0 + t; j < xq1; j += T) {
       const double d = __ldcg(p.x + j) - __ldg(p.xs + j);
       acc = fma(d, d, acc);
     }
-    const double s = csr_block_sum(acc, s_red);
-    if (tid == 0) __stcg(p.errpart + g, s);
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) s_red[warp] = acc;
+    named_bar_sync(1, T);
+    if (t == 0) {
+      double sum = 0.0;
+      for (int w = w0; w < kCsrWarps; ++w) sum += s_red[w];
+      __stcg(p.errpart + g, sum);
+    }
   };
   // ||Aᵀ(Ax - b + z)|| / scale (solvers.py:410-419) through csr/csc matvecs
   auto residual_partials = [&]() {
@@ -250,7 +263,7 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
   bool finished = false;
   if (p.k_begin == 1 && checking) {
     if (oracle) {
-      oracle_partial();
+      oracle_partial(0);
       gsync();
     } else {
       residual_partials();
@@ -283,10 +296,19 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     const double cs = pl.c_scale, rs = pl.r_scale;
     if (p.extended && st_u) __syncthreads();
     PROF(0);
-    if (p.extended) {
+    // The z update of the rows outside I (one thread per segment) and the row
+    // sweep (one warp per row of I) are independent: when the CTA's rows of I
+    // occupy only some warps, the other warps take all the segments and the
+    // two run side by side
+    const int nI = pl.r_hi - pl.r_lo;
+    int nrw = nI > g ? (nI - g + G - 1) / G : 0;  // warps of this CTA with a row of I (rows: CTAs first, then warps)
+    const bool split_p = p.extended && p.specialize && nrw <= kCsrWarps - 8;
+    const int segT = split_p ? (kCsrWarps - nrw) * 32 : kCsrThreads;
+    const int segt = split_p ? tid - nrw * 32 : tid;
+    if (p.extended && segt >= 0) {
       const int64_t s0 = p.cseg_cta[(int64_t)pl.cb * (G + 1) + g];
       const int64_t s1 = p.cseg_cta[(int64_t)pl.cb * (G + 1) + g + 1];
-      for (int64_t sg = s0 + tid; sg < s1; sg += kCsrThreads) {
+      for (int64_t sg = s0 + segt; sg < s1; sg += segT) {
         const int i = p.cseg_row[sg];
         if (i >= pl.r_lo && i < pl.r_hi) continue;  // done by the row-sweep threads below
         const double zi = __ldcg(p.z + i);  // issued with the entry loads, not after the sum
@@ -350,7 +372,17 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     PROF(2);
     gsync();
     PROF(3);
-    // ---- Q(k)
+    // ---- Q(k): the x update (one thread per segment), the error partial of
+    // a check, and u_{k+1} (one warp per column of the next column block, from
+    // z_k) — u does not depend on x, so when its columns occupy only some of
+    // the CTA's warps the others do the x update and the check beside it
+    const Plan* nxt = (p.extended && k < p.k_end) ? &p.plan[k + 1 - p.k_begin] : nullptr;
+    int ncw = 0;
+    if (nxt) {
+      const int nJn = nxt->c_hi - nxt->c_lo;
+      ncw = nJn > g ? (nJn - g + G - 1) / G : 0;
+    }
+    const bool split_q = p.specialize && ncw > 0 && ncw <= kCsrWarps - 8 && (!check_k || oracle);
     {
       const int64_t s0 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g];
       const int64_t s1 = p.rseg_cta[(int64_t)pl.rb * (G + 1) + g + 1];
@@ -358,39 +390,55 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
         for (int c = tid; c < pl.r_hi - pl.r_lo; c += kCsrThreads) s_r[c] = __ldcg(p.r + c);
         __syncthreads();
       }
-      for (int64_t sg = s0 + tid; sg < s1; sg += kCsrThreads) {
-        const int j = p.rseg_col[sg];
-        // step_dsbgs: only x[J] moves (solvers.py:378-379)
-        if (p.dsbgs && (j < pl.c_lo || j >= pl.c_hi)) continue;
-        const double xj = __ldcg(p.x + j);
-        double acc = 0.0;
-        const int64_t e1 = p.rseg_ptr[sg + 1];
-        if (st_r)
-          for (int64_t e = p.rseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.rval[e], s_r[p.rrow[e]]);
-        else
-          for (int64_t e = p.rseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.rval[e], __ldcg(p.r + p.rrow[e]));
-        __stcg(p.x + j, __dsub_rn(xj, __dmul_rn(rs, acc)));
-      }
+      const int xT = split_q ? (kCsrWarps - ncw) * 32 : kCsrThreads;
+      const int xt = split_q ? tid - ncw * 32 : tid;
+      if (xt >= 0)
+        for (int64_t sg = s0 + xt; sg < s1; sg += xT) {
+          const int j = p.rseg_col[sg];
+          // step_dsbgs: only x[J] moves (solvers.py:378-379)
+          if (p.dsbgs && (j < pl.c_lo || j >= pl.c_hi)) continue;
+          const double xj = __ldcg(p.x + j);
+          double acc = 0.0;
+          const int64_t e1 = p.rseg_ptr[sg + 1];
+          if (st_r)
+            for (int64_t e = p.rseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.rval[e], s_r[p.rrow[e]]);
+          else
+            for (int64_t e = p.rseg_ptr[sg]; e < e1; ++e) acc = madd(acc, p.rval[e], __ldcg(p.r + p.rrow[e]));
+          __stcg(p.x + j, __dsub_rn(xj, __dmul_rn(rs, acc)));
+        }
     }
-    __syncthreads();
-    PROF(4);
-    if (check_k) {
-      if (oracle) {
-        oracle_partial();
+    if (split_q) {
+      if (warp < ncw) {
+        compute_u(*nxt);
+      } else if (check_k) {
+        oracle_partial(ncw);
+      }
+      if (check_k) {  // uniform across the CTA
         pending = true;
         pending_k = k;
-      } else {
-        gsync();
-        residual_partials();
-        gsync();
-        if (decide(k)) {
-          finished = true;
-          break;
+      }
+      PROF(4);
+    } else {
+      __syncthreads();
+      PROF(4);
+      if (check_k) {
+        if (oracle) {
+          oracle_partial(0);
+          pending = true;
+          pending_k = k;
+        } else {
+          gsync();
+          residual_partials();
+          gsync();
+          if (decide(k)) {
+            finished = true;
+            break;
+          }
         }
       }
+      PROF(5);
+      if (nxt) compute_u(*nxt);
     }
-    PROF(5);
-    if (p.extended && k < p.k_end) compute_u(p.plan[k + 1 - p.k_begin]);
     PROF(6);
     gsync();
     PROF(7);
@@ -403,7 +451,7 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     if (!finished && p.k_end == p.max_iters) {
       if (checking && (p.max_iters % p.stride) != 0) {
         if (oracle) {
-          oracle_partial();
+          oracle_partial(0);
           gsync();
         } else {
           residual_partials();

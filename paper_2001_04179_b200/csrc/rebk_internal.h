@@ -223,6 +223,7 @@ struct CsrParams {
   int32_t nonfinite_stop;
   int32_t dsbgs;  // step_dsbgs: x update restricted to the plan's column block, no z
   int32_t su_cap, sr_cap;  // u / r staged in shared memory (capacities in doubles, even; 0 = gathered from L2)
+  int32_t specialize;      // independent parts of a phase on disjoint warps of the CTA (REBK_CSR_SPEC, default 1)
   int32_t l2_prefetch;  // bulk L2 prefetch of the next phases' block data (REBK_CSR_PF, default 1)
   long long* prof;  // optional per-CTA phase cycle counters [G][16] (REBK_PROF=1)
 };
