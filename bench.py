@@ -631,8 +631,8 @@ def run_ours_c5(args):
                "time_to_tol_s": e_s / args.steps,
                "path": "paper_2001_04179_b200.multirhs.run_multi(A, B, config): A (1 GB fp32), B and X* uploaded "
                        "from pinned host memory every step (fresh fp32 device context incl. its transposed copy; "
-                       "the sampler weights from the fp64 upcast on the host, as the public API does), "
-                       "X and Z read back"}
+                       "the sampler's block weights computed on the device from that copy, as the public API does "
+                       "by default), X and Z read back"}
 
     cpu = None
     if not args.no_cpu:

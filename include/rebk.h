@@ -287,7 +287,9 @@ int rebk_shard_run_virtual(rebk_ctx* ctx, int vranks, const int64_t* rows_per_ra
 int rebk_sample_sequence(const rebk_cfg* cfg, int64_t k0, int64_t count, int32_t* picks_out);
 
 /* Device block Frobenius norms (matrix.py:170-189): out[nb] for contiguous
- * blocks ptr[nb+1] along axis 0 (rows) or 1 (columns). */
+ * blocks ptr[nb+1] along axis 0 (rows) or 1 (columns).  Dense fp64 contexts
+ * and fp32 contexts (rebk_ctx_create_dense_f32; squares accumulated in
+ * fp64, i.e. the norms of the matrix's exact fp64 upcast). */
 int rebk_block_frobenius_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* ptr,
                             double* out);
 

@@ -2152,9 +2152,11 @@ int rebk_sample_sequence(const rebk_cfg* cfg, int64_t k0, int64_t count, int32_t
 
 int rebk_block_frobenius_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* ptr, double* out) {
   if (!ctx || !ptr || !out || nb < 1 || (axis != 0 && axis != 1)) return fail(REBK_EINVAL, "bad argument");
-  if (ctx->kind != 0) return fail(REBK_EINVAL, "device block norms are implemented for dense matrices");
+  if (ctx->kind != 0 && ctx->kind != 2) return fail(REBK_EINVAL, "device block norms are implemented for dense matrices");
   const int64_t len = axis == 0 ? ctx->m : ctx->n;
   if (ptr[0] != 0 || ptr[nb] != len) return fail(REBK_EINVAL, "partition does not cover the axis");
+  for (int64_t b = 0; b < nb; ++b)
+    if (ptr[b + 1] < ptr[b]) return fail(REBK_EINVAL, "block pointers must be nondecreasing");
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t stream;
   CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
@@ -2167,7 +2169,13 @@ int rebk_block_frobenius_sq(rebk_ctx* ctx, int axis, int64_t nb, const int64_t* 
     cudaError_t e = arena.alloc(&d_ptr, nb + 1);
     if (!e) e = arena.alloc(&d_out, nb);
     if (!e) e = cudaMemcpyAsync(d_ptr, ptr, (nb + 1) * 8, cudaMemcpyHostToDevice, stream);
-    if (!e) e = launch_block_norms(ctx->A, ctx->lda, ctx->m, ctx->n, axis, nb, d_ptr, d_out, stream);
+    if (!e && ctx->kind == 2) {  // fp32 storage, fp64 accumulation
+      double* d_part = nullptr;
+      e = arena.alloc(&d_part, (size_t)(nb * block_norms_f32_scratch()));
+      if (!e) e = launch_block_norms_f32(ctx->A32, ctx->lda, ctx->m, ctx->n, axis, nb, d_ptr, d_part, d_out, stream);
+    } else if (!e) {
+      e = launch_block_norms(ctx->A, ctx->lda, ctx->m, ctx->n, axis, nb, d_ptr, d_out, stream);
+    }
     if (!e) e = cudaMemcpyAsync(out, d_out, nb * 8, cudaMemcpyDeviceToHost, stream);
     if (!e) e = cudaStreamSynchronize(stream);
     if (e) rc = fail(REBK_ECUDA, "block norms failed: %s", cudaGetErrorString(e));

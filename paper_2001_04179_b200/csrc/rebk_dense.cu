@@ -503,6 +503,56 @@ __global__ void block_norms_kernel(const double* A, int64_t lda, int64_t m, int6
   }
 }
 
+// fp32 storage (multi-RHS contexts): squares accumulated in fp64.  Each block
+// is cut into kNormChunks row chunks (grid.y) so that a handful of wide
+// blocks still fills the GPU; chunk partials part[b * kNormChunks + q] are
+// summed in chunk order by block_norms_finish (fixed order: runs replay).
+constexpr int kNormChunks = 32;
+__global__ void block_norms_f32_kernel(const float* A, int64_t lda, int64_t m, int64_t n, int axis,
+                                       const int64_t* ptr, double* part) {
+  __shared__ double red[kWarps];
+  const int64_t b = blockIdx.x;
+  const int q = blockIdx.y;
+  const int64_t lo = ptr[b], hi = ptr[b + 1];
+  // rows of this chunk: axis 0 -> rows of the block, axis 1 -> all rows of A
+  const int64_t R0 = axis == 0 ? lo : 0, R1 = axis == 0 ? hi : m;
+  const int64_t r0 = R0 + (R1 - R0) * q / kNormChunks, r1 = R0 + (R1 - R0) * (q + 1) / kNormChunks;
+  const int64_t c0 = axis == 0 ? 0 : lo, c1 = axis == 0 ? n : hi;
+  double acc = 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    const float* row = A + r * lda;
+    for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+      const double a = (double)__ldg(row + c);
+      acc = fma(a, a, acc);
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    part[b * kNormChunks + q] = s;
+  }
+}
+__global__ void block_norms_finish(const double* part, int64_t nb, double* out) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  double s = 0.0;
+  for (int q = 0; q < kNormChunks; ++q) s += part[b * kNormChunks + q];
+  out[b] = s;
+}
+
+// part_dev: scratch of nb * block_norms_f32_scratch() doubles
+int64_t block_norms_f32_scratch() { return kNormChunks; }
+cudaError_t launch_block_norms_f32(const float* A, int64_t lda, int64_t m, int64_t n, int axis, int64_t nb,
+                                   const int64_t* ptr_dev, double* part_dev, double* out_dev, cudaStream_t stream) {
+  if (nb <= 0) return cudaSuccess;
+  block_norms_f32_kernel<<<dim3((unsigned)nb, kNormChunks), kThreads, 0, stream>>>(A, lda, m, n, axis, ptr_dev, part_dev);
+  block_norms_finish<<<(unsigned)((nb + 127) / 128), 128, 0, stream>>>(part_dev, nb, out_dev);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_block_norms(const double* A, int64_t lda, int64_t m, int64_t n, int axis, int64_t nb,
                                const int64_t* ptr_dev, double* out_dev, cudaStream_t stream) {
   if (nb <= 0) return cudaSuccess;

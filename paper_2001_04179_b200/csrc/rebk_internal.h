@@ -371,6 +371,9 @@ cudaError_t shard_err(int64_t n, const double* x, const double* xs, double* out,
 cudaError_t launch_block_norms(const double* A, int64_t lda, int64_t m, int64_t n, int axis,
                                int64_t nb, const int64_t* ptr_dev, double* out_dev,
                                cudaStream_t stream);
+int64_t block_norms_f32_scratch();
+cudaError_t launch_block_norms_f32(const float* A, int64_t lda, int64_t m, int64_t n, int axis, int64_t nb,
+                                   const int64_t* ptr_dev, double* part_dev, double* out_dev, cudaStream_t stream);
 // rebk_beta.cu: sigma_1(B_b)^2 of every block of a contiguous partition
 cudaError_t block_sigma1_sq(const double* A, int64_t lda, int64_t m, int64_t n, int axis, int64_t nb,
                             const int64_t* h_ptr, int kmax, double* theta_out, int32_t* steps_out,

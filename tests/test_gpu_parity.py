@@ -398,6 +398,45 @@ def test_multi_rhs_fp32_matches_reference_columns():
             assert rel(tr.X[:, c], g["x_K"][:, c]) <= 1e-4
 
 
+def test_multi_rhs_device_block_weights_give_the_reference_sequence():
+    """run_multi's default sampler arrays: block weights from the device's
+    fp32 copy of A (fp64 accumulation) against the reference's arithmetic on
+    the host upcast (`flat @ flat` per block): equal to rounding, and the
+    block sequences drawn from the two sets of arrays are identical; X and Z
+    after 200 iterations agree to fp32 rounding on either route."""
+    from paper_2001_04179_b200.multirhs import DeviceMatrix32, _DeviceWeightsContext, run_multi
+    from paper_2001_04179_b200.solvers import SolverContext
+    from paper_2001_04179_b200.workloads import c5_arrays
+
+    g = load("c5mini_golden.npz")
+    a32, b32, xs = c5_arrays(6000, 600, 8)
+    # ragged last blocks on both axes
+    rp, cp = P.contiguous_partition(6000, 70, "row"), P.contiguous_partition(600, 64, "col")
+    cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=17, max_iters=200, row_partition=rp,
+                         col_partition=cp, stop=P.StoppingRule(mode="max_iters_only"), beta_max=float(g["beta"]))
+    a64 = P.Matrix.from_dense(a32.astype(np.float64))
+    prob = P.ProblemInstance(a=a64, b=b32[:, 0].astype(np.float64), x_star=None, b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    host = SolverContext(prob, cfg)
+    dm = DeviceMatrix32(a32)
+    dev = _DeviceWeightsContext(dm, 6000, 600, cfg)
+    assert np.allclose(dev.row_sampler.weights, host.row_sampler.weights, rtol=1e-13, atol=0.0)
+    assert np.allclose(dev.col_sampler.weights, host.col_sampler.weights, rtol=1e-13, atol=0.0)
+    picks = []
+    for ctx in (host, dev):
+        c = ctx.make_cfg(stop_mode="max_iters_only", tol=1.0, stride=1, max_iters=20000, key=_lib.philox_key(17))
+        out = np.empty(2 * 20000, dtype=np.int32)
+        _lib.check(_lib.load().rebk_sample_sequence(ctypes.byref(c), 1, 20000,
+                                                    out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))),
+                   "rebk_sample_sequence")
+        picks.append(out)
+    assert np.array_equal(picks[0], picks[1])
+    t_dev = run_multi(a32, b32, cfg, device_matrix=dm)
+    t_host = run_multi(a32, b32, cfg, device_matrix=dm, a64=a64)
+    assert t_dev.iters == t_host.iters == 200
+    assert rel(t_dev.X, t_host.X) <= 1e-6 and rel(t_dev.Z, t_host.Z) <= 1e-6
+
+
 @pytest.mark.slow
 def test_multi_rhs_fp32_baseline_c5_matches_reference_columns():
     """BASELINE config 5 at its stated size: fp32 A = randn(50000, 5000), 64
