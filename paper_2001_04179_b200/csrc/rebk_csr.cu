@@ -286,15 +286,25 @@ __global__ void __launch_bounds__(kCsrThreads) rebk_csr_kernel(CsrParams p) {
     // while warp 0 sums the error partials of the pending check
     if (p.extended && st_u)
       for (int c = tid; c < pl.c_hi - pl.c_lo; c += kCsrThreads) s_u[c] = __ldcg(p.u + c);
+    if (pending && warp == 0) {  // (decide(), with its loads beside the copy's and one barrier for both)
+      double sum = 0.0;
+      for (int q = lane; q < G; q += 32) sum += __ldcg(p.errpart + q);
+      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      if (lane == 0) s_bcast[0] = sum;
+    }
+    if (pending || (p.extended && st_u)) __syncthreads();
     if (pending) {
       pending = false;
-      if (decide(pending_k)) {
+      double err = sqrt(s_bcast[0]);
+      if (!oracle) err = err / p.res_scale;
+      const bool conv = check_stops(err, p.tol, p.nonfinite_stop);
+      if (g == 0 && tid == 0) record_check(ctl, p.errs, p.errs_cap, p.record, err, p.tol, p.nonfinite_stop, pending_k);
+      if (conv) {
         finished = true;
         break;
       }
     }
     const double cs = pl.c_scale, rs = pl.r_scale;
-    if (p.extended && st_u) __syncthreads();
     PROF(0);
     // The z update of the rows outside I (one thread per segment) and the row
     // sweep (one warp per row of I) are independent: when the CTA's rows of I
