@@ -819,8 +819,9 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
         G0 >= CS && encode_fn() != nullptr) {
       // (a finer grid for small problems was measured and not adopted: C1 on
       // 40-88 CTAs instead of 16 runs 6.7 instead of 7.9 us per iteration, but
-      // its end-to-end rate became bimodal, 45-68k against a steady 68k
-      // iters/s; profiles/r02_c1_grid_sweep.txt.  REBK_GRID selects it.)
+      // its end-to-end rate was more variable and on average lower (56-67k
+      // against a steady 65-68k iters/s); profiles/r02_c1_grid_sweep.txt.
+      // REBK_GRID selects it.)
       const int Gf = G0;
       int NC = std::max(1, Gf / CS);
       for (int attempt = 0; attempt < 3 && NC >= 1; ++attempt) {
