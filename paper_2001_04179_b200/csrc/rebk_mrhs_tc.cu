@@ -891,12 +891,12 @@ __global__ void __launch_bounds__(NTW, 1)
                 }
               }
               if (mode0) {
-                float4* dst = reinterpret_cast<float4*>(part + ((size_t)J.slot * 256 + J.prow + row) * RHS + c0);
+                // partial slices are stored [slice][c][256 rows]: for a fixed
+                // right-hand side the warp's 32 rows are one 128-byte line
+                // (row-major [row][c] was 32 partial sectors per store)
+                float* dst = part + ((size_t)J.slot * RHS + c0) * 256 + J.prow + row;
 #pragma unroll
-                for (int w = 0; w < 4; ++w)
-                  dst[w] = any ? make_float4(h[4 * w] + l[4 * w], h[4 * w + 1] + l[4 * w + 1],
-                                             h[4 * w + 2] + l[4 * w + 2], h[4 * w + 3] + l[4 * w + 3])
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int q = 0; q < 16; ++q) __stcg(dst + (size_t)q * 256, any ? h[q] + l[q] : 0.f);
               } else {
                 if (live && any) {
 #pragma unroll
@@ -1032,21 +1032,22 @@ __global__ void __launch_bounds__(NTW, 1)
               }
             }
           }
-          // U = Σ_q part1[q]: 128 chunks of 128 entries (two rows j of 64
-          // columns); the chunk's 32 float4 groups get NRED / 32 threads each,
-          // thread `sub` summing slices [ns1*sub/T, ns1*(sub+1)/T) with all its
-          // loads in flight, then the T range sums are added in order
+          // U = Σ_q part1[q] (slices stored [q][c][256]): 128 chunks of 128
+          // entries (half a right-hand side's row of Ut); the chunk's 32 float4
+          // groups get NRED / 32 threads each, thread `sub` summing slices
+          // [ns1*sub/T, ns1*(sub+1)/T) with all its loads in flight, then the T
+          // range sums are added in order
           if (a.extended && k <= a.k_end) {
             const Plan& pl = a.plan[k - a.k_begin];
             const int nJ = pl.c_hi - pl.c_lo;
             constexpr int T = NRED / 32;
             const int gi = tr / T, sub = tr % T;
             for (int ch = b; ch < 256 * RHS / 128; ch += G) {
-              const int j = 2 * ch + gi / 16, c4 = (gi % 16) * 4;
+              const int c = ch >> 1, j4 = (ch & 1) * 128 + gi * 4;
               float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (j < nJ) {
+              if (j4 < nJ) {
                 const int q0 = (a.ns1 * sub) / T, q1 = (a.ns1 * (sub + 1)) / T;
-                const float4* src = reinterpret_cast<const float4*>(a.part1 + (size_t)j * RHS + c4);
+                const float4* src = reinterpret_cast<const float4*>(a.part1 + (size_t)c * 256 + j4);
                 constexpr int QB = 4;
                 for (int qb = q0; qb < q1; qb += QB) {
                   float4 v[QB];
@@ -1077,37 +1078,40 @@ __global__ void __launch_bounds__(NTW, 1)
                   acc.z += w.z;
                   acc.w += w.w;
                 }
-                const bool valid = j < nJ;
-                a.Ut[(size_t)(c4 + 0) * 256 + j] = valid ? acc.x : 0.f;
-                a.Ut[(size_t)(c4 + 1) * 256 + j] = valid ? acc.y : 0.f;
-                a.Ut[(size_t)(c4 + 2) * 256 + j] = valid ? acc.z : 0.f;
-                a.Ut[(size_t)(c4 + 3) * 256 + j] = valid ? acc.w : 0.f;
+                // rows past |J| are K padding of the z update: zero
+                float4 o;
+                o.x = j4 + 0 < nJ ? acc.x : 0.f;
+                o.y = j4 + 1 < nJ ? acc.y : 0.f;
+                o.z = j4 + 2 < nJ ? acc.z : 0.f;
+                o.w = j4 + 3 < nJ ? acc.w : 0.f;
+                *reinterpret_cast<float4*>(a.Ut + (size_t)c * 256 + j4) = o;
               }
               named_bar(2, NRED);
             }
           }
         } else {
           // R = ((Σ_q part3[q]) - B_I) + Z_I  (solvers.py:291-293 order), zero past |I|;
-          // float4 groups as for U, b_I and z_I fetched before the partials
+          // float4 groups along the rows as for U, b_I and z_I fetched before the partials
           const Plan& pl = a.plan[k - a.k_begin];
           const int nI = pl.r_hi - pl.r_lo;
           constexpr int T = NRED / 32;
           const int gi = tr / T, sub = tr % T;
           for (int ch = b; ch < 256 * RHS / 128; ch += G) {
-            const int i = 2 * ch + gi / 16, c4 = (gi % 16) * 4;
-            const bool valid = i < nI;
+            const int c = ch >> 1, i4 = (ch & 1) * 128 + gi * 4;
+            const bool valid = i4 < nI;
             float bt[4] = {0.f, 0.f, 0.f, 0.f}, zt[4] = {0.f, 0.f, 0.f, 0.f};
             if (sub == 0 && valid) {
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                bt[u] = ld_cg_f32(a.Bt + (size_t)(c4 + u) * a.m + pl.r_lo + i);
-                if (a.extended) zt[u] = ld_cg_f32(a.Zt + (size_t)(c4 + u) * a.m + pl.r_lo + i);
-              }
+              for (int u = 0; u < 4; ++u)
+                if (i4 + u < nI) {
+                  bt[u] = ld_cg_f32(a.Bt + (size_t)c * a.m + pl.r_lo + i4 + u);
+                  if (a.extended) zt[u] = ld_cg_f32(a.Zt + (size_t)c * a.m + pl.r_lo + i4 + u);
+                }
             }
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             if (valid) {
               const int q0 = (a.ns3 * sub) / T, q1 = (a.ns3 * (sub + 1)) / T;
-              const float4* src = reinterpret_cast<const float4*>(a.part3 + (size_t)i * RHS + c4);
+              const float4* src = reinterpret_cast<const float4*>(a.part3 + (size_t)c * 256 + i4);
               constexpr int QB = 4;
               for (int qb = q0; qb < q1; qb += QB) {
                 float4 v[QB];
@@ -1139,15 +1143,17 @@ __global__ void __launch_bounds__(NTW, 1)
                 acc.w += w.w;
               }
               const float sum[4] = {acc.x, acc.y, acc.z, acc.w};
+              float o[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 float v = 0.f;
-                if (valid) {
+                if (i4 + u < nI) {
                   v = sum[u] - bt[u];
                   if (a.extended) v += zt[u];
                 }
-                a.Rt[(size_t)(c4 + u) * 256 + i] = v;
+                o[u] = v;
               }
+              *reinterpret_cast<float4*>(a.Rt + (size_t)c * 256 + i4) = make_float4(o[0], o[1], o[2], o[3]);
             }
             named_bar(2, NRED);
           }
