@@ -354,6 +354,46 @@ def test_sparse_cases_bitwise_equal_to_reference():
                     assert np.array_equal(st.z, g[f"z_{k}"]), (case, k, rel(st.z, g[f"z_{k}"]))
 
 
+@pytest.mark.parametrize("env", [{}, {"REBK_CSR_SPEC": "0"}, {"REBK_CSR_STAGE": "0"}, {"REBK_CSR_PF": "0"},
+                                 {"REBK_GRID": "3"}, {"REBK_GRID": "40"},
+                                 {"REBK_CSR_SPEC": "0", "REBK_CSR_STAGE": "0", "REBK_CSR_PF": "0"}])
+def test_sparse_kernel_variants_bitwise_equal_to_scipy_order(monkeypatch, env):
+    """The CSR kernel's shared-memory staging of u / r, its L2 prefetch and
+    its warp specialisation (and the fallbacks taken when a CTA's rows of I or
+    columns of J fill all its warps: small grids) change where and when
+    values are read, never the order they are summed in: a 12000 x 3000 sparse
+    run (ragged blocks, stride 3, stop inside the run) equals the scipy-order
+    oracle bit for bit under every switch."""
+    import scipy.sparse as sp
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rs = np.random.default_rng(11)
+    m, n = 12000, 3000
+    a = sp.random(m, n, density=4e-3, format="csr", random_state=rs, data_rvs=rs.standard_normal)
+    xs = rs.standard_normal(n)
+    b = a @ xs + 1e-3 * rs.standard_normal(m)
+    from scipy.sparse.linalg import lsqr
+
+    x_star = lsqr(a, b, atol=1e-14, btol=1e-14, iter_lim=4000)[0]
+    prob = P.ProblemInstance(a=P.Matrix.from_sparse(a), b=b, x_star=x_star, b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    rp, cp = P.contiguous_partition(m, 700, "row"), P.contiguous_partition(n, 260, "col")
+    tol = 0.5 * float(np.linalg.norm(x_star))
+    cfg = P.SolverConfig(algorithm="rebk", alpha=1.2, seed=5, max_iters=600, row_partition=rp, col_partition=cp,
+                         stop=P.StoppingRule(tol=tol, check_stride=3), beta_max=1.0)
+    t = P.run(prob, cfg)
+    assert t.kernel_path == 3
+    rp_ptr = np.array(list(range(0, m, 700)) + [m])
+    cp_ptr = np.array(list(range(0, n, 260)) + [n])
+    orc = OracleSolver(a, b, rp_ptr, cp_ptr, cfg.alpha, algorithm="rebk")
+    res = orc.run(5, 600, tol, x_star, stride=3)
+    assert res["iters"] == t.iters and res["converged"] == t.converged
+    assert 3 <= t.iters < 600 or not t.converged
+    assert np.array_equal(t.x, res["x"]), rel(t.x, res["x"])
+    assert np.array_equal(t.z, res["z"]), rel(t.z, res["z"])
+
+
 @pytest.mark.slow
 def test_c4_sparse_full_run_matches_reference():
     """BASELINE config 4: CSR 200000 x 50000, 1e7 nnz, blocks 2000/1000."""
@@ -611,6 +651,28 @@ def test_stream_path_matches_reference_c1(monkeypatch, grid):
     assert t1.converged and t1.iters == k
     assert rel(t1.x, g[f"x_{k}"]) <= RTOL and rel(t1.z, g[f"z_{k}"]) <= RTOL
     assert np.array_equal(t1.x, t2.x) and np.array_equal(t1.z, t2.z)
+
+
+@pytest.mark.parametrize("env", [{"REBK_STREAM_ORDER": "1"}, {"REBK_STREAM_ORDER": "1", "REBK_STREAM_TAIL": "2"},
+                                 {"REBK_STREAM_TAIL": "3"}, {"REBK_STREAM_REV": "0"}, {"REBK_STREAM_DBG": "1"}])
+def test_stream_path_schedule_variants_bitwise(monkeypatch, env):
+    """The streaming kernel's pass order within a step, its L2 retention of
+    C1's tail, walk direction and an extra barrier per step move boxes and
+    barriers around, not arithmetic: ITER, x and z equal the default
+    schedule's bit for bit (and the reference's within 1e-10).  (A different
+    ring depth changes the box height, hence the summation order.)"""
+    monkeypatch.setenv("REBK_NO_FAST", "1")
+    monkeypatch.setenv("REBK_STREAM", "2")
+    g, a, prob, cfg = c1_instance()
+    t0 = P.run(prob, cfg)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    t1 = P.run(prob, cfg)
+    assert t0.kernel_path == 7 and t1.kernel_path == 7
+    k = int(g["iters"])
+    assert t1.converged and t1.iters == k == t0.iters
+    assert np.array_equal(t0.x, t1.x) and np.array_equal(t0.z, t1.z)
+    assert rel(t1.x, g[f"x_{k}"]) <= RTOL and rel(t1.z, g[f"z_{k}"]) <= RTOL
 
 
 @pytest.mark.parametrize("algorithm", ["rebk", "rabk", "rk", "rek"])
