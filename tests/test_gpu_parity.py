@@ -654,13 +654,13 @@ def test_stream_path_matches_reference_c1(monkeypatch, grid):
 
 
 @pytest.mark.parametrize("env", [{"REBK_STREAM_ORDER": "1"}, {"REBK_STREAM_ORDER": "1", "REBK_STREAM_TAIL": "2"},
-                                 {"REBK_STREAM_TAIL": "3"}, {"REBK_STREAM_REV": "0"}, {"REBK_STREAM_DBG": "1"}])
+                                 {"REBK_STREAM_TAIL": "3"}, {"REBK_STREAM_DBG": "1"}])
 def test_stream_path_schedule_variants_bitwise(monkeypatch, env):
     """The streaming kernel's pass order within a step, its L2 retention of
-    C1's tail, walk direction and an extra barrier per step move boxes and
-    barriers around, not arithmetic: ITER, x and z equal the default
+    C1's tail and an extra barrier per step move boxes and barriers around,
+    not arithmetic: ITER, x and z equal the default
     schedule's bit for bit (and the reference's within 1e-10).  (A different
-    ring depth changes the box height, hence the summation order.)"""
+    ring depth or walk direction changes the summation order.)"""
     monkeypatch.setenv("REBK_NO_FAST", "1")
     monkeypatch.setenv("REBK_STREAM", "2")
     g, a, prob, cfg = c1_instance()
