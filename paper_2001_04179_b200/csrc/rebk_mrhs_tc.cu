@@ -741,7 +741,9 @@ __global__ void __launch_bounds__(NTW, 1)
                 }
               }
               umma::commit(&P.rempty[q]);
-              umma::commit(&P.lempty[l]);
+              // with equally deep rings the raw stage and the TMEM-A slot of a
+              // k-block are released by the same event: one commit serves both
+              if (PK_NRAW != PK_NA) umma::commit(&P.lempty[l]);
             }
             umma::commit(&P.tfull[b]);
             pk_jstamp(a, k, phase, j, 3);
@@ -774,7 +776,7 @@ __global__ void __launch_bounds__(NTW, 1)
               phf ^= 1u << q;
               if (a.dbg & 64) {  // REBK_PK_DBG=64: no conversion (timing experiments only)
                 if (it >= PK_NA) {
-                  mbar_wait(&P.lempty[l], (phl >> l) & 1u);
+                  mbar_wait(PK_NRAW != PK_NA ? &P.lempty[l] : &P.rempty[l], (phl >> l) & 1u);
                   phl ^= 1u << l;
                 }
               } else if (aconv) {
@@ -801,7 +803,7 @@ __global__ void __launch_bounds__(NTW, 1)
                   umma::split_tf32(hi[e], h, lo[e]);
                 }
                 if (it >= PK_NA) {  // the MMAs of stage it - PK_NA are done with slot l
-                  mbar_wait(&P.lempty[l], (phl >> l) & 1u);
+                  mbar_wait(PK_NRAW != PK_NA ? &P.lempty[l] : &P.rempty[l], (phl >> l) & 1u);
                   phl ^= 1u << l;
                 }
                 const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
