@@ -423,6 +423,24 @@ void print_prof(const std::vector<long long>& h, int G, int gsplit, int khz, dou
   }
 }
 
+int env_int(const char* name, int dflt);
+// Streaming kernel, L2 retention of the column pass (StreamParams.tail): when
+// the launch's slice of a column block plus its slice of a row block fit in
+// L2 (a rank of a sharded run: 100 + 10 MB at C3 / 8), every C1 box is loaded
+// evict_last and the C2 pass re-reads the slice from L2 (measured on that
+// shape, one GPU: 44.7 -> 38.8 us per iteration); otherwise C1 streams
+// evict_first (C3 on one GPU: 800 MB).  REBK_STREAM_TAIL overrides (chunks
+// from the end of C1 to keep).
+int stream_tail(const rebk_ctx* ctx, int64_t rows_in_launch, int nJ_max, int64_t nI_rows_in_launch, bool extended) {
+  const int forced = env_int("REBK_STREAM_TAIL", -1);
+  if (forced >= 0) return forced;
+  if (!extended) return 0;
+  int l2 = 0;
+  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device) != cudaSuccess || l2 <= 0) return 0;
+  const double need = 8.0 * ((double)rows_in_launch * nJ_max + (double)nI_rows_in_launch * (double)ctx->n);
+  return need <= 0.9 * (double)l2 ? (1 << 30) : 0;
+}
+
 int env_int(const char* name, int dflt) {
   const char* s = getenv(name);
   return s ? atoi(s) : dflt;
@@ -1089,7 +1107,7 @@ int run_device_impl_once(rebk_ctx* ctx, const rebk_cfg* cfg, const double* b_dev
         spar.pfence = env_int("REBK_STREAM_PFENCE", 0);
         spar.dbg = env_int("REBK_STREAM_DBG", 0);
         spar.order = env_int("REBK_STREAM_ORDER", 0);
-  spar.tail = env_int("REBK_STREAM_TAIL", 0);
+  spar.tail = stream_tail(ctx, ctx->m, stg.nJ_max, stg.nI_max, extended);
         spar.zprev = d_zprev;
         err = launch_dense_stream(spar, tm_sc, tm_sr, G, stg.smem_bytes, stream);
       } else {
@@ -1396,7 +1414,7 @@ int shard_stream_impl(rebk_ctx* ctx, const rebk_cfg* cfg, ShardLaunch& L, const 
   spar.pfence = env_int("REBK_STREAM_PFENCE", 0);
   spar.dbg = env_int("REBK_STREAM_DBG", 0);
   spar.order = env_int("REBK_STREAM_ORDER", 0);
-  spar.tail = env_int("REBK_STREAM_TAIL", 0);
+  spar.tail = stream_tail(ctx, ctx->m, nJ_max, (int64_t)nI_loc * L.vranks, extended);
   double* d_zprev = nullptr;
   if (extended) CUDA_TRY(arena.alloc(&d_zprev, ctx->m));
   spar.zprev = d_zprev;
