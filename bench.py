@@ -880,6 +880,7 @@ def run_ours_c3_sharded(args):
         try:
             c = wl.cfg("oracle_error", tol, args.max_iters)
             xchg = ShardExchange(ws, rank, int(np.diff(wl.col_ptr).max()), n, local, dist.all_gather_object)
+            xchg.probe(dist.barrier)  # peer stores arrive before any kernel waits on them
             dm = DeviceMatrix.from_device_pointer(a_local.data_ptr(), a_local.shape[0], n, n, local)
             with torch.cuda.stream(stream):
                 x_d.zero_()

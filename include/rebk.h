@@ -258,6 +258,9 @@ int rebk_shard_run(rebk_ctx* ctx, void* comm, const rebk_shard_run_args* args, i
  *   rebk_shard_grid_ctas    CTAs per rank this device runs (all ranks must use the same value: take the min)
  *   rebk_shard_xchg_create  this rank's exchange buffer (nranks <= 8)
  *   rebk_shard_xchg_ipc_handle / _open_peers  export the buffer, map every peer's (handles: [nranks][64])
+ *   rebk_shard_xchg_probe   checks the mapping with the protocol's own instructions: phase 0 stores a token word
+ *                           into every rank's buffer (st.release.sys through the peer mapping); phase 1 (after a
+ *                           host-side barrier of the ranks) counts the ranks whose word did not arrive here
  *   rebk_shard_run_device   one solve of this rank's shard; ctx = this rank's rows; cfg = the GLOBAL partitions
  *                           and sampler arrays (row_ptr of the whole matrix); local_ranges [n_row_blocks][2] =
  *                           this rank's rows of each block in local numbering; b_dev, z_io_dev local; x_io_dev,
@@ -273,6 +276,7 @@ int rebk_shard_xchg_create(int nranks, int rank, int64_t nJ_cap, int64_t n_cap, 
                            rebk_shard_xchg** out);
 int rebk_shard_xchg_ipc_handle(rebk_shard_xchg* x, unsigned char handle_out[64]);
 int rebk_shard_xchg_open_peers(rebk_shard_xchg* x, const unsigned char* handles);
+int rebk_shard_xchg_probe(rebk_shard_xchg* x, int phase, uint64_t token, int* missing_out);
 int rebk_shard_xchg_destroy(rebk_shard_xchg* x);
 int rebk_shard_run_device(rebk_ctx* ctx, rebk_shard_xchg* x, const rebk_cfg* cfg, const int64_t* local_ranges,
                           const double* b_dev, const double* x_star_dev, double* x_io_dev, double* z_io_dev,

@@ -148,6 +148,7 @@ SIGNATURES = {
     "rebk_shard_xchg_create": (c_int, [c_int, c_int, c_int64, c_int64, c_int, c_int, POINTER(c_void_p)]),
     "rebk_shard_xchg_ipc_handle": (c_int, [c_void_p, ctypes.c_char_p]),
     "rebk_shard_xchg_open_peers": (c_int, [c_void_p, ctypes.c_char_p]),
+    "rebk_shard_xchg_probe": (c_int, [c_void_p, c_int, ctypes.c_uint64, POINTER(c_int)]),
     "rebk_shard_xchg_destroy": (c_int, [c_void_p]),
     "rebk_shard_run_device": (c_int, [c_void_p, c_void_p, POINTER(RebkCfg), _P_I64, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p, POINTER(RebkTrace)]),

@@ -1935,7 +1935,7 @@ struct rebk_shard_xchg {
   int device = 0, P = 1, rank = 0, Gr = 0;
   int64_t nJ_cap = 0, n_cap = 0;
   char* buf = nullptr;  // this rank's exchange buffer (cudaMalloc: exportable by CUDA IPC)
-  size_t bytes = 0;
+  size_t bytes = 0, probe_off = 0;
   char* peer[kMaxRanks] = {};  // every rank's buffer mapped into this process (peer[rank] = buf)
   bool opened[kMaxRanks] = {};
   unsigned long long seq_base = 0;  // exchanges completed by earlier solves (identical on every rank)
@@ -1968,7 +1968,9 @@ int rebk_shard_xchg_create(int nranks, int rank, int64_t nJ_cap, int64_t n_cap, 
   x->Gr = grid_ctas;
   x->nJ_cap = (nJ_cap + 1) & ~(int64_t)1;
   x->n_cap = (n_cap + 1) & ~(int64_t)1;
-  x->bytes = xchg_bytes(nranks, x->nJ_cap, x->n_cap, grid_ctas);
+  // the protocol area, then kMaxRanks probe words (rebk_shard_xchg_probe)
+  x->probe_off = (xchg_bytes(nranks, x->nJ_cap, x->n_cap, grid_ctas) + 255) & ~(size_t)255;
+  x->bytes = x->probe_off + sizeof(unsigned long long) * kMaxRanks;
   cudaError_t e = cudaMalloc(&x->buf, x->bytes);
   if (e == cudaSuccess) e = cudaMemset(x->buf, 0, x->bytes);
   if (e != cudaSuccess) {
@@ -2003,6 +2005,59 @@ int rebk_shard_xchg_open_peers(rebk_shard_xchg* x, const unsigned char* handles)
     x->peer[q] = (char*)ptr;
     x->opened[q] = true;
   }
+  return REBK_OK;
+}
+
+// Probe of the mapped peer buffers with the protocol's own instructions:
+// phase 0 stores token * 16 + rank + 1 into probe word [rank] of EVERY rank's
+// buffer (st.release.sys through the peer mapping); phase 1, called after a
+// host-side barrier of the ranks, reads this rank's probe words
+// (ld.acquire.sys) and counts the ranks whose word is missing.  Neither
+// kernel waits on another rank's kernel.
+struct ProbePeers {
+  unsigned long long* w[kMaxRanks];
+};
+__global__ void shard_probe_post(ProbePeers pp, int P, int rank, unsigned long long token) {
+  const int q = threadIdx.x;
+  if (q < P)
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pp.w[q] + rank), "l"(token * 16ull + (unsigned long long)rank + 1ull)
+                 : "memory");
+}
+__global__ void shard_probe_check(const unsigned long long* mine, int P, unsigned long long token, int* missing) {
+  const int q = threadIdx.x;
+  if (q < P) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + q) : "memory");
+    if (v != token * 16ull + (unsigned long long)q + 1ull) atomicAdd(missing, 1);
+  }
+}
+
+int rebk_shard_xchg_probe(rebk_shard_xchg* x, int phase, uint64_t token, int* missing_out) {
+  if (!x || (phase != 0 && phase != 1) || (phase == 1 && !missing_out)) return fail(REBK_EINVAL, "rebk_shard_xchg_probe: bad argument");
+  for (int q = 0; q < x->P; ++q)
+    if (!x->peer[q]) return fail(REBK_EINVAL, "rank %d's exchange buffer is not mapped (rebk_shard_xchg_open_peers)", q);
+  CUDA_TRY(cudaSetDevice(x->device));
+  std::lock_guard<std::mutex> lock(x->mu);
+  if (phase == 0) {
+    ProbePeers pp = {};
+    for (int q = 0; q < x->P; ++q) pp.w[q] = (unsigned long long*)(x->peer[q] + x->probe_off);
+    shard_probe_post<<<1, 32>>>(pp, x->P, x->rank, (unsigned long long)token);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    return REBK_OK;
+  }
+  int* d_missing = nullptr;
+  CUDA_TRY(cudaMalloc(&d_missing, sizeof(int)));
+  cudaError_t e = cudaMemset(d_missing, 0, sizeof(int));
+  if (e == cudaSuccess) {
+    shard_probe_check<<<1, 32>>>((const unsigned long long*)(x->buf + x->probe_off), x->P, (unsigned long long)token, d_missing);
+    e = cudaGetLastError();
+  }
+  int missing = -1;
+  if (e == cudaSuccess) e = cudaMemcpy(&missing, d_missing, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(d_missing);
+  if (e != cudaSuccess) return fail(REBK_ECUDA, "rebk_shard_xchg_probe: %s", cudaGetErrorString(e));
+  *missing_out = missing;
   return REBK_OK;
 }
 

@@ -517,6 +517,22 @@ class ShardExchange:
             ctypes.byref(tr)), "rebk_shard_run_device")
         return tr
 
+    def probe(self, barrier, token: int = 1) -> None:
+        """Collective check of the peer mappings before any persistent kernel
+        depends on them: every rank stores a token word into every rank's
+        buffer with the protocol's own st.release.sys, the ranks meet at
+        `barrier()` (host side), then each rank verifies that all words
+        arrived.  Raises RuntimeError naming the count of missing ranks."""
+        _lib.check(self.lib.rebk_shard_xchg_probe(self.handle, 0, int(token), None), "rebk_shard_xchg_probe")
+        barrier()
+        missing = ctypes.c_int(-1)
+        _lib.check(self.lib.rebk_shard_xchg_probe(self.handle, 1, int(token), ctypes.byref(missing)),
+                   "rebk_shard_xchg_probe")
+        barrier()
+        if missing.value != 0:
+            raise RuntimeError(f"rank {self.rank}: the probe words of {missing.value} of {self.nranks} ranks did not "
+                               "arrive through the peer mapping")
+
     def close(self):
         if getattr(self, "handle", None):
             self.lib.rebk_shard_xchg_destroy(self.handle)

@@ -139,3 +139,55 @@ def test_persistent_sharded_c3_full_size_matches_single_gpu():
     res = run_persistent_virtual(wl.a, wl.b, wl.x_star, c, wl.row_ptr, 8)
     assert res["iters"] == int(tr.iters) and res["converged"]
     assert rel(res["x"], xs1) <= RTOL and rel(res["z"], zs1) <= RTOL
+
+
+def _ipc_rank_main(rank, world, port, out_dir):
+    import os
+
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_2001_04179_b200.sharded import ShardExchange
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # every process uses GPU 0: CUDA IPC maps a buffer of another PROCESS the
+    # same way whether it lives on this GPU or on an NVLink peer
+    x = ShardExchange(world, rank, 500, 10000, 0, dist.all_gather_object)
+    ok, err = 1, ""
+    try:
+        for token in (1, 2, 7):
+            x.probe(dist.barrier, token)
+    except Exception as exc:  # reported through the file, the parent asserts
+        ok, err = 0, repr(exc)
+    np.savez(os.path.join(out_dir, f"ipc{rank}.npz"), ok=ok, err=err, grid=x.grid_ctas)
+    dist.barrier()
+    x.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_exchange_buffers_map_across_processes_over_cuda_ipc(world):
+    """The multi-process setup of the in-kernel exchange on real CUDA: `world`
+    processes (all on this one GPU) create their exchange buffers, export and
+    map them over CUDA IPC (rebk_shard_xchg_ipc_handle / _open_peers) and
+    probe the mappings with the protocol's own st.release.sys / ld.acquire.sys
+    words, meeting at a host barrier in between (no kernel waits on another
+    process's kernel, so this is legal on one GPU; the persistent kernels
+    themselves are tested as emulated ranks in one launch above)."""
+    import socket
+    import tempfile
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_ipc_rank_main, args=(world, port, d), nprocs=world, join=True)
+        outs = [np.load(os.path.join(d, f"ipc{r}.npz")) for r in range(world)]
+    for r, o in enumerate(outs):
+        assert int(o["ok"]) == 1, (r, str(o["err"]))
+        assert int(o["grid"]) == int(outs[0]["grid"])
