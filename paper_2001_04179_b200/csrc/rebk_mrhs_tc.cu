@@ -422,6 +422,7 @@ struct PkArgs {
   int64_t trace_k0;
   int trace_n;
   unsigned long long* trace2;
+  long long* trace3;  // -DPK_STAGE_TRACE: clock64 stamps [stage][8] of CTA 0 at iteration trace_k0
   int prefetch;  // L2 prefetch of the next phase's A boxes
   int dbg;       // REBK_PK_DBG experiments (8: check without the warp sums, 16: check without x* loads)
 };
@@ -494,6 +495,23 @@ __device__ __forceinline__ void pk_jstamp(const PkArgs& a, int64_t k, int phase,
     const int sel = blockIdx.x == 0 ? 0 : 1;
     a.trace2[((sel * 2 + phase) * 4 + j) * 8 + ev] = t;
   }
+}
+// per-stage stamps (CTA 0, iteration trace_k0, first PK_STAGE_TRACE_N stages;
+// SM clock): 0 producer saw the stage free, 1 producer issued it, 2 A
+// converter saw it full, 3 A converter's TMEM stores done, 4 B converter
+// done, 5 MMA thread saw it converted, 6 MMA thread committed it
+constexpr int PK_STAGE_TRACE_N = 96;
+#ifdef PK_STAGE_TRACE
+#define PK_SC_NEXT(k, sc) if ((k) == a.trace_k0) ++(sc)
+#else
+#define PK_SC_NEXT(k, sc) (void)(sc)
+#endif
+__device__ __forceinline__ void pk_sstamp(const PkArgs& a, int64_t k, int cnt, int ev) {
+#ifdef PK_STAGE_TRACE
+  if (a.trace3 && blockIdx.x == 0 && k == a.trace_k0 && cnt < PK_STAGE_TRACE_N) a.trace3[cnt * 8 + ev] = clock64();
+#else
+  (void)a; (void)k; (void)cnt; (void)ev;
+#endif
 }
 __device__ __forceinline__ bool pk_is_check(const PkArgs& a, int64_t k) {
   return a.checking && k >= 1 && (k % a.stride == 0 || k == a.max_iters);
@@ -641,7 +659,7 @@ __global__ void __launch_bounds__(NTW, 1)
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
       uint32_t ph = 0;
-      int it = 0;
+      int it = 0, sc = 0;
       for (int64_t k = a.k_begin; k <= k_last; ++k) {
         for (int phase = 0; phase < 2; ++phase) {
           if (phase == 1) {
@@ -674,6 +692,7 @@ __global__ void __launch_bounds__(NTW, 1)
                 mbar_wait(&P.rempty[q], (ph >> q) & 1u);
                 ph ^= 1u << q;
               }
+              pk_sstamp(a, k, sc, 0);
               mbar_arrive_expect_tx(&P.full[q], (TM + RHS) * BK * 4);
               const int kbe = kb;
               if (J.kind == 2)  // Z update: A_J through At, box 128 rows of z x 32 columns of J (L2-warm from P1)
@@ -681,6 +700,8 @@ __global__ void __launch_bounds__(NTW, 1)
               else
                 tma_load_2d(a_raw(q), ma, J.kc0 + kbe * BK, J.row0, &P.full[q]);
               tma_load_2d(b_raw(q), mb, kbe * BK, 0, &P.full[q]);
+              pk_sstamp(a, k, sc, 1);
+              PK_SC_NEXT(k, sc);
             }
             pk_jstamp(a, k, phase, j, 1);
           }
@@ -708,7 +729,7 @@ __global__ void __launch_bounds__(NTW, 1)
       const uint32_t idesc = umma::idesc_tf32(TM, RHS);
       const uint32_t idesc2 = umma::idesc_tf32(TM, 2 * RHS);
       uint32_t phc = 0, pht = 0;
-      int it = 0, jt = 0;
+      int it = 0, jt = 0, sc = 0;
       for (int64_t k = a.k_begin; k <= k_last; ++k) {
         for (int phase = 0; phase < 2; ++phase) {
           if (phase == 1) {
@@ -728,6 +749,7 @@ __global__ void __launch_bounds__(NTW, 1)
               const int q = it % PK_NRAW, l = it % PK_NA;
               mbar_wait(&P.conv[l], (phc >> l) & 1u);
               phc ^= 1u << l;
+              pk_sstamp(a, k, sc, 5);
               if (kb == J.kb0) pk_jstamp(a, k, phase, j, 2);
               umma::fence_after_sync();
               const uint32_t tah = ta_hi(l), tal = tah + 32;
@@ -744,6 +766,8 @@ __global__ void __launch_bounds__(NTW, 1)
               // with equally deep rings the raw stage and the TMEM-A slot of a
               // k-block are released by the same event: one commit serves both
               if (PK_NRAW != PK_NA) umma::commit(&P.lempty[l]);
+              pk_sstamp(a, k, sc, 6);
+              PK_SC_NEXT(k, sc);
             }
             umma::commit(&P.tfull[b]);
             pk_jstamp(a, k, phase, j, 3);
@@ -757,7 +781,7 @@ __global__ void __launch_bounds__(NTW, 1)
     const bool conv = warp < EPI0;
     const int tr = tid - CONV0 * 32;  // 0 .. NRED-1
     uint32_t phf = 0, pht = 0, phl = 0;
-    int it = 0, jt = 0;
+    int it = 0, jt = 0, sc = 0;
     for (int64_t k = a.k_begin; k <= k_last; ++k) {
       for (int phase = 0; phase < 2; ++phase) {
         if (phase == 1 && k == k_last) break;
@@ -774,6 +798,7 @@ __global__ void __launch_bounds__(NTW, 1)
               const int q = it % PK_NRAW, l = it % PK_NA;
               mbar_wait(&P.full[q], (phf >> q) & 1u);
               phf ^= 1u << q;
+              if (tid == 128) pk_sstamp(a, k, sc, 2);
               if (a.dbg & 64) {  // REBK_PK_DBG=64: no conversion (timing experiments only)
                 if (it >= PK_NA) {
                   mbar_wait(PK_NRAW != PK_NA ? &P.lempty[l] : &P.rempty[l], (phl >> l) & 1u);
@@ -832,6 +857,9 @@ __global__ void __launch_bounds__(NTW, 1)
                 fence_proxy_async();
               }
               __syncwarp();
+              if (tid == 128) pk_sstamp(a, k, sc, 3);
+              if (tid == 64) pk_sstamp(a, k, sc, 4);
+              PK_SC_NEXT(k, sc);
               if (lane == 0) mbar_arrive(&P.conv[l]);
             }
         } else {
@@ -1445,6 +1473,10 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
       pa.trace = d_tr;
       TC_TRY(cudaMallocAsync((void**)&pa.trace2, sizeof(unsigned long long) * 2 * 2 * 4 * 8, stream));
       TC_TRY(cudaMemsetAsync(pa.trace2, 0, sizeof(unsigned long long) * 2 * 2 * 4 * 8, stream));
+#ifdef PK_STAGE_TRACE
+      TC_TRY(cudaMallocAsync((void**)&pa.trace3, sizeof(long long) * PK_STAGE_TRACE_N * 8, stream));
+      TC_TRY(cudaMemsetAsync(pa.trace3, 0, sizeof(long long) * PK_STAGE_TRACE_N * 8, stream));
+#endif
     }
     for (int64_t k0 = 1; k0 <= cfg->max_iters; k0 += CHK) {
       const int64_t cnt = std::min(CHK, cfg->max_iters - k0 + 1);
@@ -1497,6 +1529,21 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
             fprintf(stderr, "\n");
           }
       cudaFree(pa.trace2);
+#ifdef PK_STAGE_TRACE
+      std::vector<long long> h3(PK_STAGE_TRACE_N * 8);
+      TC_TRY(cudaMemcpy(h3.data(), pa.trace3, h3.size() * 8, cudaMemcpyDeviceToHost));
+      long long c0 = 0;
+      for (int i = 0; i < PK_STAGE_TRACE_N; ++i)
+        if (h3[i * 8 + 1] && (!c0 || h3[i * 8 + 1] < c0)) c0 = h3[i * 8 + 1];
+      fprintf(stderr, "[pk stage] cycles since the first issue: free issued | A full, A stored | B done | MMA conv, committed\n");
+      for (int i = 0; i < PK_STAGE_TRACE_N; ++i) {
+        if (!h3[i * 8 + 1]) continue;
+        fprintf(stderr, "[pk stage] %3d:", i);
+        for (int ev = 0; ev < 7; ++ev) fprintf(stderr, " %7lld", h3[i * 8 + ev] ? h3[i * 8 + ev] - c0 : -1LL);
+        fprintf(stderr, "\n");
+      }
+      cudaFree(pa.trace3);
+#endif
     }
     all_done = true;  // skip the per-product loop below
     for (void* ptr : {(void*)p1, (void*)p3, (void*)ep, (void*)d_kf, (void*)d_stopped, (void*)d_gbar, (void*)d_plan_all})
