@@ -160,6 +160,29 @@ __global__ void __launch_bounds__(kSplitThreads, 1) __cluster_dims__(kClusterCS,
     __syncthreads();
     stamp(1);
     PROF(xb + 0);
+    if (NCg == 1) {
+      // a group of ONE cluster (C1): the cluster sums are final, so the
+      // round trip through the global LL words is skipped — slice owners
+      // finalize and broadcast straight from the scattered partials
+      // (0.0 + sum: the same value the one-term cluster sum would give)
+      if (tid == 0) mbar_arrive_expect_tx(&xbar[1], (uint32_t)(ne * 8));
+      __syncthreads();
+      PROF(xb + 2);
+      const uint32_t out_base = smem_u32(s_out), bar1 = smem_u32(&xbar[1]);
+      for (int e = tid; e < nmy; e += kSplitThreads) {
+        double acc = 0.0;
+        for (int q = 0; q < CS; ++q) acc += s_in[q * sl + e];
+        acc = finalize(e0 + e, 0.0 + acc, mypre);
+        const uint32_t la = out_base + 8u * (uint32_t)(e0 + e);
+        for (int dst = 0; dst < CS; ++dst) st_async_f64(mapa_u32(la, dst), acc, mapa_u32(bar1, dst));
+      }
+      if (tid == 0) mbar_wait(&xbar[1], xpar[1]);
+      xpar[1] ^= 1u;
+      __syncthreads();
+      stamp(3);
+      PROF(xb + 3);
+      return;
+    }
     for (int e = tid; e < nmy; e += kSplitThreads) {
       double acc = 0.0;
       for (int q = 0; q < CS; ++q) acc += s_in[q * sl + e];
