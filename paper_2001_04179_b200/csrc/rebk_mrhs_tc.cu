@@ -508,7 +508,7 @@ constexpr int PK_STAGE_TRACE_N = 96;
 #endif
 __device__ __forceinline__ void pk_sstamp(const PkArgs& a, int64_t k, int cnt, int ev) {
 #ifdef PK_STAGE_TRACE
-  if (a.trace3 && blockIdx.x == 0 && k == a.trace_k0 && cnt < PK_STAGE_TRACE_N) a.trace3[cnt * 8 + ev] = clock64();
+  if (a.trace3 && blockIdx.x == 0 && k == a.trace_k0 && cnt < PK_STAGE_TRACE_N) a.trace3[cnt * 12 + ev] = clock64();
 #else
   (void)a; (void)k; (void)cnt; (void)ev;
 #endif
@@ -859,6 +859,8 @@ __global__ void __launch_bounds__(NTW, 1)
               __syncwarp();
               if (tid == 128) pk_sstamp(a, k, sc, 3);
               if (tid == 64) pk_sstamp(a, k, sc, 4);
+              if (lane == 0 && warp >= 5) pk_sstamp(a, k, sc, 3 + warp);  // 8, 9, 10: A converter warps 5, 6, 7
+              if (tid == 96) pk_sstamp(a, k, sc, 11);                     // the second B converter warp
               PK_SC_NEXT(k, sc);
               if (lane == 0) mbar_arrive(&P.conv[l]);
             }
@@ -1474,8 +1476,8 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
       TC_TRY(cudaMallocAsync((void**)&pa.trace2, sizeof(unsigned long long) * 2 * 2 * 4 * 8, stream));
       TC_TRY(cudaMemsetAsync(pa.trace2, 0, sizeof(unsigned long long) * 2 * 2 * 4 * 8, stream));
 #ifdef PK_STAGE_TRACE
-      TC_TRY(cudaMallocAsync((void**)&pa.trace3, sizeof(long long) * PK_STAGE_TRACE_N * 8, stream));
-      TC_TRY(cudaMemsetAsync(pa.trace3, 0, sizeof(long long) * PK_STAGE_TRACE_N * 8, stream));
+      TC_TRY(cudaMallocAsync((void**)&pa.trace3, sizeof(long long) * PK_STAGE_TRACE_N * 12, stream));
+      TC_TRY(cudaMemsetAsync(pa.trace3, 0, sizeof(long long) * PK_STAGE_TRACE_N * 12, stream));
 #endif
     }
     for (int64_t k0 = 1; k0 <= cfg->max_iters; k0 += CHK) {
@@ -1530,16 +1532,16 @@ int run_mrhs_tc(const MrhsRun& w, const SampleParams& sp_template, int64_t* iter
           }
       cudaFree(pa.trace2);
 #ifdef PK_STAGE_TRACE
-      std::vector<long long> h3(PK_STAGE_TRACE_N * 8);
+      std::vector<long long> h3(PK_STAGE_TRACE_N * 12);
       TC_TRY(cudaMemcpy(h3.data(), pa.trace3, h3.size() * 8, cudaMemcpyDeviceToHost));
       long long c0 = 0;
       for (int i = 0; i < PK_STAGE_TRACE_N; ++i)
-        if (h3[i * 8 + 1] && (!c0 || h3[i * 8 + 1] < c0)) c0 = h3[i * 8 + 1];
-      fprintf(stderr, "[pk stage] cycles since the first issue: free issued | A full, A stored | B done | MMA conv, committed\n");
+        if (h3[i * 12 + 1] && (!c0 || h3[i * 12 + 1] < c0)) c0 = h3[i * 12 + 1];
+      fprintf(stderr, "[pk stage] cycles since the first issue: free issued | A full, A stored (warp 4) | B done (warp 2) | MMA conv, committed | - | A stored warps 5 6 7 | B done warp 3\n");
       for (int i = 0; i < PK_STAGE_TRACE_N; ++i) {
-        if (!h3[i * 8 + 1]) continue;
+        if (!h3[i * 12 + 1]) continue;
         fprintf(stderr, "[pk stage] %3d:", i);
-        for (int ev = 0; ev < 7; ++ev) fprintf(stderr, " %7lld", h3[i * 8 + ev] ? h3[i * 8 + ev] - c0 : -1LL);
+        for (int ev = 0; ev < 12; ++ev) fprintf(stderr, " %7lld", h3[i * 12 + ev] ? h3[i * 12 + ev] - c0 : -1LL);
         fprintf(stderr, "\n");
       }
       cudaFree(pa.trace3);
