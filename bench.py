@@ -1043,7 +1043,8 @@ def main():
                     help="BASELINE config; c3 (the largest config that fits one B200) is the headline")
     ap.add_argument("--max-iters", type=int, default=50_000)
     ap.add_argument("--ref-iters", type=int, default=2000, help="iterations per CPU reference sample (c1/c2/c4)")
-    ap.add_argument("--ref-iters-c3", type=int, default=20, help="iterations per CPU reference sample (c3)")
+    ap.add_argument("--ref-iters-c3", type=int, default=100,
+                    help="iterations per CPU reference sample (c3): ~2 s of host work each at ~50 iters/s")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="c3: row-sharded path also at N = 1")

@@ -11,7 +11,10 @@ namespace rebk {
 constexpr int kThreads = 256;
 // cluster shape of the clustered dense kernels (rebk_dense_fast.cu,
 // rebk_dense_split.cu), fixed at compile time with __cluster_dims__
-constexpr int kClusterCS = 8;
+#ifndef REBK_CLUSTER_CS
+#define REBK_CLUSTER_CS 8  // measured on C2: 6 -> 84.8 ms per solve, 8 -> 84.0 (profiles/r01_split_ncc_sweep.txt)
+#endif
+constexpr int kClusterCS = REBK_CLUSTER_CS;
 constexpr int kWarps = kThreads / 32;
 // dynamic shared memory we are willing to ask for (227 KB max per CTA on B200)
 constexpr int kSmemBudget = 218 * 1024;
