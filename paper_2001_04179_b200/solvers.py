@@ -538,6 +538,72 @@ def run(problem: ProblemInstance, config: SolverConfig) -> RunTrace:
     )
 
 
+def resume(problem: ProblemInstance, config: SolverConfig, trace: RunTrace) -> RunTrace:
+    """Continue a run from the state a RunTrace carries (resume =
+    (x, z, k); the reference's SolverState (solvers.py:88-93) is resumable
+    in-process only).  `config` is the configuration of the WHOLE run
+    (same seed, partitions, stepsize; `max_iters` the total budget): the
+    device continues at iteration trace.iters + 1 with the Philox stream
+    advanced past the 2 * trace.iters uniforms already consumed, so the
+    iterates are the ones an uninterrupted run(problem, config) computes
+    (bitwise when both use the same kernel).  The returned trace counts
+    iterations from the start of the whole run.
+
+    The checks of the continued run fall on multiples of check_stride
+    counted from trace.iters, so trace.iters must be a multiple of
+    check_stride (it is whenever the first leg stopped at a check or at a
+    budget that is one)."""
+    if trace.x is None:
+        raise ValueError("resume needs a RunTrace carrying the iterates (x, z)")
+    ctx = prepare(problem, config)
+    if ctx.extended and trace.z is None:
+        raise ValueError("resume of an extended method needs the trace's z")
+    stop = config.stop
+    k0 = int(trace.iters)
+    if k0 < 0 or k0 > config.max_iters:
+        raise ValueError("trace.iters lies outside the run's iteration budget")
+    if stop.mode != "max_iters_only" and k0 % stop.check_stride != 0:
+        raise ValueError("resume needs trace.iters to be a multiple of check_stride")
+    x_star = None
+    if stop.mode == "oracle_error":
+        if problem.x_star is None:
+            raise ValueError("oracle_error stopping needs a problem with x_star")
+        x_star = np.asarray(problem.x_star, dtype=np.float64)
+    x0 = np.asarray(trace.x, dtype=np.float64)
+    z0 = np.asarray(trace.z, dtype=np.float64) if ctx.extended else None
+    if x0.shape != (ctx.a.cols,) or (z0 is not None and z0.shape != (ctx.a.rows,)):
+        raise ValueError("the trace's iterates do not match the problem's shape")
+    has_error = stop.mode != "max_iters_only"
+    record = bool(config.record_errors and has_error)
+    left = config.max_iters - k0
+    cap = (left // stop.check_stride + 2) if record else 0
+    cfg = ctx.make_cfg(
+        stop_mode=stop.mode, tol=stop.tol, stride=stop.check_stride, max_iters=left,
+        key=_lib.philox_key(config.seed), draw_offset=2 * k0, record=record,
+        residual_scale=_residual_scale(ctx) if stop.mode == "residual_proxy" else 1.0,
+    )
+    x, z, tr, errs = ctx.device_run(cfg, x0, z0, x_star, errors_cap=cap)
+    errors = checkpoints = None
+    if record:
+        nc = int(tr.n_checks)
+        errors = errs[:nc].copy()
+        checkpoints = k0 + np.minimum(np.arange(nc, dtype=np.int64) * stop.check_stride, left)
+    return RunTrace(
+        iters=k0 + int(tr.iters),
+        converged=bool(tr.converged),
+        wall_time=float(tr.loop_ms) / 1e3,
+        final_error=float(tr.final_error) if (has_error and tr.has_error) else None,
+        errors=errors,
+        checkpoints=checkpoints,
+        warnings=tuple(ctx.warnings),
+        x=x,
+        z=z,
+        grid_ctas=int(tr.grid_ctas),
+        nonfinite_at=None if int(tr.nonfinite_at) < 0 else k0 + int(tr.nonfinite_at),
+        kernel_path=int(tr.kernel_path),
+    )
+
+
 def default_partitions(a: Matrix, tau_row: int, tau_col: int | None = None):
     row = contiguous_partition(a.rows, min(tau_row, a.rows), "row")
     col = contiguous_partition(a.cols, min(tau_col or tau_row, a.cols), "col")

@@ -200,3 +200,40 @@ def test_residual_proxy_on_the_fast_kernels(monkeypatch, path_env, expect_path):
     np.testing.assert_allclose(tr.errors, ref["errors"], rtol=1e-9)
     rel = lambda u, v: np.linalg.norm(u - v) / np.linalg.norm(v)
     assert rel(tr.x, ref["x"]) <= 1e-10 and rel(tr.z, ref["z"]) <= 1e-10
+
+
+def test_resume_continues_a_run_bitwise():
+    """resume(): a run cut at a budget and continued from its RunTrace (x, z,
+    k; Philox stream advanced past the consumed draws) ends at the same
+    iteration with bitwise the same iterates as the uninterrupted run
+    (resume = (x, z, k))."""
+    import dataclasses
+    import os
+
+    from paper_2001_04179_b200.workloads import c1_matrix
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c1_golden.npz"))
+    a = c1_matrix()
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(a), b=g["b"], x_star=g["x_star"], b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    rp, cp = P.contiguous_partition(2000, 100, "row"), P.contiguous_partition(500, 100, "col")
+    cfg = P.SolverConfig(algorithm="rebk", alpha=float(g["alpha"]), seed=int(g["seed"]), max_iters=50_000,
+                         row_partition=rp, col_partition=cp, stop=P.StoppingRule(tol=float(g["tol"])),
+                         beta_max=float(g["beta"]), record_errors=True)
+    whole = P.run(prob, cfg)
+    assert whole.converged and whole.iters == int(g["iters"])
+    first = P.run(prob, dataclasses.replace(cfg, max_iters=200))
+    assert not first.converged and first.iters == 200
+    second = P.resume(prob, cfg, first)
+    assert second.converged and second.iters == whole.iters
+    assert np.array_equal(second.x, whole.x) and np.array_equal(second.z, whole.z)
+    # the error curve of the continued leg is the tail of the whole run's
+    assert int(second.checkpoints[0]) == 200 and int(second.checkpoints[-1]) == whole.iters
+    assert np.array_equal(second.errors, whole.errors[200:])
+    # a second cut, through a budget-only leg
+    leg = P.resume(prob, dataclasses.replace(cfg, max_iters=400, stop=P.StoppingRule(mode="max_iters_only")), first)
+    assert leg.iters == 400 and not leg.converged
+    third = P.resume(prob, cfg, leg)
+    assert third.iters == whole.iters and np.array_equal(third.x, whole.x) and np.array_equal(third.z, whole.z)
+    with pytest.raises(ValueError):
+        P.resume(prob, dataclasses.replace(cfg, stop=P.StoppingRule(tol=float(g["tol"]), check_stride=7)), first)

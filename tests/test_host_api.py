@@ -176,3 +176,14 @@ def test_dsbgs_joint_sampler_tables_and_picks_match_reference(case):
         lo, hi = ctx._ds_off[j], ctx._ds_off[j + 1]
         np.testing.assert_array_equal(ctx._ds_cum[lo:hi], cond.cumulative)
         np.testing.assert_array_equal(ctx._ds_alive[lo:hi], alive)
+
+
+def test_resume_needs_a_trace_with_iterates():
+    """resume() refuses a RunTrace without x before touching the device."""
+    import pytest
+
+    import paper_2001_04179_b200 as P
+
+    tr = P.RunTrace(iters=10, converged=False, wall_time=0.0, final_error=None)
+    with pytest.raises(ValueError, match="iterates"):
+        P.resume(None, None, tr)
