@@ -592,6 +592,9 @@ __device__ __forceinline__ bool pk_job(const PkArgs& a, int phase, int64_t k, in
 #ifndef PK_NA
 #define PK_NA 4
 #endif
+#ifndef PK_QB
+#define PK_QB 4  // split-K partial slices a reduction thread keeps in flight (8: 86.5 ms per C5 solve against 79.2)
+#endif
 // one raw stage: A tile, B tile, and B's lo part right behind it, so that
 // [B hi; B lo] is a single 128-row K-major operand: one N = 128 MMA
 // computes A_hi·B_hi and A_hi·B_lo into the two adjacent accumulators
@@ -1080,7 +1083,7 @@ __global__ void __launch_bounds__(NTW, 1)
               if (j4 < nJ) {
                 const int q0 = (a.ns1 * sub) / T, q1 = (a.ns1 * (sub + 1)) / T;
                 const float4* src = reinterpret_cast<const float4*>(a.part1 + (size_t)c * 256 + j4);
-                constexpr int QB = 4;
+                constexpr int QB = PK_QB;
                 for (int qb = q0; qb < q1; qb += QB) {
                   float4 v[QB];
 #pragma unroll
@@ -1144,7 +1147,7 @@ __global__ void __launch_bounds__(NTW, 1)
             if (valid) {
               const int q0 = (a.ns3 * sub) / T, q1 = (a.ns3 * (sub + 1)) / T;
               const float4* src = reinterpret_cast<const float4*>(a.part3 + (size_t)c * 256 + i4);
-              constexpr int QB = 4;
+              constexpr int QB = PK_QB;
               for (int qb = q0; qb < q1; qb += QB) {
                 float4 v[QB];
 #pragma unroll
