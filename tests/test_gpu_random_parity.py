@@ -94,3 +94,67 @@ def test_random_problem_matches_oracle(seed):
     assert rel(tr.x, ref["x"]) <= 1e-10, rel(tr.x, ref["x"])
     if ref["z"] is not None:
         assert rel(tr.z, ref["z"]) <= 1e-10, rel(tr.z, ref["z"])
+
+
+_MIDSIZE_PATHS = {}
+
+
+def draw_midsize(seed):
+    """Mid-size dense problems of the shapes the clustered kernels take (the
+    bench kernels of C1/C2: split column/row groups, fused; TMA tiles need
+    even column-block starts) and the streaming kernel: ragged last blocks,
+    row blocks of any width, strides, budgets that end between checks."""
+    g = np.random.default_rng(7000 + seed)
+    m = int(g.choice([640, 1100, 2000, 3001]))
+    n = int(g.choice([256, 500, 750, 1024]))
+    a = g.standard_normal((m, n))
+    xs = g.standard_normal(n)
+    b = a @ xs + 0.1 * g.standard_normal(m)
+    x_star = np.linalg.lstsq(a, b, rcond=None)[0]
+    tau_r = int(g.choice([37, 64, 100, 128, 250]))
+    tau_c = int(g.choice([50, 64, 100, 126]))  # even: every column block starts on an even column
+    algo = str(g.choice(["rebk", "rebk", "rebk", "rabk"]))
+    mode = str(g.choice(["oracle_error", "oracle_error", "max_iters_only", "residual_proxy"]))
+    stride = int(g.choice([1, 1, 4, 16]))
+    max_iters = int(g.choice([150, 333, 600]))
+    tol = {"oracle_error": 1e-3 * float(np.linalg.norm(x_star)), "residual_proxy": 1e-3, "max_iters_only": 1.0}[mode]
+    return dict(a=a, b=b, x_star=x_star, tau_r=tau_r, tau_c=tau_c, algo=algo, mode=mode, stride=stride,
+                max_iters=max_iters, tol=tol, alpha=float(g.uniform(0.8, 1.6)), seed=int(g.integers(0, 2**31)))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_midsize_problem_on_the_fast_kernels_matches_oracle(seed):
+    c = draw_midsize(seed)
+    m, n = c["a"].shape
+    prob = P.ProblemInstance(a=P.Matrix.from_dense(c["a"]), b=c["b"], x_star=c["x_star"], b_perp=None,
+                             meta=P.ProblemMeta(0, None, False, 0, 0.0))
+    rp = P.contiguous_partition(m, c["tau_r"], "row")
+    cp = P.contiguous_partition(n, c["tau_c"], "col") if c["algo"] == "rebk" else None
+    cfg = P.SolverConfig(algorithm=c["algo"], alpha=c["alpha"], seed=c["seed"], max_iters=c["max_iters"],
+                         row_partition=rp, col_partition=cp, record_errors=True, beta_max=1e-300,
+                         stop=P.StoppingRule(mode=c["mode"], tol=c["tol"], check_stride=c["stride"]))
+    tr = P.run(prob, cfg)
+    rb = [np.arange(i, min(i + c["tau_r"], m)) for i in range(0, m, c["tau_r"])]
+    cb = None if cp is None else [np.arange(j, min(j + c["tau_c"], n)) for j in range(0, n, c["tau_c"])]
+    orc = OracleSolver(c["a"], c["b"], rb, cb, c["alpha"], c["algo"])
+    ref = orc.run(c["seed"], c["max_iters"], c["tol"], c["x_star"], c["stride"], c["mode"], rng=NumpyRng(c["seed"]),
+                  record=True)
+    assert tr.iters == ref["iters"] and tr.converged == ref["converged"], (tr.iters, ref["iters"], tr.kernel_path)
+    if c["mode"] != "max_iters_only":
+        np.testing.assert_array_equal(tr.checkpoints, ref["checkpoints"])
+        np.testing.assert_allclose(tr.errors, ref["errors"], rtol=1e-9, atol=1e-14)
+    assert rel(tr.x, ref["x"]) <= 1e-10, (rel(tr.x, ref["x"]), tr.kernel_path)
+    if ref["z"] is not None:
+        assert rel(tr.z, ref["z"]) <= 1e-10, (rel(tr.z, ref["z"]), tr.kernel_path)
+    _MIDSIZE_PATHS[seed] = (tr.kernel_path, tr.grid_ctas, m, n, c["algo"], c["mode"])
+
+
+def test_midsize_sweep_exercises_the_fast_kernels():
+    """The sweep above is there for the bench kernels: it must have reached
+    the split kernel (path 6) and a fused / streaming one, not only the
+    general kernel (which small grids and short residual strides select)."""
+    if len(_MIDSIZE_PATHS) < 16:
+        pytest.skip("runs after the whole mid-size sweep")
+    paths = {v[0] for v in _MIDSIZE_PATHS.values()}
+    assert 6 in paths, _MIDSIZE_PATHS
+    assert paths & {1, 2, 7}, _MIDSIZE_PATHS
